@@ -1,0 +1,348 @@
+"""Schedules and the contributor-set verifier — TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Everything here is written in *logical* ranks: the straggler is sigma = n-1
+("Without loss of generality, we assume rank n-1 is the persistent straggler",
+P:200 §3.1).  Mapping to physical ranks is done in ``numerics.py``.
+
+Algorithm 1 is garbled in several places.  The readings taken here
+are SURVEY.md §8(c).3 rows 1-11 and are listed again in DESIGN.md:
+
+  (1) loop bound: r in [0, n+L-3], i.e. exactly n+L-2 rounds (Thm 1).
+  (2) the P/Q matching of line 182 runs only for r >= L.
+  (3) Phase 1 "any rank g > 2(log n - 1) without a chunk": the
+      mandated send first, then the other holders in ascending order each send
+      to the lowest-index available chunk-free non-straggler g > 2(L-1).
+  (4) critical window = [r+1, r+L] (text).
+  (5) window partner rule from the text: g in Q pairs with
+      the lowest-index available P rank outside the window, which sends
+      c_{r-L}; g in P pairs with a Q rank outside the window holding the oldest
+      active chunk c_j that g lacks with j <= g-L.
+  (6) line 178 roles: the partner sends g the chunk g lacks, g sends its own.
+  (7) Remark 1: for r >= n-1 sigma is appended to Q
+      (sorted last) and zipped with P; it sends only c_{n-2}; the send *to*
+      sigma is redundant and skipped.
+  (8) "c_{n-1}" at P:294 is a typo for c_{n-2}.
+  (9) "exactly one matching per round" is read as "at most one".
+  (10) the sigma pairing is a bidirectional exchange, both sides Reduce (P:164,
+      P:206).
+  (11) snapshot rounds: a chunk received in round r is sendable from r+1 on
+      ("c_r can only be sent ... from round r+1 onwards").
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Dict, FrozenSet, List, Optional, Tuple
+
+REDUCE = "reduce"
+REPLACE = "replace"
+
+
+@dataclass(frozen=True)
+class Transfer:
+    """One directed chunk transfer inside a round.
+
+    kind == "reduce": the receiver adds the payload into its copy
+    kind == "replace": the receiver overwrites its copy with the payload
+    """
+
+    src: int
+    dst: int
+    chunk: int
+    kind: str
+
+
+@dataclass
+class Schedule:
+    """Ordered rounds of transfers; ranks are logical."""
+
+    algorithm: str
+    n: int
+    straggler: int
+    num_chunks: int
+    rounds: List[List[Transfer]] = field(default_factory=list)
+
+    @property
+    def num_rounds(self) -> int:
+        return len(self.rounds)
+
+
+class ScheduleError(Exception):
+    pass
+
+
+def log2_exact(n: int) -> int:
+    if n < 2 or n & (n - 1):
+        raise ScheduleError(f"n={n} is not a power of two >= 2 (Alg. 1 input, P:156)")
+    return n.bit_length() - 1
+
+
+# --------------------------------------------------------------------------
+# Algorithm 1 — StragglAR schedule generator (§3.1)
+# --------------------------------------------------------------------------
+def generate_stragglar(n: int) -> Schedule:
+    """Algorithm 1 for power-of-2 n with sigma = n-1.
+
+    Returns a schedule of n + log2(n) - 2 rounds (Thm 1).  The
+    straggler pairing of round r < n-1 is a two-way Reduce of c_r.
+    """
+    L = log2_exact(n)
+    sigma = n - 1
+    R = n + L - 2                                    # reading (1)
+    # A: active chunk -> set of non-straggler holders
+    A: Dict[int, set] = {}
+    sched = Schedule("stragglar", n, sigma, n - 1)
+
+    for r in range(R):
+        avail = set(range(n - 1))                    # non-stragglers not yet matched
+        sigma_free = True
+        round_tx: List[Transfer] = []
+
+        def active_of(h: int) -> Optional[int]:
+            for c, hs in A.items():
+                if h in hs:
+                    return c
+            return None
+
+        # rank r <-> sigma exchange c_r, both fully reduce it
+        if r < n - 1:
+            round_tx.append(Transfer(r, sigma, r, REDUCE))
+            round_tx.append(Transfer(sigma, r, r, REDUCE))
+            avail.discard(r)
+            sigma_free = False
+
+        if 0 < r < L:
+            # Phase 1
+            src, dst, c = r - 1, r - 1 + L, r - 1
+            round_tx.append(Transfer(src, dst, c, REPLACE))
+            avail.discard(src)
+            avail.discard(dst)
+            receivers = {dst}
+            # reading (3): other holders, ascending, to the lowest chunk-free g > 2(L-1)
+            for h in sorted(avail):
+                ch = active_of(h)
+                if ch is None:
+                    continue
+                cands = [g for g in sorted(avail)
+                         if g > 2 * (L - 1) and active_of(g) is None and g not in receivers and g != h]
+                if not cands:
+                    raise ScheduleError(f"round {r}: no chunk-free receiver for rank {h} (contradicts Lemma 1)")
+                g = cands[0]
+                round_tx.append(Transfer(h, g, ch, REPLACE))
+                avail.discard(h)
+                avail.discard(g)
+                receivers.add(g)
+        elif r >= L:
+            # Phase 2
+            old = r - L                              # c_{r-log n}, the oldest active chunk
+            P = sorted(h for h in A.get(old, ()) if h in avail)
+            Q = sorted(h for c, hs in A.items() if c != old for h in hs if h in avail)
+            sigma_in_Q = r >= n - 1 and sigma_free   # reading (7), Remark 1
+            window = set(range(r + 1, r + L + 1))    # reading (4)
+            matched: set = set()
+
+            def exchange(p: int, q: int) -> None:
+                """p in P sends c_old to q; q sends its active chunk to p."""
+                round_tx.append(Transfer(p, q, old, REPLACE))
+                round_tx.append(Transfer(q, p, active_of(q), REPLACE))
+                matched.add(p)
+                matched.add(q)
+
+            # critical window first, reading (5)/(6)
+            for g in range(r + 1, r + L + 1):
+                if g >= n - 1 or g in matched or g not in avail:
+                    continue
+                if g in Q:
+                    partners = [p for p in P if p not in matched and p not in window]
+                    if not partners:
+                        raise ScheduleError(f"round {r}: no partner for window rank {g} in Q")
+                    exchange(partners[0], g)
+                elif g in P:
+                    found = None
+                    for j in sorted(c for c in A if c != old and c <= g - L):
+                        if g in A[j]:
+                            continue
+                        hs = [h for h in sorted(A[j]) if h in Q and h not in matched and h not in window]
+                        if hs:
+                            found = hs[0]
+                            break
+                    if found is None:
+                        raise ScheduleError(f"round {r}: no admissible partner for window rank {g} in P")
+                    exchange(g, found)
+            # line 182: zip remaining P with remaining Q (sigma last)
+            Pr = [p for p in P if p not in matched]
+            Qr = [q for q in Q if q not in matched]
+            if sigma_in_Q:
+                Qr.append(sigma)
+            if len(Pr) != len(Qr):
+                raise ScheduleError(f"round {r}: |P|={len(Pr)} != |Q|={len(Qr)} after the window")
+            for p, q in zip(Pr, Qr):
+                if q == sigma:
+                    # Remark 1: sigma sends only c_{n-2}; p -> sigma would be redundant
+                    round_tx.append(Transfer(sigma, p, n - 2, REPLACE))
+                    matched.add(p)
+                else:
+                    exchange(p, q)
+
+        sched.rounds.append(round_tx)
+
+        # bookkeeping, snapshot semantics (reading 11)
+        for t in round_tx:
+            if t.kind == REPLACE and t.chunk in A and t.dst != sigma:
+                A[t.chunk].add(t.dst)
+        if r >= L:
+            A.pop(r - L, None)                       # P:187 c_{r-log n} fully propagated
+        if r < n - 1:
+            A[r] = {r}                               # P:191 newly active chunk
+    return sched
+
+
+# --------------------------------------------------------------------------
+# Baseline: Ring; S:257 fixes the transfer pattern
+# --------------------------------------------------------------------------
+def generate_ring(n: int) -> Schedule:
+    """Ring AllReduce: n chunks, 2(n-1) rounds.
+
+    Rounds 0..n-2: rank i sends chunk (i - t) mod n to rank i+1, which adds
+    its own (Reduce).  Rounds n-1..2n-3: all-gather copies (Replace).  Ring
+    direction ascending.
+    """
+    if n < 2:
+        raise ScheduleError("ring needs n >= 2")
+    s = Schedule("ring", n, n - 1, n)
+    for t in range(n - 1):
+        s.rounds.append([Transfer(i, (i + 1) % n, (i - t) % n, REDUCE) for i in range(n)])
+    for u in range(n - 1):
+        # after RS, rank i holds the full chunk (i+1) mod n; forward what you hold
+        s.rounds.append([Transfer(i, (i + 1) % n, (i + 1 - u) % n, REPLACE) for i in range(n)])
+    return s
+
+
+# --------------------------------------------------------------------------
+# Contributor-set verifier
+# --------------------------------------------------------------------------
+State = Dict[Tuple[int, int], FrozenSet[int]]
+
+
+def initial_state_stragglar(n: int) -> State:
+    """Precondition: NS rank g holds c_g reduced over
+    all non-stragglers; every other cell holds only its own rank."""
+    sigma = n - 1
+    ns = frozenset(range(n - 1))
+    st: State = {}
+    for h in range(n):
+        for c in range(n - 1):
+            st[(h, c)] = ns if (h == c and h != sigma) else frozenset([h])
+    return st
+
+
+def initial_state_uniform(n: int, num_chunks: int) -> State:
+    """every cell holds its own rank only."""
+    return {(h, c): frozenset([h]) for h in range(n) for c in range(num_chunks)}
+
+
+@dataclass
+class Report:
+    valid: bool
+    rounds_executed: int
+    violations: List[Tuple[int, str]]
+    beta_coefficient: Fraction
+    final_state: State
+
+
+def apply_round(state: State, rnd: List[Transfer], n: int, r: int = 0,
+                violations: Optional[list] = None, matching: bool = True) -> State:
+    """snapshot semantics; Reduce = disjoint union; Replace = superset copy.
+
+    Single port: every rank sends <= 1 and receives <= 1 chunk per
+    round.  With ``matching`` (StragglAR, P:204 / S:46) every rank also talks to
+    a single partner; Ring sends to i+1 while receiving from i-1, so it is
+    checked with ``matching=False``.
+    """
+    viol = violations if violations is not None else []
+    partner: Dict[int, int] = {}
+    sends: Dict[int, int] = {}
+    recvs: Dict[int, int] = {}
+    for t in rnd:
+        if t.src == t.dst:
+            viol.append((r, f"self transfer at rank {t.src}"))
+        for a, b in ((t.src, t.dst), (t.dst, t.src)):
+            if matching and partner.setdefault(a, b) != b:
+                viol.append((r, f"port violation: rank {a} in two matchings"))
+        sends[t.src] = sends.get(t.src, 0) + 1
+        recvs[t.dst] = recvs.get(t.dst, 0) + 1
+    for k, v in list(sends.items()) + list(recvs.items()):
+        if v > 1:
+            viol.append((r, f"port violation: rank {k} moves {v} chunks one way"))
+    payload = [(t, state[(t.src, t.chunk)]) for t in rnd]   # snapshot first
+    new = dict(state)
+    for t, p in payload:
+        if not p:
+            viol.append((r, f"phantom send {t}"))
+        cur = new[(t.dst, t.chunk)]
+        if t.kind == REDUCE:
+            if cur & p:
+                viol.append((r, f"double count: {sorted(cur)} + {sorted(p)} at {t}"))
+            new[(t.dst, t.chunk)] = cur | p
+        elif t.kind == REPLACE:
+            if not p >= cur:
+                viol.append((r, f"regression: replace {sorted(cur)} by {sorted(p)} at {t}"))
+            new[(t.dst, t.chunk)] = p
+        else:
+            viol.append((r, f"unknown kind {t.kind}"))
+    return new
+
+
+def verify_schedule(s: Schedule) -> Report:
+    """replay from the algorithm's initial state; valid iff no
+    violations and every cell ends with contributors {0..n-1}."""
+    if s.algorithm == "stragglar":
+        st = initial_state_stragglar(s.n)
+    else:
+        st = initial_state_uniform(s.n, s.num_chunks)
+    viol: List[Tuple[int, str]] = []
+    beta = Fraction(0)
+    for r, rnd in enumerate(s.rounds):
+        st = apply_round(st, rnd, s.n, r, viol, matching=(s.algorithm == "stragglar"))
+        per_port: Dict[Tuple[int, str], int] = {}
+        for t in rnd:
+            per_port[(t.src, "out")] = per_port.get((t.src, "out"), 0) + 1
+            per_port[(t.dst, "in")] = per_port.get((t.dst, "in"), 0) + 1
+        beta += Fraction(max(per_port.values()) if per_port else 0, s.num_chunks)
+    full = frozenset(range(s.n))
+    for (h, c), v in st.items():
+        if v != full:
+            viol.append((len(s.rounds), f"postcondition: rank {h} chunk {c} has {sorted(v)}"))
+    return Report(not viol, len(s.rounds), viol, beta, st)
+
+
+# --------------------------------------------------------------------------
+# Holder-set trace used to state Lemma 1 / I(r) / Lemma 2 / Remark 1
+# --------------------------------------------------------------------------
+def fully_reduced_holders(s: Schedule) -> List[Dict[int, FrozenSet[int]]]:
+    """Before each round r (index r) and after the last (index R): chunk -> set of
+    ranks holding it fully reduced, obtained by replaying the verifier."""
+    st = initial_state_stragglar(s.n)
+    full = frozenset(range(s.n))
+    out = []
+
+    def snap(state: State) -> Dict[int, FrozenSet[int]]:
+        return {c: frozenset(h for h in range(s.n) if state[(h, c)] == full) for c in range(s.num_chunks)}
+
+    out.append(snap(st))
+    for r, rnd in enumerate(s.rounds):
+        st = apply_round(st, rnd, s.n, r)
+        out.append(snap(st))
+    return out
+
+
+def to_json(s: Schedule) -> dict:
+    """S:114 schedule JSON (pairs derived from transfers)."""
+    rounds = []
+    for rnd in s.rounds:
+        pairs: Dict[Tuple[int, int], list] = {}
+        for t in rnd:
+            key = (min(t.src, t.dst), max(t.src, t.dst))
+            pairs.setdefault(key, []).append({"src": t.src, "dst": t.dst, "chunks": [t.chunk], "kind": t.kind})
+        rounds.append([{"pair": list(k), "transfers": v} for k, v in sorted(pairs.items())])
+    return {"algorithm": s.algorithm, "n": s.n, "straggler": s.straggler, "num_chunks": s.num_chunks, "rounds": rounds}
