@@ -1,0 +1,162 @@
+/*
+ * stragglar.h — C ABI of libstragglar.so, a B200 (sm_100a) implementation of the
+ * StragglAR straggler-aware AllReduce (arXiv 2505.23523).
+ *
+ * Citations: P:<line> = /root/reference/PAPER.md line (section in brackets).
+ *
+ * The operation (§3.1): n ranks each hold a buffer of `count`
+ * elements; rank `straggler_rank` is the persistent straggler (§1
+ * "Assumptions"), swapped internally with logical rank n-1.
+ *   Phase A  the n-1 non-stragglers ReduceScatter among themselves while the
+ *            straggler is delayed: logical rank g ends with chunk c_g summed
+ *            over the non-stragglers (Alg. 1 "Initialization").
+ *   Phase B  the n+log2(n)-2 rounds of Algorithm 1 (Thm 1):
+ *            round r < n-1 exchanges c_r between rank r and the straggler,
+ *            both fully reduce it; every other transfer
+ *            copies an already fully reduced chunk.
+ * Postcondition: every rank holds the elementwise SUM of all n input
+ * buffers, bitwise identical on every rank.
+ *
+ * Numerics: the non-straggler sum is taken in
+ * ascending physical rank order with fp32 accumulation (int32 wraps mod 2^32);
+ * bf16 is rounded to nearest-even once after Phase A and once after adding
+ * the straggler's data.
+ *
+ * Buffer layout: one contiguous array of `count` elements, 16-byte aligned,
+ * split into n-1 chunks of Ce = roundup(ceil(count/(n-1)), 16/esize) elements
+ * (the last ones shorter or empty).  Chunk j is "owned" by logical rank j.
+ *
+ * Two communicator kinds exist in one process at a time:
+ *   - the per-process communicator (stragglar_init ...): one process per GPU,
+ *     peers' buffers and flags mapped with CUDA IPC; data moves over
+ *     NVLink/NVSwitch with device-initiated loads and stores;
+ *   - the single-device team (stragglar_team_*): all `world` logical ranks
+ *     live on the current device of this process; "peer" accesses are plain
+ *     HBM accesses.  Same kernels, same flags, same schedule.
+ *
+ * Conventions for every function:
+ *   - returns a stragglar_status_t (0 = OK) and never throws or aborts;
+ *   - collective calls must be made by every rank with the same count, dtype
+ *     and op, in the same order (like ncclAllReduce);
+ *   - asynchronous: work is enqueued on `stream` (a cudaStream_t; NULL = the
+ *     legacy default stream) and the call returns without host sync; device
+ *     faults and spin-wait timeouts surface through stragglar_check_error /
+ *     stragglar_team_check_error after a stream synchronize;
+ *   - count == 0 is a successful no-op; buf must be 16-byte aligned;
+ *   - the library owns its flags, workspace, IPC mappings and schedule tables
+ *     (released by *_finalize); the caller owns buffers and streams.
+ */
+#ifndef STRAGGLAR_H_
+#define STRAGGLAR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  STRAGGLAR_INT32 = 0,    /* wraps modulo 2^32 */
+  STRAGGLAR_FLOAT32 = 1,  /* IEEE binary32, round-to-nearest-even adds */
+  STRAGGLAR_BFLOAT16 = 2  /* fp32 accumulation, RNE rounding (see above) */
+} stragglar_dtype_t;
+
+typedef enum { STRAGGLAR_SUM = 0 } stragglar_op_t;
+
+typedef enum {
+  STRAGGLAR_OK = 0,
+  STRAGGLAR_ERR_INVALID_ARG = 1,     /* NULL/unaligned buffer, bad rank, ... */
+  STRAGGLAR_ERR_UNSUPPORTED = 2,     /* world not in {2,4,8}, unknown dtype/op */
+  STRAGGLAR_ERR_NOT_INITIALIZED = 3, /* no communicator / handles not imported */
+  STRAGGLAR_ERR_NOT_REGISTERED = 4,  /* buf not inside a registered buffer */
+  STRAGGLAR_ERR_CUDA = 5,            /* a CUDA runtime/driver call failed */
+  STRAGGLAR_ERR_TIMEOUT = 6,         /* a device spin-wait exceeded the watchdog */
+  STRAGGLAR_ERR_INTERNAL = 7
+} stragglar_status_t;
+
+/* ---- library info ------------------------------------------------------ */
+int stragglar_version(void);                       /* 100*major + minor */
+const char* stragglar_status_string(int status);   /* static string, never NULL */
+
+/* ---- schedule introspection (host only; no GPU needed) -------------------
+ * The library's own C++ implementation of Algorithm 1 in logical
+ * ranks (straggler = world-1).  stragglar_schedule_rounds returns R =
+ * world + log2(world) - 2 (Thm 1).  stragglar_schedule_round writes the
+ * transfers of round `round` as int quadruples {src, dst, chunk, kind} with
+ * kind 0 = Reduce (the straggler exchange), 1 = Replace (copy of a fully
+ * reduced chunk), into out[0 .. 4*max_transfers), and their number into
+ * *n_transfers.  Supports power-of-two world in [2, 64]. */
+int stragglar_schedule_rounds(int world, int* rounds);
+int stragglar_schedule_round(int world, int round, int* out, int max_transfers, int* n_transfers);
+
+/* ---- per-process communicator (one process per GPU) ----------------------
+ * stragglar_init(rank, world, straggler_rank): rank and straggler_rank in
+ * [0, world), world in {2,4,8}; uses the calling thread's current CUDA
+ * device; allocates the flag array and builds this rank's round table.
+ * The straggler is fixed for the communicator's lifetime. */
+int stragglar_init(int rank, int world, int straggler_rank);
+/* Size of the opaque per-rank blob that carries IPC handles. */
+int stragglar_handle_size(size_t* bytes);
+/* Writes this rank's flag-array IPC handle into blob (handle_size bytes). */
+int stragglar_export_handle(void* blob);
+/* blobs: world * handle_size bytes, rank order (exchanged by the caller, e.g.
+ * torch.distributed all_gather); opens every peer's flag array. */
+int stragglar_import_handles(const void* blobs, int world);
+/* Registers [buf, buf+bytes) (device memory of this process) for peer access
+ * and writes its IPC blob (handle_size bytes) into blob_out.  Collective in
+ * effect: every rank registers its corresponding buffer, then all ranks call
+ * stragglar_import_buffer with everyone's blobs. */
+int stragglar_register_buffer(void* buf, size_t bytes, void* blob_out);
+int stragglar_import_buffer(void* buf, const void* blobs, int world);
+/* StragglAR AllReduce in place ("similar functionality to
+ * ncclAllReduce()").  buf must lie in a registered buffer at the same offset
+ * on every rank.  Non-stragglers enqueue Phase A then Phase B; the straggler
+ * enqueues Phase B only (its delay is whatever precedes it on its stream). */
+int stragglar_allreduce(void* buf, size_t count, int dtype, int op, void* stream);
+/* Hand-written Ring AllReduce baseline on the same transport:
+ * 2(n-1) pull steps of ~count/n elements; bf16 partials rounded per hop. */
+int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* stream);
+/* Device-side barrier among all ranks of the communicator (bench start line). */
+int stragglar_barrier(void* stream);
+/* Bench only: a one-thread kernel that spins on %globaltimer for `ns`
+ * nanoseconds from its own start (the paper's idle kernel). */
+int stragglar_inject_delay(uint64_t ns, void* stream);
+/* Reads and clears the device error word (watchdog timeouts, bad arguments
+ * seen on the device).  *code = 0 if none.  Synchronizes the device. */
+int stragglar_check_error(int* code);
+int stragglar_finalize(void);
+
+/* ---- single-device team (all ranks on the current device) ---------------
+ * bufs: array of `world` device pointers (physical rank order), each 16-byte
+ * aligned with `count` elements; they must not overlap. */
+int stragglar_team_init(int world, int straggler_rank);
+int stragglar_team_allreduce(void* const* bufs, size_t count, int dtype, int op, void* stream);
+/* The two phases separately (the allreduce is exactly phase A then phase B):
+ * reduce_scatter = Phase A over the n-1 non-stragglers;
+ * complete       = Phase B over all n ranks (requires Phase A on the same
+ *                  buffers first). */
+int stragglar_team_reduce_scatter(void* const* bufs, size_t count, int dtype, int op, void* stream);
+int stragglar_team_complete(void* const* bufs, size_t count, int dtype, int op, void* stream);
+int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, int op, void* stream);
+/* Bench only: spin until `ns` nanoseconds after the start of the most
+ * recent team Phase A launch (the straggler's arrival time). */
+int stragglar_team_inject_delay(uint64_t ns, void* stream);
+/* End to end from host memory: copies host_in[p] -> bufs[p] (H2D), runs the
+ * StragglAR AllReduce, copies bufs[p] -> host_out[p] (D2H), and synchronizes
+ * `stream`.  host_in/host_out should be pinned for full PCIe bandwidth;
+ * host_out may equal host_in. */
+int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_out, void* const* bufs,
+                                  size_t count, int dtype, int op, void* stream);
+/* Slices per rank (CTAs per rank per launch) chosen at team_init. */
+int stragglar_team_slices(int* slices);
+int stragglar_team_check_error(int* code);
+int stragglar_team_finalize(void);
+
+/* Number of kernel launches the library enqueued since load (bench evidence). */
+int stragglar_launch_count(uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STRAGGLAR_H_ */

@@ -1,0 +1,591 @@
+// C ABI of libstragglar.so (declared in include/stragglar.h).
+//
+// Host side only: argument checks, the per-rank schedule programs, IPC handle
+// plumbing, flag/epoch management and kernel launches.  No data is touched on
+// the host; every step of the collective runs in kernels.cu.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <vector>
+
+#include "../../include/stragglar.h"
+#include "plan.h"
+#include "schedule.h"
+
+namespace stragglar {
+void* select_kernel(int which, int dtype, int world);
+cudaError_t launch_plan_kernel(int which, int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream);
+cudaError_t launch_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st, cudaStream_t stream);
+cudaError_t launch_barrier(const LaunchPlan& P, cudaStream_t stream);
+cudaError_t occupancy_blocks_per_sm(int which, int dtype, int world, int* blocks);
+}  // namespace stragglar
+
+using namespace stragglar;
+
+namespace {
+
+enum { K_RS = 0, K_COMPLETE = 1, K_RING = 2 };
+
+std::atomic<uint64_t> g_launches{0};
+
+struct IpcBlob {          // what travels between processes, per rank
+  cudaIpcMemHandle_t handle;
+  uint64_t offset;        // of the registered pointer inside its allocation
+  uint64_t bytes;
+};
+
+struct Registration {
+  char* local = nullptr;
+  size_t bytes = 0;
+  char* peer[kMaxWorld] = {nullptr};
+};
+
+struct Comm {
+  bool active = false;
+  bool team = false;
+  int world = 0, rank = -1, sigma = -1, device = -1;
+  int G = 0;
+  uint32_t epoch = 0;
+  uint32_t rs_epoch = 0;       // team: epoch of a Phase A awaiting its Phase B
+  bool rs_pending = false;
+  uint32_t* flags = nullptr;   // own flag array(s); team: world arrays back to back
+  uint32_t* peer_flags[kMaxWorld] = {nullptr};
+  bool imported = false;
+  DevState* state = nullptr;
+  RankPrograms progs;
+  uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
+  std::vector<Registration> regs;
+  std::vector<void*> opened;   // IPC mappings to close
+};
+
+Comm g_proc;   // per-process communicator
+Comm g_team;   // single-device team
+std::mutex g_mu;
+
+#define CK(x)                                        \
+  do {                                               \
+    cudaError_t e_ = (x);                            \
+    if (e_ != cudaSuccess) return STRAGGLAR_ERR_CUDA;\
+  } while (0)
+
+int esize_of(int dtype) {
+  switch (dtype) {
+    case STRAGGLAR_INT32:
+    case STRAGGLAR_FLOAT32: return 4;
+    case STRAGGLAR_BFLOAT16: return 2;
+    default: return 0;
+  }
+}
+
+bool pow2_world(int w) { return w == 2 || w == 4 || w == 8; }
+
+uint64_t chunk_elems(uint64_t count, int parts, int esize) {
+  const uint64_t v = 16 / esize;
+  const uint64_t per = count ? (count + parts - 1) / parts : 0;
+  return (per + v - 1) / v * v;
+}
+
+uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* s = std::getenv(name);
+  if (!s || !*s) return dflt;
+  return std::strtoull(s, nullptr, 10);
+}
+
+// Smallest occupancy over all kernels of this world size, times the SM count.
+int resident_ctas(int world, int* sm_count) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  int best = 1 << 30;
+  for (int which = 0; which < 3; ++which)
+    for (int dt = 0; dt < 3; ++dt) {
+      int b = 0;
+      if (occupancy_blocks_per_sm(which, dt, world, &b) != cudaSuccess) return -1;
+      best = b < best ? b : best;
+    }
+  if (sm_count) *sm_count = sms;
+  return best * sms;
+}
+
+int common_init(Comm& c, int world, int rank, int sigma, bool team) {
+  if (!pow2_world(world)) return STRAGGLAR_ERR_UNSUPPORTED;
+  if (sigma < 0 || sigma >= world) return STRAGGLAR_ERR_INVALID_ARG;
+  if (!team && (rank < 0 || rank >= world)) return STRAGGLAR_ERR_INVALID_ARG;
+  try {
+    c.progs = build_programs(world, sigma);
+  } catch (const std::exception&) {
+    return STRAGGLAR_ERR_INTERNAL;
+  }
+  CK(cudaGetDevice(&c.device));
+  int sms = 0;
+  const int cap = resident_ctas(world, &sms);
+  if (cap <= 0) return STRAGGLAR_ERR_CUDA;
+  int G;
+  if (team) {
+    G = cap / world;                                   // every rank's CTAs co-resident
+  } else {
+    G = (int)env_u64("STRAGGLAR_SLICES", (uint64_t)(2 * sms));
+    if (G > cap) G = cap;
+  }
+  const uint64_t forced = env_u64(team ? "STRAGGLAR_TEAM_SLICES" : "STRAGGLAR_SLICES_FORCE", 0);
+  if (forced) G = (int)forced;
+  if (G > kMaxSlices) G = kMaxSlices;
+  if (G < 1 || (team && G * world > cap)) return STRAGGLAR_ERR_UNSUPPORTED;
+  c.G = G;
+  c.world = world;
+  c.rank = team ? -1 : rank;
+  c.sigma = sigma;
+  c.team = team;
+  c.epoch = 0;
+  c.rs_pending = false;
+  c.timeout_ns = env_u64("STRAGGLAR_TIMEOUT_MS", 10000) * 1000000ull;
+  const size_t per_rank = (size_t)kSlots * G * sizeof(uint32_t);
+  const size_t nbytes = team ? per_rank * world : per_rank;
+  CK(cudaMalloc(&c.flags, nbytes));
+  CK(cudaMemset(c.flags, 0, nbytes));
+  CK(cudaMalloc(&c.state, sizeof(DevState)));
+  CK(cudaMemset(c.state, 0, sizeof(DevState)));
+  CK(cudaDeviceSynchronize());
+  for (int p = 0; p < kMaxWorld; ++p) c.peer_flags[p] = nullptr;
+  if (team) {
+    for (int p = 0; p < world; ++p) c.peer_flags[p] = c.flags + (size_t)p * kSlots * G;
+    c.imported = true;
+  } else {
+    c.peer_flags[rank] = c.flags;
+    c.imported = (world == 1);
+  }
+  c.active = true;
+  return STRAGGLAR_OK;
+}
+
+void common_finalize(Comm& c) {
+  if (!c.active) return;
+  cudaDeviceSynchronize();
+  for (void* p : c.opened) cudaIpcCloseMemHandle(p);
+  c.opened.clear();
+  c.regs.clear();
+  if (c.flags) cudaFree(c.flags);
+  if (c.state) cudaFree(c.state);
+  c = Comm();
+}
+
+LaunchPlan base_plan(const Comm& c, size_t count, int dtype, uint32_t epoch) {
+  LaunchPlan P;
+  std::memset(&P, 0, sizeof(P));
+  P.world = c.world;
+  P.sigma = c.sigma;
+  P.G = c.G;
+  P.epoch = epoch;
+  P.count = count;
+  P.esize = esize_of(dtype);
+  P.ce = chunk_elems(count, c.world - 1, P.esize);
+  P.nchunks = c.world - 1;
+  P.timeout_ns = c.timeout_ns;
+  P.state = c.state;
+  for (int p = 0; p < c.world; ++p) {
+    P.flags[p] = c.peer_flags[p];
+    P.logical_of_phys[p] = c.progs.logical_of_phys[p];
+    P.nops[p] = c.progs.nops[p];
+    for (int k = 0; k < c.progs.nops[p]; ++k) P.ops[p][k] = c.progs.ops[p][k];
+  }
+  return P;
+}
+
+int check_args(const void* buf, size_t count, int dtype, int op) {
+  if (op != STRAGGLAR_SUM) return STRAGGLAR_ERR_UNSUPPORTED;
+  if (!esize_of(dtype)) return STRAGGLAR_ERR_UNSUPPORTED;
+  if (count == 0) return STRAGGLAR_OK;
+  if (!buf) return STRAGGLAR_ERR_INVALID_ARG;
+  if (reinterpret_cast<uintptr_t>(buf) % 16) return STRAGGLAR_ERR_INVALID_ARG;
+  return STRAGGLAR_OK;
+}
+
+int team_check(void* const* bufs, size_t count, int dtype, int op) {
+  if (!g_team.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (op != STRAGGLAR_SUM || !esize_of(dtype)) return STRAGGLAR_ERR_UNSUPPORTED;
+  if (count == 0) return STRAGGLAR_OK;
+  if (!bufs) return STRAGGLAR_ERR_INVALID_ARG;
+  for (int p = 0; p < g_team.world; ++p) {
+    int st = check_args(bufs[p], count, dtype, op);
+    if (st) return st;
+  }
+  return STRAGGLAR_OK;
+}
+
+int launch(int which, int dtype, const LaunchPlan& P, int nblocks, void* stream) {
+  cudaError_t e = launch_plan_kernel(which, dtype, P, nblocks, (cudaStream_t)stream);
+  if (e != cudaSuccess) return STRAGGLAR_ERR_CUDA;
+  g_launches.fetch_add(1);
+  return STRAGGLAR_OK;
+}
+
+// team: Phase A over the non-stragglers (all in one launch)
+int team_rs(void* const* bufs, size_t count, int dtype, void* stream, uint32_t epoch) {
+  Comm& c = g_team;
+  LaunchPlan P = base_plan(c, count, dtype, epoch);
+  for (int p = 0; p < c.world; ++p) P.buf[p] = (char*)bufs[p];
+  int k = 0;
+  for (int p = 0; p < c.world; ++p)
+    if (p != c.sigma) P.local_rank[k++] = p;
+  P.nlocal = k;
+  return launch(K_RS, dtype, P, k * c.G, stream);
+}
+
+int team_b(void* const* bufs, size_t count, int dtype, void* stream, uint32_t epoch) {
+  Comm& c = g_team;
+  LaunchPlan P = base_plan(c, count, dtype, epoch);
+  for (int p = 0; p < c.world; ++p) {
+    P.buf[p] = (char*)bufs[p];
+    P.local_rank[p] = p;
+  }
+  P.nlocal = c.world;
+  return launch(K_COMPLETE, dtype, P, c.world * c.G, stream);
+}
+
+int read_error(Comm& c, int* code) {
+  if (!code) return STRAGGLAR_ERR_INVALID_ARG;
+  if (!c.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  CK(cudaDeviceSynchronize());
+  DevState h;
+  CK(cudaMemcpy(&h, c.state, sizeof(h), cudaMemcpyDeviceToHost));
+  *code = (int)h.err;
+  if (h.err) {
+    uint32_t z[2] = {0, 0};
+    CK(cudaMemcpy(c.state, z, sizeof(z), cudaMemcpyHostToDevice));
+  }
+  return h.err == ERR_TIMEOUT ? STRAGGLAR_ERR_TIMEOUT : STRAGGLAR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int stragglar_version(void) { return 100; }
+
+const char* stragglar_status_string(int s) {
+  switch (s) {
+    case STRAGGLAR_OK: return "ok";
+    case STRAGGLAR_ERR_INVALID_ARG: return "invalid argument";
+    case STRAGGLAR_ERR_UNSUPPORTED: return "unsupported (world must be 2, 4 or 8; dtype int32/float32/bfloat16; op SUM)";
+    case STRAGGLAR_ERR_NOT_INITIALIZED: return "communicator not initialized (or peer handles not imported)";
+    case STRAGGLAR_ERR_NOT_REGISTERED: return "buffer is not inside a registered, peer-mapped allocation";
+    case STRAGGLAR_ERR_CUDA: return "CUDA error";
+    case STRAGGLAR_ERR_TIMEOUT: return "device spin-wait timed out (a peer never arrived)";
+    case STRAGGLAR_ERR_INTERNAL: return "internal error";
+    default: return "unknown status";
+  }
+}
+
+int stragglar_launch_count(uint64_t* n) {
+  if (!n) return STRAGGLAR_ERR_INVALID_ARG;
+  *n = g_launches.load();
+  return STRAGGLAR_OK;
+}
+
+// ---------------------------------------------------------------- schedule
+int stragglar_schedule_rounds(int world, int* rounds) {
+  if (!rounds) return STRAGGLAR_ERR_INVALID_ARG;
+  try {
+    *rounds = (int)generate_schedule(world).size();
+  } catch (const std::exception&) {
+    return STRAGGLAR_ERR_UNSUPPORTED;
+  }
+  return STRAGGLAR_OK;
+}
+
+int stragglar_schedule_round(int world, int round, int* out, int max_transfers, int* n_transfers) {
+  if (!n_transfers || (!out && max_transfers > 0)) return STRAGGLAR_ERR_INVALID_ARG;
+  try {
+    auto s = generate_schedule(world);
+    if (round < 0 || round >= (int)s.size()) return STRAGGLAR_ERR_INVALID_ARG;
+    const auto& rd = s[round];
+    *n_transfers = (int)rd.size();
+    if ((int)rd.size() > max_transfers) return STRAGGLAR_ERR_INVALID_ARG;
+    for (size_t i = 0; i < rd.size(); ++i) {
+      out[4 * i + 0] = rd[i].src;
+      out[4 * i + 1] = rd[i].dst;
+      out[4 * i + 2] = rd[i].chunk;
+      out[4 * i + 3] = rd[i].reduce ? 0 : 1;
+    }
+  } catch (const std::exception&) {
+    return STRAGGLAR_ERR_UNSUPPORTED;
+  }
+  return STRAGGLAR_OK;
+}
+
+// ---------------------------------------------------------------- per-process communicator
+int stragglar_init(int rank, int world, int straggler_rank) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_proc.active) common_finalize(g_proc);
+  return common_init(g_proc, world, rank, straggler_rank, false);
+}
+
+int stragglar_handle_size(size_t* bytes) {
+  if (!bytes) return STRAGGLAR_ERR_INVALID_ARG;
+  *bytes = sizeof(IpcBlob);
+  return STRAGGLAR_OK;
+}
+
+int stragglar_export_handle(void* blob) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_proc.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (!blob) return STRAGGLAR_ERR_INVALID_ARG;
+  IpcBlob b;
+  std::memset(&b, 0, sizeof(b));
+  CK(cudaIpcGetMemHandle(&b.handle, g_proc.flags));
+  b.offset = 0;
+  b.bytes = (uint64_t)kSlots * g_proc.G * sizeof(uint32_t);
+  std::memcpy(blob, &b, sizeof(b));
+  return STRAGGLAR_OK;
+}
+
+int stragglar_import_handles(const void* blobs, int world) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  if (!c.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (!blobs || world != c.world) return STRAGGLAR_ERR_INVALID_ARG;
+  const IpcBlob* b = static_cast<const IpcBlob*>(blobs);
+  for (int p = 0; p < world; ++p) {
+    if (p == c.rank) continue;
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, b[p].handle, cudaIpcMemLazyEnablePeerAccess));
+    c.opened.push_back(ptr);
+    c.peer_flags[p] = reinterpret_cast<uint32_t*>(static_cast<char*>(ptr) + b[p].offset);
+  }
+  c.imported = true;
+  return STRAGGLAR_OK;
+}
+
+int stragglar_register_buffer(void* buf, size_t bytes, void* blob_out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_proc.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (!buf || !bytes || !blob_out) return STRAGGLAR_ERR_INVALID_ARG;
+  // driver entry point through the runtime: the library does not link libcuda
+  typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange get_range = nullptr;
+  if (!get_range) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return STRAGGLAR_ERR_CUDA;
+    get_range = reinterpret_cast<GetRange>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, (CUdeviceptr)buf) != CUDA_SUCCESS) return STRAGGLAR_ERR_CUDA;
+  if ((CUdeviceptr)buf + bytes > base + size) return STRAGGLAR_ERR_INVALID_ARG;
+  IpcBlob b;
+  std::memset(&b, 0, sizeof(b));
+  CK(cudaIpcGetMemHandle(&b.handle, (void*)base));
+  b.offset = (uint64_t)((CUdeviceptr)buf - base);
+  b.bytes = bytes;
+  std::memcpy(blob_out, &b, sizeof(b));
+  return STRAGGLAR_OK;
+}
+
+int stragglar_import_buffer(void* buf, const void* blobs, int world) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  if (!c.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (!buf || !blobs || world != c.world) return STRAGGLAR_ERR_INVALID_ARG;
+  const IpcBlob* b = static_cast<const IpcBlob*>(blobs);
+  Registration r;
+  r.local = static_cast<char*>(buf);
+  r.bytes = b[c.rank].bytes;
+  for (int p = 0; p < world; ++p) {
+    if (p == c.rank) {
+      r.peer[p] = r.local;
+      continue;
+    }
+    if (b[p].bytes != r.bytes) return STRAGGLAR_ERR_INVALID_ARG;
+    void* ptr = nullptr;
+    CK(cudaIpcOpenMemHandle(&ptr, b[p].handle, cudaIpcMemLazyEnablePeerAccess));
+    c.opened.push_back(ptr);
+    r.peer[p] = static_cast<char*>(ptr) + b[p].offset;
+  }
+  c.regs.push_back(r);
+  return STRAGGLAR_OK;
+}
+
+static int proc_plan(void* buf, size_t count, int dtype, LaunchPlan* P, uint32_t epoch) {
+  Comm& c = g_proc;
+  const size_t bytes = count * esize_of(dtype);
+  const Registration* reg = nullptr;
+  for (const auto& r : c.regs)
+    if ((char*)buf >= r.local && (char*)buf + bytes <= r.local + r.bytes) reg = &r;
+  if (!reg) return STRAGGLAR_ERR_NOT_REGISTERED;
+  const size_t delta = (char*)buf - reg->local;
+  *P = base_plan(c, count, dtype, epoch);
+  for (int p = 0; p < c.world; ++p) P->buf[p] = reg->peer[p] + delta;
+  P->nlocal = 1;
+  P->local_rank[0] = c.rank;
+  return STRAGGLAR_OK;
+}
+
+int stragglar_allreduce(void* buf, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  int st = check_args(buf, count, dtype, op);
+  if (st || count == 0) return st;
+  LaunchPlan P;
+  if ((st = proc_plan(buf, count, dtype, &P, c.epoch + 1))) return st;
+  ++c.epoch;
+  if (c.rank != c.sigma)
+    if ((st = launch(K_RS, dtype, P, c.G, stream))) return st;
+  return launch(K_COMPLETE, dtype, P, c.G, stream);
+}
+
+int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  int st = check_args(buf, count, dtype, op);
+  if (st || count == 0) return st;
+  LaunchPlan P;
+  if ((st = proc_plan(buf, count, dtype, &P, c.epoch + 1))) return st;
+  ++c.epoch;
+  P.ce = chunk_elems(count, c.world, P.esize);
+  P.nchunks = c.world;
+  return launch(K_RING, dtype, P, c.G, stream);
+}
+
+int stragglar_barrier(void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  LaunchPlan P = base_plan(c, 0, STRAGGLAR_INT32, ++c.epoch);
+  P.nlocal = 1;
+  P.local_rank[0] = c.rank;
+  if (launch_barrier(P, (cudaStream_t)stream) != cudaSuccess) return STRAGGLAR_ERR_CUDA;
+  g_launches.fetch_add(1);
+  return STRAGGLAR_OK;
+}
+
+int stragglar_inject_delay(uint64_t ns, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_proc.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (launch_delay(nullptr, ns, g_proc.state, (cudaStream_t)stream) != cudaSuccess) return STRAGGLAR_ERR_CUDA;
+  g_launches.fetch_add(1);
+  return STRAGGLAR_OK;
+}
+
+int stragglar_check_error(int* code) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return read_error(g_proc, code);
+}
+
+int stragglar_finalize(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  common_finalize(g_proc);
+  return STRAGGLAR_OK;
+}
+
+// ---------------------------------------------------------------- team
+int stragglar_team_init(int world, int straggler_rank) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_team.active) common_finalize(g_team);
+  return common_init(g_team, world, -1, straggler_rank, true);
+}
+
+int stragglar_team_slices(int* slices) {
+  if (!slices) return STRAGGLAR_ERR_INVALID_ARG;
+  if (!g_team.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  *slices = g_team.G;
+  return STRAGGLAR_OK;
+}
+
+int stragglar_team_reduce_scatter(void* const* bufs, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int st = team_check(bufs, count, dtype, op);
+  if (st || count == 0) return st;
+  const uint32_t ep = ++g_team.epoch;
+  if ((st = team_rs(bufs, count, dtype, stream, ep))) return st;
+  g_team.rs_epoch = ep;
+  g_team.rs_pending = true;
+  return STRAGGLAR_OK;
+}
+
+int stragglar_team_complete(void* const* bufs, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int st = team_check(bufs, count, dtype, op);
+  if (st || count == 0) return st;
+  if (!g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;   // Phase B needs its Phase A
+  g_team.rs_pending = false;
+  return team_b(bufs, count, dtype, stream, g_team.rs_epoch);
+}
+
+int stragglar_team_allreduce(void* const* bufs, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int st = team_check(bufs, count, dtype, op);
+  if (st || count == 0) return st;
+  const uint32_t ep = ++g_team.epoch;
+  g_team.rs_pending = false;
+  if ((st = team_rs(bufs, count, dtype, stream, ep))) return st;
+  return team_b(bufs, count, dtype, stream, ep);
+}
+
+int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int st = team_check(bufs, count, dtype, op);
+  if (st || count == 0) return st;
+  Comm& c = g_team;
+  LaunchPlan P = base_plan(c, count, dtype, ++c.epoch);
+  P.ce = chunk_elems(count, c.world, P.esize);
+  P.nchunks = c.world;
+  for (int p = 0; p < c.world; ++p) {
+    P.buf[p] = (char*)bufs[p];
+    P.local_rank[p] = p;
+  }
+  P.nlocal = c.world;
+  return launch(K_RING, dtype, P, c.world * c.G, stream);
+}
+
+int stragglar_team_inject_delay(uint64_t ns, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_team.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (launch_delay(&g_team.state->t_rs_start, ns, g_team.state, (cudaStream_t)stream) != cudaSuccess)
+    return STRAGGLAR_ERR_CUDA;
+  g_launches.fetch_add(1);
+  return STRAGGLAR_OK;
+}
+
+int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_out, void* const* bufs,
+                                  size_t count, int dtype, int op, void* stream) {
+  if (!host_in || !host_out) return STRAGGLAR_ERR_INVALID_ARG;
+  int st;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if ((st = team_check(bufs, count, dtype, op))) return st;
+  }
+  if (count == 0) return STRAGGLAR_OK;
+  const size_t bytes = count * esize_of(dtype);
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int p = 0; p < g_team.world; ++p) {
+    if (!host_in[p] || !host_out[p]) return STRAGGLAR_ERR_INVALID_ARG;
+    CK(cudaMemcpyAsync(bufs[p], host_in[p], bytes, cudaMemcpyHostToDevice, s));
+  }
+  if ((st = stragglar_team_allreduce(bufs, count, dtype, op, stream))) return st;
+  for (int p = 0; p < g_team.world; ++p) CK(cudaMemcpyAsync(host_out[p], bufs[p], bytes, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return STRAGGLAR_OK;
+}
+
+int stragglar_team_check_error(int* code) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return read_error(g_team, code);
+}
+
+int stragglar_team_finalize(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  common_finalize(g_team);
+  return STRAGGLAR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,120 @@
+// Device primitives for the StragglAR kernels (sm_100a): 16-byte vector moves,
+// dtype-specific adds, and cross-GPU flag signalling with release/acquire at
+// system scope (valid for NVLink peer memory mapped through CUDA IPC and for
+// same-device "team" ranks alike).
+#pragma once
+#include <cuda_bf16.h>
+#include <cstdint>
+
+namespace stragglar {
+
+enum DType : int { DT_I32 = 0, DT_F32 = 1, DT_BF16 = 2 };
+
+// ---------------------------------------------------------------- memory ops
+__device__ __forceinline__ uint4 ld_vec(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_vec(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("fence.acq_rel.sys;\n\tst.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---------------------------------------------------------------- arithmetic
+__device__ __forceinline__ float bf_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float bf_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+__device__ __forceinline__ uint32_t pack_bf16_rn(float lo, float hi) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);  // .x (low 16 bits) = lo
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int DT>
+__device__ __forceinline__ uint32_t add_word(uint32_t a, uint32_t b) {
+  if constexpr (DT == DT_I32) {
+    return a + b;  // two's-complement wrap
+  } else if constexpr (DT == DT_F32) {
+    return __float_as_uint(__fadd_rn(__uint_as_float(a), __uint_as_float(b)));
+  } else {
+    return pack_bf16_rn(__fadd_rn(bf_lo(a), bf_lo(b)), __fadd_rn(bf_hi(a), bf_hi(b)));
+  }
+}
+template <int DT>
+__device__ __forceinline__ uint4 add_vec(const uint4& a, const uint4& b) {
+  return make_uint4(add_word<DT>(a.x, b.x), add_word<DT>(a.y, b.y), add_word<DT>(a.z, b.z), add_word<DT>(a.w, b.w));
+}
+
+// Accumulator for the Phase-A reduction: fp32 lanes for float types, u32 for int.
+template <int DT>
+struct Acc {
+  static constexpr int kLanes = (DT == DT_BF16) ? 8 : 4;
+  uint32_t u[4];
+  float f[8];
+  __device__ __forceinline__ void init(const uint4& v) {
+    if constexpr (DT == DT_I32) {
+      u[0] = v.x; u[1] = v.y; u[2] = v.z; u[3] = v.w;
+    } else if constexpr (DT == DT_F32) {
+      f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y);
+      f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
+    } else {
+      f[0] = bf_lo(v.x); f[1] = bf_hi(v.x); f[2] = bf_lo(v.y); f[3] = bf_hi(v.y);
+      f[4] = bf_lo(v.z); f[5] = bf_hi(v.z); f[6] = bf_lo(v.w); f[7] = bf_hi(v.w);
+    }
+  }
+  __device__ __forceinline__ void add(const uint4& v) {
+    if constexpr (DT == DT_I32) {
+      u[0] += v.x; u[1] += v.y; u[2] += v.z; u[3] += v.w;
+    } else if constexpr (DT == DT_F32) {
+      f[0] = __fadd_rn(f[0], __uint_as_float(v.x)); f[1] = __fadd_rn(f[1], __uint_as_float(v.y));
+      f[2] = __fadd_rn(f[2], __uint_as_float(v.z)); f[3] = __fadd_rn(f[3], __uint_as_float(v.w));
+    } else {
+      f[0] = __fadd_rn(f[0], bf_lo(v.x)); f[1] = __fadd_rn(f[1], bf_hi(v.x));
+      f[2] = __fadd_rn(f[2], bf_lo(v.y)); f[3] = __fadd_rn(f[3], bf_hi(v.y));
+      f[4] = __fadd_rn(f[4], bf_lo(v.z)); f[5] = __fadd_rn(f[5], bf_hi(v.z));
+      f[6] = __fadd_rn(f[6], bf_lo(v.w)); f[7] = __fadd_rn(f[7], bf_hi(v.w));
+    }
+  }
+  __device__ __forceinline__ uint4 get() const {
+    if constexpr (DT == DT_I32) {
+      return make_uint4(u[0], u[1], u[2], u[3]);
+    } else if constexpr (DT == DT_F32) {
+      return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]), __float_as_uint(f[3]));
+    } else {
+      return make_uint4(pack_bf16_rn(f[0], f[1]), pack_bf16_rn(f[2], f[3]), pack_bf16_rn(f[4], f[5]),
+                        pack_bf16_rn(f[6], f[7]));
+    }
+  }
+};
+
+// Scalar versions for the (< 16 byte) tail of the buffer.
+template <int DT>
+__device__ __forceinline__ void scalar_add_store(void* dst0, void* dst1, const void* a, const void* b) {
+  if constexpr (DT == DT_BF16) {
+    float s = __fadd_rn(__uint_as_float(uint32_t(*(const volatile uint16_t*)a) << 16),
+                        __uint_as_float(uint32_t(*(const volatile uint16_t*)b) << 16));
+    __nv_bfloat16 h = __float2bfloat16_rn(s);
+    uint16_t bits = *reinterpret_cast<uint16_t*>(&h);
+    *(volatile uint16_t*)dst0 = bits;
+    if (dst1) *(volatile uint16_t*)dst1 = bits;
+  } else {
+    uint32_t v = add_word<DT>(*(const volatile uint32_t*)a, *(const volatile uint32_t*)b);
+    *(volatile uint32_t*)dst0 = v;
+    if (dst1) *(volatile uint32_t*)dst1 = v;
+  }
+}
+
+}  // namespace stragglar

@@ -1,0 +1,404 @@
+// StragglAR kernels for sm_100a.
+//
+//   k_reduce_scatter  Phase A: owner g pulls its chunk
+//                     from the n-2 other non-stragglers, sums in canonical
+//                     order (ascending physical rank, fp32 accumulation) and
+//                     stores in place.  Replaces ncclReduceScatter.
+//   k_complete        Phase B (Algorithm 1): a persistent round
+//                     executor.  Each CTA owns one slice of every chunk and
+//                     walks its rank's op list in round order.  The straggler
+//                     exchange is fused with its reduction (P:347
+//                     "separate kernels for reduction" become one pass).
+//   k_ring            hand-written Ring baseline, pull-based.
+//   k_delay           the paper's idle kernel on %globaltimer.
+//   k_barrier         device barrier among ranks (bench start line).
+//
+// One launch serves `nlocal` ranks: 1 in the per-process (NVLink) mode, all
+// of them in the single-device team mode (block b works for local rank b/G,
+// slice b%G).  All CTAs of a launch must be co-resident (cooperative launch),
+// because they spin on flags produced by CTAs of other ranks.
+#include <cooperative_groups.h>
+
+#include "device.cuh"
+#include "plan.h"
+
+namespace stragglar {
+
+// ---------------------------------------------------------------- flags
+__device__ __forceinline__ bool flag_ok(uint32_t v, uint32_t epoch) { return int32_t(v - epoch) >= 0; }
+
+// Spin (one thread) until *f >= epoch.  Bounded by the watchdog; gives up
+// early if another CTA of this process already reported an error.
+__device__ bool spin_wait(const uint32_t* f, uint32_t epoch, const LaunchPlan& P, uint32_t where) {
+  if (flag_ok(ld_acquire_sys(f), epoch)) return true;
+  const uint64_t t0 = globaltimer();
+  for (uint32_t it = 1;; ++it) {
+    if (flag_ok(ld_acquire_sys(f), epoch)) return true;
+    if (it > 64) __nanosleep(40);
+    if ((it & 127) == 0) {
+      if (*(volatile uint32_t*)&P.state->err) return false;
+      if (globaltimer() - t0 > P.timeout_ns) {
+        if (atomicCAS(&P.state->err, 0u, (uint32_t)ERR_TIMEOUT) == 0u) atomicExch(&P.state->err_info, where);
+        return false;
+      }
+    }
+  }
+}
+
+// Whole-CTA wait: thread 0 spins, the barrier publishes the acquired state.
+__device__ __forceinline__ bool cta_wait(const uint32_t* f, uint32_t epoch, const LaunchPlan& P, uint32_t where) {
+  int ok = 1;
+  if (threadIdx.x == 0) ok = spin_wait(f, epoch, P, where);
+  return __syncthreads_and(ok);
+}
+
+// Whole-CTA signal: all prior stores of the CTA happen-before the flag store.
+__device__ __forceinline__ void cta_signal(uint32_t* f, uint32_t epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) st_release_sys(f, epoch);
+}
+
+__device__ __forceinline__ uint32_t* flag_at(uint32_t* base, int slot, int G, int s) {
+  return base + (size_t)slot * G + s;
+}
+
+// ---------------------------------------------------------------- ranges
+struct Range {
+  uint64_t lo, hi;  // elements
+};
+
+// Slice s of [clo, chi): an even split of the 16-byte vectors; identical on
+// every rank (it depends only on count, world and G).
+__device__ __forceinline__ Range slice_of(uint64_t clo, uint64_t chi, int s, int G, int V) {
+  const uint64_t nv = (chi - clo + V - 1) / V;
+  const uint64_t a = nv * (uint64_t)s / G, b = nv * (uint64_t)(s + 1) / G;
+  Range r;
+  r.lo = clo + a * V;
+  r.hi = clo + b * V < chi ? clo + b * V : chi;
+  if (r.lo > r.hi) r.lo = r.hi;
+  return r;
+}
+
+__device__ __forceinline__ Range chunk_range(const LaunchPlan& P, int c) {
+  uint64_t lo = (uint64_t)c * P.ce, hi = lo + P.ce;
+  if (lo > P.count) lo = P.count;
+  if (hi > P.count) hi = P.count;
+  return {lo, hi};
+}
+
+// ---------------------------------------------------------------- data movers
+constexpr int kUnroll = 4;
+constexpr int kMinBlocks = 4;  // <= 64 registers: 4 CTAs of 256 threads per SM
+
+// dst <- src for 16-byte vectors [0, nv)
+__device__ __forceinline__ void copy_vecs(char* __restrict__ dst, const char* __restrict__ src, uint64_t nv) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  uint64_t i = threadIdx.x;
+  const uint64_t step = (uint64_t)kUnroll * blockDim.x;
+  for (; i + (kUnroll - 1) * blockDim.x < nv; i += step) {
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) v[u] = ld_vec(s + i + u * blockDim.x);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) st_vec(d + i + u * blockDim.x, v[u]);
+  }
+  for (; i < nv; i += blockDim.x) st_vec(d + i, ld_vec(s + i));
+}
+
+// d0 = d1 = a (+) b for 16-byte vectors [0, nv)  (fused exchange-reduce)
+template <int DT>
+__device__ __forceinline__ void add2_vecs(char* d0, char* d1, const char* a, const char* b, uint64_t nv) {
+  const uint4* pa = reinterpret_cast<const uint4*>(a);
+  const uint4* pb = reinterpret_cast<const uint4*>(b);
+  uint4* q0 = reinterpret_cast<uint4*>(d0);
+  uint4* q1 = reinterpret_cast<uint4*>(d1);
+  uint64_t i = threadIdx.x;
+  constexpr int U = 2;
+  const uint64_t step = (uint64_t)U * blockDim.x;
+  for (; i + (U - 1) * blockDim.x < nv; i += step) {
+    uint4 va[U], vb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      va[u] = ld_vec(pa + i + u * blockDim.x);
+      vb[u] = ld_vec(pb + i + u * blockDim.x);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint4 z = add_vec<DT>(va[u], vb[u]);
+      st_vec(q0 + i + u * blockDim.x, z);
+      if (q1) st_vec(q1 + i + u * blockDim.x, z);
+    }
+  }
+  for (; i < nv; i += blockDim.x) {
+    uint4 z = add_vec<DT>(ld_vec(pa + i), ld_vec(pb + i));
+    st_vec(q0 + i, z);
+    if (q1) st_vec(q1 + i, z);
+  }
+}
+
+// elementwise tail (< 16 bytes) of an add2
+template <int DT>
+__device__ __forceinline__ void add2_tail(char* d0, char* d1, const char* a, const char* b, int nelem, int esz) {
+  if ((int)threadIdx.x < nelem) {
+    const int o = threadIdx.x * esz;
+    scalar_add_store<DT>(d0 + o, d1 ? d1 + o : nullptr, a + o, b + o);
+  }
+}
+
+__device__ __forceinline__ void copy_tail(char* dst, const char* src, int nbytes) {
+  if ((int)threadIdx.x < nbytes) dst[threadIdx.x] = *(const volatile char*)(src + threadIdx.x);
+}
+
+// ---------------------------------------------------------------- Phase A
+// Canonical sum of the slice over the non-stragglers in ascending physical order.
+template <int DT, int W>
+__device__ void rs_slice(const LaunchPlan& P, const char* const (&src)[W - 1], char* dst, uint64_t lo_b, uint64_t hi_b) {
+  const uint64_t nv = (hi_b - lo_b) / 16;
+  constexpr int U = (W <= 4) ? 4 : 2;
+  uint64_t i = threadIdx.x;
+  const uint64_t step = (uint64_t)U * blockDim.x;
+  for (; i + (U - 1) * blockDim.x < nv; i += step) {
+    uint4 v[U][W - 1];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < W - 1; ++j) v[u][j] = ld_vec(src[j] + lo_b + (i + u * blockDim.x) * 16);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      Acc<DT> acc;
+      acc.init(v[u][0]);
+#pragma unroll
+      for (int j = 1; j < W - 1; ++j) acc.add(v[u][j]);
+      st_vec(dst + lo_b + (i + u * blockDim.x) * 16, acc.get());
+    }
+  }
+  for (; i < nv; i += blockDim.x) {
+    Acc<DT> acc;
+    acc.init(ld_vec(src[0] + lo_b + i * 16));
+#pragma unroll
+    for (int j = 1; j < W - 1; ++j) acc.add(ld_vec(src[j] + lo_b + i * 16));
+    st_vec(dst + lo_b + i * 16, acc.get());
+  }
+  // tail: fewer than 16 bytes at the very end of the buffer
+  const int tail = (int)((hi_b - lo_b) % 16) / P.esize;
+  if ((int)threadIdx.x < tail) {
+    const uint64_t o = lo_b + nv * 16 + threadIdx.x * P.esize;
+    if constexpr (DT == DT_BF16) {
+      float a = 0.f;
+#pragma unroll
+      for (int j = 0; j < W - 1; ++j) {
+        float x = __uint_as_float(uint32_t(*(const volatile uint16_t*)(src[j] + o)) << 16);
+        a = (j == 0) ? x : __fadd_rn(a, x);
+      }
+      __nv_bfloat16 h = __float2bfloat16_rn(a);
+      *(volatile uint16_t*)(dst + o) = *reinterpret_cast<uint16_t*>(&h);
+    } else {
+      uint32_t a = *(const volatile uint32_t*)(src[0] + o);
+#pragma unroll
+      for (int j = 1; j < W - 1; ++j) a = add_word<DT>(a, *(const volatile uint32_t*)(src[j] + o));
+      *(volatile uint32_t*)(dst + o) = a;
+    }
+  }
+}
+
+template <int DT, int W>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_reduce_scatter(const __grid_constant__ LaunchPlan P) {
+  const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
+  const int me = P.local_rank[li];
+  const int G = P.G;
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.state->t_rs_start = globaltimer();
+  // barrier (1) among the non-stragglers, per slice
+  if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
+    st_release_sys(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), P.epoch);
+  if (threadIdx.x == 0) {
+    bool ok = true;
+    for (int p = 0; p < W && ok; ++p)
+      if (p != me && p != P.sigma)
+        ok = spin_wait(flag_at(P.flags[me], SLOT_ARRIVE + p, G, s), P.epoch, P, 0x100 | p);
+    (void)ok;
+  }
+  if (!__syncthreads_and(*(volatile uint32_t*)&P.state->err == 0)) return;
+
+  const int g = P.logical_of_phys[me];  // owned chunk
+  const Range c = chunk_range(P, g);
+  const Range r = slice_of(c.lo, c.hi, s, G, 16 / P.esize);
+  // non-stragglers in ascending physical order (compile-time indices, no local memory)
+  const char* src[W - 1];
+#pragma unroll
+  for (int j = 0; j < W - 1; ++j) src[j] = P.buf[j < P.sigma ? j : j + 1];
+  // with two ranks the owner's chunk already is the non-straggler "sum"
+  if constexpr (W > 2) rs_slice<DT, W>(P, src, P.buf[me], r.lo * P.esize, r.hi * P.esize);
+  // "partial ready" for the straggler's half of the exchange
+  cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, G, s), P.epoch);
+}
+
+// ---------------------------------------------------------------- Phase B
+template <int DT, int W>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_constant__ LaunchPlan P) {
+  const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
+  const int me = P.local_rank[li];
+  const int G = P.G;
+  const int V = 16 / P.esize;
+  const uint32_t ep = P.epoch;
+  // the straggler reaches barrier (2): announce per slice to the others
+  if (me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
+    st_release_sys(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep);
+
+  char* mine = P.buf[me];
+  const int nops = P.nops[me];
+  for (int k = 0; k < nops; ++k) {
+    const Op op = P.ops[me][k];
+    const int c = op.chunk, peer = op.peer;
+    const Range cr = chunk_range(P, c);
+    const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
+    const uint64_t nvec_total = (sl.hi - sl.lo + V - 1) / V;
+    const uint64_t mid = sl.lo + (nvec_total / 2) * V < sl.hi ? sl.lo + (nvec_total / 2) * V : sl.hi;
+    if (op.kind == OP_EXCH_LOW) {
+      // non-straggler r: [lo, mid) of c_r = partial_r (+) x_sigma, stored at both ends
+      if (!cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, G, s), ep, P, 0x200 | k)) return;
+      const uint64_t a = sl.lo * P.esize, b = mid * P.esize;
+      add2_vecs<DT>(mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, (b - a) / 16);
+      add2_tail<DT>(mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
+                    mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
+                    (int)((b - a) % 16) / P.esize, P.esize);
+      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep);
+    } else if (op.kind == OP_EXCH_HIGH) {
+      // straggler: [mid, hi) of c_r; waits for rank r's Phase-A partial
+      if (!cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, G, s), ep, P, 0x300 | k)) return;
+      const uint64_t a = mid * P.esize, b = sl.hi * P.esize;
+      add2_vecs<DT>(mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, (b - a) / 16);
+      add2_tail<DT>(mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
+                    P.buf[peer] + a + (b - a) / 16 * 16, mine + a + (b - a) / 16 * 16,
+                    (int)((b - a) % 16) / P.esize, P.esize);
+      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep);
+    } else {
+      // copy of a fully reduced chunk (push)
+      if (!cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x400 | k)) return;
+      const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
+      copy_vecs(P.buf[peer] + a, mine + a, (b - a) / 16);
+      copy_tail(P.buf[peer] + a + (b - a) / 16 * 16, mine + a + (b - a) / 16 * 16, (int)((b - a) % 16));
+      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep);
+    }
+  }
+  // postcondition: every chunk has landed here
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < P.nchunks; ++c)
+      if (!spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x500 | c)) break;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- Ring
+// Physical ring 0 -> 1 -> ... -> n-1 -> 0 with n chunks.  Step t < n-1: pull
+// the left neighbour's partial of chunk (j-1-t) and add the own data (RS);
+// step t >= n-1: copy the left neighbour's final chunk (j-t+n-1) (AllGather).
+template <int DT, int W>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_constant__ LaunchPlan P) {
+  const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
+  const int j = P.local_rank[li];
+  const int G = P.G;
+  const int V = 16 / P.esize;
+  const uint32_t ep = P.epoch;
+  const int left = (j + W - 1) % W, right = (j + 1) % W;
+  if (threadIdx.x == 0) st_release_sys(flag_at(P.flags[right], SLOT_RING_ARRIVE, G, s), ep);
+  char* mine = P.buf[j];
+  const char* lbuf = P.buf[left];
+  for (int t = 0; t < 2 * (W - 1); ++t) {
+    const int wslot = (t == 0) ? SLOT_RING_ARRIVE : SLOT_RING_READY + t - 1;
+    if (!cta_wait(flag_at(P.flags[j], wslot, G, s), ep, P, 0x600 | t)) return;
+    const int k = (t < W - 1) ? ((j - 1 - t) % W + 2 * W) % W : ((j - t + W - 1) % W + 2 * W) % W;
+    const Range cr = chunk_range(P, k);
+    const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
+    const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
+    const uint64_t nv = (b - a) / 16;
+    if (t < W - 1) {
+      add2_vecs<DT>(mine + a, nullptr, lbuf + a, mine + a, nv);
+      add2_tail<DT>(mine + a + nv * 16, nullptr, lbuf + a + nv * 16, mine + a + nv * 16, (int)((b - a) % 16) / P.esize,
+                    P.esize);
+    } else {
+      copy_vecs(mine + a, lbuf + a, nv);
+      copy_tail(mine + a + nv * 16, lbuf + a + nv * 16, (int)((b - a) % 16));
+    }
+    if (t < 2 * (W - 1) - 1) cta_signal(flag_at(P.flags[right], SLOT_RING_READY + t, G, s), ep);
+  }
+  // I am done reading the left buffer; wait until the right neighbour is done with mine
+  cta_signal(flag_at(P.flags[left], SLOT_RING_DONE, G, s), ep);
+  cta_wait(flag_at(P.flags[j], SLOT_RING_DONE, G, s), ep, P, 0x700);
+}
+
+// ---------------------------------------------------------------- delay / barrier
+// Spin until base + ns, base = *base_ptr if given (team: start of Phase A),
+// else this kernel's own start (P:405-407 idle kernel; %globaltimer is
+// independent of the SM clock).
+__global__ void k_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st) {
+  uint64_t base = base_ptr ? *(volatile const uint64_t*)base_ptr : globaltimer();
+  const uint64_t until = base + ns;
+  uint64_t now;
+  while ((now = globaltimer()) < until) {
+    uint64_t left = until - now;
+    __nanosleep(left > 2000 ? 1000 : 64);
+  }
+  st->t_release = globaltimer();
+}
+
+__global__ void k_barrier(const __grid_constant__ LaunchPlan P) {
+  const int me = P.local_rank[0];
+  if (threadIdx.x < P.world && (int)threadIdx.x != me)
+    st_release_sys(flag_at(P.flags[threadIdx.x], SLOT_BARRIER + me, P.G, 0), P.epoch);
+  if (threadIdx.x < P.world && (int)threadIdx.x != me)
+    spin_wait(flag_at(P.flags[me], SLOT_BARRIER + threadIdx.x, P.G, 0), P.epoch, P, 0x800 | threadIdx.x);
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- host launchers
+template <int DT, int W>
+static void* kernel_ptr(int which) {
+  switch (which) {
+    case 0: return (void*)k_reduce_scatter<DT, W>;
+    case 1: return (void*)k_complete<DT, W>;
+    default: return (void*)k_ring<DT, W>;
+  }
+}
+
+void* select_kernel(int which, int dtype, int world) {
+#define SEL(DT)                                      \
+  switch (world) {                                   \
+    case 2: return kernel_ptr<DT, 2>(which);         \
+    case 4: return kernel_ptr<DT, 4>(which);         \
+    case 8: return kernel_ptr<DT, 8>(which);         \
+    default: return nullptr;                         \
+  }
+  switch (dtype) {
+    case DT_I32: SEL(DT_I32);
+    case DT_F32: SEL(DT_F32);
+    case DT_BF16: SEL(DT_BF16);
+    default: return nullptr;
+  }
+#undef SEL
+}
+
+cudaError_t launch_plan_kernel(int which, int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream) {
+  void* fn = select_kernel(which, dtype, P.world);
+  if (!fn) return cudaErrorInvalidValue;
+  void* args[] = {(void*)&P};
+  return cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(kThreads), args, 0, stream);
+}
+
+cudaError_t launch_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st, cudaStream_t stream) {
+  k_delay<<<1, 1, 0, stream>>>(base_ptr, ns, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_barrier(const LaunchPlan& P, cudaStream_t stream) {
+  k_barrier<<<1, 32, 0, stream>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t occupancy_blocks_per_sm(int which, int dtype, int world, int* blocks) {
+  void* fn = select_kernel(which, dtype, world);
+  if (!fn) return cudaErrorInvalidValue;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fn, kThreads, 0);
+}
+
+}  // namespace stragglar

@@ -1,0 +1,60 @@
+// Launch descriptors shared by the host API and the kernels.
+#pragma once
+#include <cstdint>
+
+#include "schedule.h"
+
+namespace stragglar {
+
+// Flag slots.  Every rank owns kSlots * G uint32 flags; slot k, slice s lives
+// at flags[k * G + s].  Flags hold the call's epoch (monotonic, never reset):
+// a waiter proceeds when (int32)(flag - epoch) >= 0.  Producers write peers'
+// flags (remote store, release at system scope); consumers spin on their own
+// (local load, acquire at system scope).
+enum Slot : int {
+  SLOT_HAVE = 0,         // + chunk: the chunk's slice has landed, fully reduced, in my buffer
+  SLOT_ARRIVE = 8,       // + physical rank: that rank's kernel started (its inputs are ready)
+  SLOT_RSDONE = 16,      // + chunk: the owner's Phase-A partial of the slice is ready (written at sigma)
+  SLOT_RING_ARRIVE = 24, // left neighbour started the ring
+  SLOT_RING_READY = 25,  // + step (0..13): left neighbour finished ring step
+  SLOT_RING_DONE = 39,   // right neighbour finished reading my buffer
+  SLOT_BARRIER = 40,     // + physical rank
+  kSlots = 48
+};
+
+constexpr int kThreads = 256;   // CTA size of the data kernels
+constexpr int kMaxSlices = 1024;
+
+// Device-resident per-communicator state (in the launching process's memory).
+struct DevState {
+  uint32_t err;          // 0 = ok, else an error code (first writer wins)
+  uint32_t err_info;
+  uint64_t t_rs_start;   // %globaltimer at the start of the last Phase-A launch (team)
+  uint64_t t_release;    // when the last injected delay released
+  uint64_t pad[5];
+};
+
+enum ErrCode : uint32_t { ERR_TIMEOUT = 1, ERR_BAD_PLAN = 2 };
+
+struct LaunchPlan {
+  int world;
+  int sigma;                 // physical straggler
+  int G;                     // slices per chunk == CTAs per rank
+  int nlocal;                // ranks served by this launch (1, or world in team mode)
+  int local_rank[kMaxWorld]; // physical rank of local index i (blockIdx.x / G)
+  char* buf[kMaxWorld];      // data buffer of each physical rank (local or peer mapping)
+  uint32_t* flags[kMaxWorld];// flag array of each physical rank
+  uint32_t epoch;
+  uint32_t pad0;
+  uint64_t count;            // elements
+  uint64_t ce;               // elements per chunk (chunks start at j*ce)
+  int nchunks;
+  int esize;
+  uint64_t timeout_ns;
+  DevState* state;
+  int logical_of_phys[kMaxWorld];
+  int nops[kMaxWorld];       // by physical rank
+  Op ops[kMaxWorld][kMaxOps];// by physical rank
+};
+
+}  // namespace stragglar

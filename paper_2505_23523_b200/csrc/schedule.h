@@ -1,0 +1,44 @@
+// Host-side StragglAR schedule (Algorithm 1) and the
+// per-rank op tables the round executor consumes.  Independent of oracle/.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace stragglar {
+
+struct Xfer {
+  int src, dst, chunk;
+  bool reduce;  // true: straggler exchange (both sides add); false: copy
+};
+using Round = std::vector<Xfer>;
+
+// Algorithm 1 in logical ranks (straggler = n-1).  n: power of two in [2, 64].
+// Throws std::runtime_error if n is unsupported or an internal invariant fails.
+std::vector<Round> generate_schedule(int n);
+
+// One step of a rank's program in the Phase-B kernel.
+enum OpKind : uint8_t {
+  OP_NONE = 0,
+  OP_EXCH_LOW = 1,   // non-straggler side of the c_r exchange: first half of every slice
+  OP_EXCH_HIGH = 2,  // straggler side of the c_r exchange: second half of every slice
+  OP_SEND = 3        // push a fully reduced chunk to `peer`
+};
+struct Op {
+  uint8_t kind, chunk, peer, round;  // peer is a PHYSICAL rank
+};
+
+constexpr int kMaxWorld = 8;
+constexpr int kMaxOps = 16;
+
+// Per-physical-rank programs for world n with physical straggler sigma.
+struct RankPrograms {
+  int n = 0, sigma = 0;
+  int phys_of_logical[kMaxWorld];
+  int logical_of_phys[kMaxWorld];
+  int nops[kMaxWorld];
+  Op ops[kMaxWorld][kMaxOps];
+};
+RankPrograms build_programs(int n, int sigma_phys);
+
+}  // namespace stragglar

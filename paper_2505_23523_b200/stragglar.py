@@ -1,0 +1,270 @@
+"""Thin ctypes binding of libstragglar.so (include/stragglar.h).
+
+Argument marshalling only: every function here forwards to the C function of
+the same name; all data movement and arithmetic run in the CUDA kernels.
+Tensors are torch CUDA tensors (PyTorch provides device memory and streams);
+their data pointers, element counts and dtypes are passed through.  There is
+no CPU fallback: if the shared library is missing, importing this module
+raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence, Tuple
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libstragglar.so")
+
+INT32, FLOAT32, BFLOAT16 = 0, 1, 2
+SUM = 0
+STATUS = {
+    0: "ok", 1: "invalid argument", 2: "unsupported", 3: "not initialized",
+    4: "not registered", 5: "CUDA error", 6: "timeout", 7: "internal error",
+}
+
+
+class StragglarError(RuntimeError):
+    def __init__(self, fn: str, status: int):
+        self.status = status
+        super().__init__(f"{fn} failed: {status} ({_status_string(status)})")
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    return ctypes.CDLL(LIB_PATH)
+
+
+_lib = _load()
+
+_c_int, _c_size, _c_u64, _vp = ctypes.c_int, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_void_p
+_PP = ctypes.POINTER(ctypes.c_void_p)
+_SIGS = {
+    "stragglar_version": ([], _c_int),
+    "stragglar_status_string": ([_c_int], ctypes.c_char_p),
+    "stragglar_launch_count": ([ctypes.POINTER(_c_u64)], _c_int),
+    "stragglar_schedule_rounds": ([_c_int, ctypes.POINTER(_c_int)], _c_int),
+    "stragglar_schedule_round": ([_c_int, _c_int, ctypes.POINTER(_c_int), _c_int, ctypes.POINTER(_c_int)], _c_int),
+    "stragglar_init": ([_c_int, _c_int, _c_int], _c_int),
+    "stragglar_handle_size": ([ctypes.POINTER(_c_size)], _c_int),
+    "stragglar_export_handle": ([_vp], _c_int),
+    "stragglar_import_handles": ([_vp, _c_int], _c_int),
+    "stragglar_register_buffer": ([_vp, _c_size, _vp], _c_int),
+    "stragglar_import_buffer": ([_vp, _vp, _c_int], _c_int),
+    "stragglar_allreduce": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_allreduce_ring": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_barrier": ([_vp], _c_int),
+    "stragglar_inject_delay": ([_c_u64, _vp], _c_int),
+    "stragglar_check_error": ([ctypes.POINTER(_c_int)], _c_int),
+    "stragglar_finalize": ([], _c_int),
+    "stragglar_team_init": ([_c_int, _c_int], _c_int),
+    "stragglar_team_allreduce": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_team_reduce_scatter": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_team_complete": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_team_allreduce_ring": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_team_inject_delay": ([_c_u64, _vp], _c_int),
+    "stragglar_team_allreduce_host": ([_PP, _PP, _PP, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_team_slices": ([ctypes.POINTER(_c_int)], _c_int),
+    "stragglar_team_check_error": ([ctypes.POINTER(_c_int)], _c_int),
+    "stragglar_team_finalize": ([], _c_int),
+}
+for _name, (_args, _res) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+EXPORTED = tuple(_SIGS)
+
+
+def _status_string(s: int) -> str:
+    return _lib.stragglar_status_string(s).decode()
+
+
+def _ck(fn: str, status: int) -> None:
+    if status != 0:
+        raise StragglarError(fn, status)
+
+
+# ---------------------------------------------------------------- marshalling helpers
+def _dtype_code(t) -> int:
+    import torch
+
+    m = {torch.int32: INT32, torch.float32: FLOAT32, torch.bfloat16: BFLOAT16}
+    if t.dtype not in m:
+        raise TypeError(f"unsupported dtype {t.dtype} (int32, float32, bfloat16)")
+    return m[t.dtype]
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    if isinstance(stream, int):
+        return stream or None
+    return stream.cuda_stream or None
+
+
+def _ptr_array(ts: Sequence) -> ctypes.Array:
+    arr = (ctypes.c_void_p * len(ts))()
+    for i, t in enumerate(ts):
+        arr[i] = t if isinstance(t, int) else t.data_ptr()
+    return arr
+
+
+def _team_args(bufs: Sequence):
+    if not bufs:
+        raise ValueError("empty buffer list")
+    n, dt = bufs[0].numel(), _dtype_code(bufs[0])
+    for b in bufs:
+        if b.numel() != n or _dtype_code(b) != dt or not b.is_cuda or not b.is_contiguous():
+            raise ValueError("team buffers must be contiguous CUDA tensors of equal size and dtype")
+    return _ptr_array(bufs), n, dt
+
+
+# ---------------------------------------------------------------- info / schedule
+def stragglar_version() -> int:
+    return _lib.stragglar_version()
+
+
+def stragglar_launch_count() -> int:
+    v = _c_u64(0)
+    _ck("stragglar_launch_count", _lib.stragglar_launch_count(ctypes.byref(v)))
+    return int(v.value)
+
+
+def stragglar_schedule_rounds(world: int) -> int:
+    r = _c_int(0)
+    _ck("stragglar_schedule_rounds", _lib.stragglar_schedule_rounds(world, ctypes.byref(r)))
+    return r.value
+
+
+def stragglar_schedule_round(world: int, rnd: int) -> List[Tuple[int, int, int, int]]:
+    cap = 4 * world
+    out = (_c_int * (4 * cap))()
+    k = _c_int(0)
+    _ck("stragglar_schedule_round", _lib.stragglar_schedule_round(world, rnd, out, cap, ctypes.byref(k)))
+    return [tuple(out[4 * i:4 * i + 4]) for i in range(k.value)]
+
+
+# ---------------------------------------------------------------- per-process communicator
+def stragglar_init(rank: int, world: int, straggler_rank: int) -> None:
+    _ck("stragglar_init", _lib.stragglar_init(rank, world, straggler_rank))
+
+
+def stragglar_handle_size() -> int:
+    v = _c_size(0)
+    _ck("stragglar_handle_size", _lib.stragglar_handle_size(ctypes.byref(v)))
+    return v.value
+
+
+def stragglar_export_handle() -> bytes:
+    buf = ctypes.create_string_buffer(stragglar_handle_size())
+    _ck("stragglar_export_handle", _lib.stragglar_export_handle(buf))
+    return buf.raw
+
+
+def stragglar_import_handles(blobs: bytes, world: int) -> None:
+    _ck("stragglar_import_handles", _lib.stragglar_import_handles(ctypes.c_char_p(blobs), world))
+
+
+def stragglar_register_buffer(t) -> bytes:
+    buf = ctypes.create_string_buffer(stragglar_handle_size())
+    nbytes = t.numel() * t.element_size()
+    _ck("stragglar_register_buffer", _lib.stragglar_register_buffer(t.data_ptr(), nbytes, buf))
+    return buf.raw
+
+
+def stragglar_import_buffer(t, blobs: bytes, world: int) -> None:
+    _ck("stragglar_import_buffer", _lib.stragglar_import_buffer(t.data_ptr(), ctypes.c_char_p(blobs), world))
+
+
+def stragglar_allreduce(t, stream=None) -> None:
+    _ck("stragglar_allreduce",
+        _lib.stragglar_allreduce(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream)))
+
+
+def stragglar_allreduce_ring(t, stream=None) -> None:
+    _ck("stragglar_allreduce_ring",
+        _lib.stragglar_allreduce_ring(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream)))
+
+
+def stragglar_barrier(stream=None) -> None:
+    _ck("stragglar_barrier", _lib.stragglar_barrier(_stream_ptr(stream)))
+
+
+def stragglar_inject_delay(ns: int, stream=None) -> None:
+    _ck("stragglar_inject_delay", _lib.stragglar_inject_delay(int(ns), _stream_ptr(stream)))
+
+
+def stragglar_check_error() -> int:
+    code = _c_int(0)
+    st = _lib.stragglar_check_error(ctypes.byref(code))
+    if st not in (0, 6):
+        _ck("stragglar_check_error", st)
+    return code.value
+
+
+def stragglar_finalize() -> None:
+    _ck("stragglar_finalize", _lib.stragglar_finalize())
+
+
+# ---------------------------------------------------------------- single-device team
+def stragglar_team_init(world: int, straggler_rank: int) -> None:
+    _ck("stragglar_team_init", _lib.stragglar_team_init(world, straggler_rank))
+
+
+def stragglar_team_slices() -> int:
+    v = _c_int(0)
+    _ck("stragglar_team_slices", _lib.stragglar_team_slices(ctypes.byref(v)))
+    return v.value
+
+
+def _team_call(name: str, bufs, stream) -> None:
+    arr, n, dt = _team_args(bufs)
+    _ck(name, getattr(_lib, name)(arr, n, dt, SUM, _stream_ptr(stream)))
+
+
+def stragglar_team_allreduce(bufs, stream=None) -> None:
+    _team_call("stragglar_team_allreduce", bufs, stream)
+
+
+def stragglar_team_reduce_scatter(bufs, stream=None) -> None:
+    _team_call("stragglar_team_reduce_scatter", bufs, stream)
+
+
+def stragglar_team_complete(bufs, stream=None) -> None:
+    _team_call("stragglar_team_complete", bufs, stream)
+
+
+def stragglar_team_allreduce_ring(bufs, stream=None) -> None:
+    _team_call("stragglar_team_allreduce_ring", bufs, stream)
+
+
+def stragglar_team_inject_delay(ns: int, stream=None) -> None:
+    _ck("stragglar_team_inject_delay", _lib.stragglar_team_inject_delay(int(ns), _stream_ptr(stream)))
+
+
+def stragglar_team_allreduce_host(host_in, host_out, bufs, stream=None) -> None:
+    """host_in/host_out: CPU tensors (pinned for full bandwidth) matching bufs."""
+    arr, n, dt = _team_args(bufs)
+    for h in list(host_in) + list(host_out):
+        if h.is_cuda or h.numel() != n or _dtype_code(h) != dt or not h.is_contiguous():
+            raise ValueError("host buffers must be contiguous CPU tensors matching the device buffers")
+    _ck("stragglar_team_allreduce_host",
+        _lib.stragglar_team_allreduce_host(_ptr_array(host_in), _ptr_array(host_out), arr, n, dt, SUM,
+                                           _stream_ptr(stream)))
+
+
+def stragglar_team_check_error() -> int:
+    code = _c_int(0)
+    st = _lib.stragglar_team_check_error(ctypes.byref(code))
+    if st not in (0, 6):
+        _ck("stragglar_team_check_error", st)
+    return code.value
+
+
+def stragglar_team_finalize() -> None:
+    _ck("stragglar_team_finalize", _lib.stragglar_team_finalize())

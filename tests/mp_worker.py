@@ -1,0 +1,99 @@
+"""Per-process (IPC) communicator exercised with every rank on cuda:0.
+
+Launched by tests/test_gpu_multiproc.py (and usable by hand):
+    python tests/mp_worker.py <world> <straggler> <count> <dtype> <port>
+Each process is one rank; torch.distributed (gloo) only exchanges the CUDA
+IPC blobs.  Ranks share one GPU, so their kernels time-slice unless MPS is
+running; the protocol must still complete (correct by construction).
+Exit code 0 = every rank's result equals the oracle bit for bit.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def worker(rank, world, sigma, count, dtype, port, q):
+    try:
+        os.environ.setdefault("STRAGGLAR_TIMEOUT_MS", "60000")
+        os.environ.setdefault("STRAGGLAR_SLICES", "8")
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        from paper_2505_23523_b200.dist import ProcessComm
+        from paper_2505_23523_b200.inputs import make_input
+        from paper_2505_23523_b200 import stragglar as S
+
+        comm = ProcessComm(sigma)
+        x = make_input(count, dtype, rank, config=7)
+        tdt = {"float32": torch.float32, "int32": torch.int32, "bfloat16": torch.bfloat16}[dtype]
+        t = torch.empty(count, dtype=tdt, device="cuda")
+        ring = torch.empty(count, dtype=tdt, device="cuda")
+        comm.register(t)
+        comm.register(ring)
+        host = torch.from_numpy(x.view(np.int16) if dtype == "bfloat16" else x)
+        t.view(host.dtype).copy_(host)
+        ring.view(host.dtype).copy_(host)
+        torch.cuda.synchronize()
+        dist.barrier()
+        S.stragglar_barrier()
+        if rank == sigma:
+            S.stragglar_inject_delay(200_000)
+        comm.allreduce(t)
+        comm.allreduce_ring(ring)
+        torch.cuda.synchronize()
+        err = S.stragglar_check_error()
+        out = t.view(host.dtype).cpu().numpy()
+        rout = ring.view(host.dtype).cpu().numpy()
+        dist.barrier()
+        comm.close()
+        q.put((rank, err, out.tobytes(), rout.tobytes()))
+        dist.destroy_process_group()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e), None, None))
+
+
+def run(world, sigma, count, dtype, port):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=worker, args=(r, world, sigma, count, dtype, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, err, out, rout = q.get(timeout=600)
+        res[r] = (err, out, rout)
+    for p in procs:
+        p.join(timeout=60)
+    from oracle import numerics as N
+    from paper_2505_23523_b200.inputs import make_inputs
+
+    xs = make_inputs(world, count, dtype, config=7)
+    want = N.stragglar_allreduce(xs, sigma, dtype)
+    rwant = N.ring_allreduce(xs, dtype)
+    ok = True
+    for r in range(world):
+        err, out, rout = res[r]
+        if out is None or err:
+            print(f"rank {r}: error {err}")
+            ok = False
+            continue
+        if out != want[r].tobytes():
+            print(f"rank {r}: stragglar result differs from the oracle")
+            ok = False
+        if rout != rwant[r].tobytes():
+            print(f"rank {r}: ring result differs from the oracle")
+            ok = False
+    return ok
+
+
+if __name__ == "__main__":
+    w, s, c, d, port = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], int(sys.argv[5])
+    ok = run(w, s, c, d, port)
+    print("OK" if ok else "FAIL")
+    sys.exit(0 if ok else 1)
