@@ -1,0 +1,86 @@
+"""world_size-2 gloo test of the multi-process host logic (CPU only): the IPC
+blob exchange that wires the per-process communicators together."""
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class FakeTensor:
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+
+class FakeLib:
+    """Stand-in for the ctypes binding that records what the C ABI would see."""
+
+    def __init__(self, rank):
+        self.rank = rank
+        self.calls = []
+
+    def stragglar_init(self, rank, world, sigma):
+        self.calls.append(("init", rank, world, sigma))
+
+    def stragglar_export_handle(self):
+        return bytes([self.rank]) * 80
+
+    def stragglar_import_handles(self, blobs, world):
+        self.calls.append(("import_handles", blobs, world))
+
+    def stragglar_register_buffer(self, t):
+        return bytes([100 + self.rank]) * 80 + t.ptr.to_bytes(8, "little")
+
+    def stragglar_import_buffer(self, t, blobs, world):
+        self.calls.append(("import_buffer", t.ptr, blobs, world))
+
+    def stragglar_allreduce(self, t, stream=None):
+        self.calls.append(("allreduce", t.ptr))
+
+    def stragglar_finalize(self):
+        self.calls.append(("finalize",))
+
+
+def _worker(rank, world, port, q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    from paper_2505_23523_b200.dist import ProcessComm
+
+    lib = FakeLib(rank)
+    comm = ProcessComm(straggler_rank=1, lib=lib)
+    comm.register(FakeTensor(1000 + rank))
+    comm.allreduce(FakeTensor(1000 + rank))
+    comm.close()
+    q.put((rank, lib.calls))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_handle_exchange_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=30)
+        assert p.exitcode == 0
+    want_handles = b"".join(bytes([r]) * 80 for r in range(world))
+    want_bufs = b"".join(bytes([100 + r]) * 80 + (1000 + r).to_bytes(8, "little") for r in range(world))
+    for r in range(world):
+        calls = got[r]
+        assert calls[0] == ("init", r, world, 1)
+        assert calls[1] == ("import_handles", want_handles, world)
+        assert calls[2] == ("import_buffer", 1000 + r, want_bufs, world)
+        assert calls[3] == ("allreduce", 1000 + r)
+        assert calls[4] == ("finalize",)
