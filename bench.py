@@ -298,6 +298,7 @@ def bench_team(args):
                         "(HBM stands in for NVLink; same kernels/flags/schedule as the NVLink mode)",
             "world": world, "straggler_rank": sigma, "count": count, "buffer_bytes": S_bytes,
             "slices_per_rank": G, "delay_us": D_ns / 1e3,
+            "mover": os.environ.get("STRAGGLAR_MOVER", "default"),
             "l2": "inputs (8 x 256 MiB) exceed the 126 MB L2; buffers reduced in place step after step",
             "parallelism": "team8-on-1gpu",
         },
@@ -479,7 +480,10 @@ def main():
     ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
     ap.add_argument("--delay-us", type=float, default=None)
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
+    ap.add_argument("--mover", choices=["lsu", "tma"], default=None, help="Phase-B data mover (default: library's)")
     args = ap.parse_args()
+    if args.mover:
+        os.environ["STRAGGLAR_MOVER"] = args.mover
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

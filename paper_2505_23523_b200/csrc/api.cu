@@ -22,7 +22,7 @@ void* select_kernel(int which, int dtype, int world);
 cudaError_t launch_plan_kernel(int which, int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream);
 cudaError_t launch_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st, cudaStream_t stream);
 cudaError_t launch_barrier(const LaunchPlan& P, cudaStream_t stream);
-cudaError_t occupancy_blocks_per_sm(int which, int dtype, int world, int* blocks);
+cudaError_t occupancy_blocks_per_sm(int which, int dtype, int world, int mover, int* blocks);
 }  // namespace stragglar
 
 using namespace stragglar;
@@ -30,6 +30,7 @@ using namespace stragglar;
 namespace {
 
 enum { K_RS = 0, K_COMPLETE = 1, K_RING = 2 };
+constexpr int kDefaultMover = MOVER_LSU;
 
 std::atomic<uint64_t> g_launches{0};
 
@@ -59,6 +60,7 @@ struct Comm {
   DevState* state = nullptr;
   RankPrograms progs;
   uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
+  int mover = MOVER_LSU;
   std::vector<Registration> regs;
   std::vector<void*> opened;   // IPC mappings to close
 };
@@ -97,7 +99,7 @@ uint64_t env_u64(const char* name, uint64_t dflt) {
 }
 
 // Smallest occupancy over all kernels of this world size, times the SM count.
-int resident_ctas(int world, int* sm_count) {
+int resident_ctas(int world, int mover, int* sm_count) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   int sms = 0;
@@ -106,7 +108,7 @@ int resident_ctas(int world, int* sm_count) {
   for (int which = 0; which < 3; ++which)
     for (int dt = 0; dt < 3; ++dt) {
       int b = 0;
-      if (occupancy_blocks_per_sm(which, dt, world, &b) != cudaSuccess) return -1;
+      if (occupancy_blocks_per_sm(which, dt, world, mover, &b) != cudaSuccess) return -1;
       best = b < best ? b : best;
     }
   if (sm_count) *sm_count = sms;
@@ -123,8 +125,12 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
     return STRAGGLAR_ERR_INTERNAL;
   }
   CK(cudaGetDevice(&c.device));
+  {
+    const char* m = std::getenv("STRAGGLAR_MOVER");
+    c.mover = (m && std::strcmp(m, "lsu") == 0) ? MOVER_LSU : (m && std::strcmp(m, "tma") == 0) ? MOVER_TMA : kDefaultMover;
+  }
   int sms = 0;
-  const int cap = resident_ctas(world, &sms);
+  const int cap = resident_ctas(world, c.mover, &sms);
   if (cap <= 0) return STRAGGLAR_ERR_CUDA;
   int G;
   if (team) {
@@ -187,6 +193,7 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, uint32_t epoch) {
   P.ce = chunk_elems(count, c.world - 1, P.esize);
   P.nchunks = c.world - 1;
   P.timeout_ns = c.timeout_ns;
+  P.mover = c.mover;
   P.state = c.state;
   for (int p = 0; p < c.world; ++p) {
     P.flags[p] = c.peer_flags[p];

@@ -87,7 +87,7 @@ __device__ __forceinline__ Range chunk_range(const LaunchPlan& P, int c) {
 }
 
 // ---------------------------------------------------------------- data movers
-constexpr int kUnroll = 4;
+constexpr int kUnroll = 8;
 constexpr int kMinBlocks = 4;  // <= 64 registers: 4 CTAs of 256 threads per SM
 
 // dst <- src for 16-byte vectors [0, nv)
@@ -114,7 +114,7 @@ __device__ __forceinline__ void add2_vecs(char* d0, char* d1, const char* a, con
   uint4* q0 = reinterpret_cast<uint4*>(d0);
   uint4* q1 = reinterpret_cast<uint4*>(d1);
   uint64_t i = threadIdx.x;
-  constexpr int U = 2;
+  constexpr int U = 4;
   const uint64_t step = (uint64_t)U * blockDim.x;
   for (; i + (U - 1) * blockDim.x < nv; i += step) {
     uint4 va[U], vb[U];
@@ -148,6 +148,115 @@ __device__ __forceinline__ void add2_tail(char* d0, char* d1, const char* a, con
 
 __device__ __forceinline__ void copy_tail(char* dst, const char* src, int nbytes) {
   if ((int)threadIdx.x < nbytes) dst[threadIdx.x] = *(const volatile char*)(src + threadIdx.x);
+}
+
+// ---------------------------------------------------------------- TMA movers (cp.async.bulk)
+// A ring of kStages shared-memory stages per CTA.  Thread 0 issues bulk loads
+// (mbarrier complete_tx) kStages pieces ahead and bulk stores (bulk groups);
+// for the fused exchange every thread adds the two staged operands in shared
+// memory before the stores.  All threads track the per-stage mbarrier parity
+// identically, so the ring persists across the ops of a kernel.
+constexpr int kStages = 3;
+constexpr uint32_t kStageBytes = 16384;
+constexpr int kTmaSmem = 128 + kStages * kStageBytes;
+
+struct Pipe {
+  uint64_t* bar;
+  char* stage;
+  uint32_t phase;  // bit s = parity to wait for on stage s
+  __device__ __forceinline__ char* buf(int s) const { return stage + (size_t)s * kStageBytes; }
+};
+
+__device__ __forceinline__ uint32_t advance_phase(uint32_t ph, uint32_t np) {
+#pragma unroll
+  for (int s = 0; s < kStages; ++s) {
+    const uint32_t uses = np / kStages + ((uint32_t)s < np % kStages ? 1u : 0u);
+    if (uses & 1u) ph ^= 1u << s;
+  }
+  return ph;
+}
+
+// dst <- src, nbytes a multiple of 16
+__device__ void tma_copy(Pipe& p, char* dst, const char* src, uint64_t nbytes) {
+  const uint32_t np = (uint32_t)((nbytes + kStageBytes - 1) / kStageBytes);
+  if (threadIdx.x == 0 && np) {
+    fence_proxy_async_global();
+    auto issue = [&](uint32_t i) {
+      const int s = i % kStages;
+      const uint64_t off = (uint64_t)i * kStageBytes;
+      const uint32_t len = (uint32_t)((nbytes - off) < kStageBytes ? (nbytes - off) : kStageBytes);
+      mbar_expect_tx(&p.bar[s], len);
+      bulk_load(p.buf(s), src + off, len, &p.bar[s]);
+    };
+    for (uint32_t i = 0; i < np && i < (uint32_t)kStages; ++i) issue(i);
+    uint32_t ph = p.phase;
+    for (uint32_t i = 0; i < np; ++i) {
+      const int s = i % kStages;
+      mbar_wait(&p.bar[s], (ph >> s) & 1u);
+      ph ^= 1u << s;
+      const uint64_t off = (uint64_t)i * kStageBytes;
+      const uint32_t len = (uint32_t)((nbytes - off) < kStageBytes ? (nbytes - off) : kStageBytes);
+      bulk_store(dst + off, p.buf(s), len);
+      bulk_commit();
+      if (i + kStages < np) {
+        bulk_wait_read_all();
+        issue(i + kStages);
+      }
+    }
+    bulk_wait_all();
+    fence_proxy_async_global();
+  }
+  p.phase = advance_phase(p.phase, np);
+}
+
+// d0 = d1 = a (+) b through shared memory, nbytes a multiple of 16
+template <int DT>
+__device__ void tma_add2(Pipe& p, char* d0, char* d1, const char* a, const char* b, uint64_t nbytes) {
+  constexpr uint32_t kPiece = kStageBytes / 2;
+  const uint32_t np = (uint32_t)((nbytes + kPiece - 1) / kPiece);
+  auto piece_len = [&](uint32_t i) -> uint32_t {
+    const uint64_t off = (uint64_t)i * kPiece;
+    return (uint32_t)((nbytes - off) < kPiece ? (nbytes - off) : kPiece);
+  };
+  auto issue = [&](uint32_t i) {
+    const int s = i % kStages;
+    const uint64_t off = (uint64_t)i * kPiece;
+    const uint32_t len = piece_len(i);
+    mbar_expect_tx(&p.bar[s], 2 * len);
+    bulk_load(p.buf(s), a + off, len, &p.bar[s]);
+    bulk_load(p.buf(s) + kPiece, b + off, len, &p.bar[s]);
+  };
+  if (threadIdx.x == 0 && np) {
+    fence_proxy_async_global();
+    for (uint32_t i = 0; i < np && i < (uint32_t)kStages; ++i) issue(i);
+  }
+  uint32_t ph = p.phase;
+  for (uint32_t i = 0; i < np; ++i) {
+    const int s = i % kStages;
+    const uint32_t len = piece_len(i);
+    mbar_wait(&p.bar[s], (ph >> s) & 1u);
+    ph ^= 1u << s;
+    uint4* A = reinterpret_cast<uint4*>(p.buf(s));
+    const uint4* B = reinterpret_cast<const uint4*>(p.buf(s) + kPiece);
+    for (uint32_t v = threadIdx.x; v < len / 16; v += blockDim.x) A[v] = add_vec<DT>(A[v], B[v]);
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint64_t off = (uint64_t)i * kPiece;
+      bulk_store(d0 + off, A, len);
+      if (d1) bulk_store(d1 + off, A, len);
+      bulk_commit();
+      if (i + kStages < np) {
+        bulk_wait_read_all();
+        issue(i + kStages);
+      }
+    }
+  }
+  if (threadIdx.x == 0 && np) {
+    bulk_wait_all();
+    fence_proxy_async_global();
+  }
+  p.phase = ph;
 }
 
 // ---------------------------------------------------------------- Phase A
@@ -245,6 +354,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
   if (me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
     st_release_sys(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep);
 
+  extern __shared__ __align__(128) unsigned char dsm[];
+  Pipe pipe{reinterpret_cast<uint64_t*>(dsm), reinterpret_cast<char*>(dsm) + 128, 0u};
+  const bool tma = P.mover == MOVER_TMA;
+  if (tma) {
+    if (threadIdx.x == 0) {
+      for (int st = 0; st < kStages; ++st) mbar_init(&pipe.bar[st], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
   char* mine = P.buf[me];
   const int nops = P.nops[me];
   for (int k = 0; k < nops; ++k) {
@@ -258,7 +377,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
       // non-straggler r: [lo, mid) of c_r = partial_r (+) x_sigma, stored at both ends
       if (!cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, G, s), ep, P, 0x200 | k)) return;
       const uint64_t a = sl.lo * P.esize, b = mid * P.esize;
-      add2_vecs<DT>(mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, (b - a) / 16);
+      if (tma)
+        tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, (b - a) / 16 * 16);
+      else
+        add2_vecs<DT>(mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, (b - a) / 16);
       add2_tail<DT>(mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
                     mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
                     (int)((b - a) % 16) / P.esize, P.esize);
@@ -267,7 +389,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
       // straggler: [mid, hi) of c_r; waits for rank r's Phase-A partial
       if (!cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, G, s), ep, P, 0x300 | k)) return;
       const uint64_t a = mid * P.esize, b = sl.hi * P.esize;
-      add2_vecs<DT>(mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, (b - a) / 16);
+      if (tma)
+        tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, (b - a) / 16 * 16);
+      else
+        add2_vecs<DT>(mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, (b - a) / 16);
       add2_tail<DT>(mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
                     P.buf[peer] + a + (b - a) / 16 * 16, mine + a + (b - a) / 16 * 16,
                     (int)((b - a) % 16) / P.esize, P.esize);
@@ -276,7 +401,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
       // copy of a fully reduced chunk (push)
       if (!cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x400 | k)) return;
       const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
-      copy_vecs(P.buf[peer] + a, mine + a, (b - a) / 16);
+      if (tma)
+        tma_copy(pipe, P.buf[peer] + a, mine + a, (b - a) / 16 * 16);
+      else
+        copy_vecs(P.buf[peer] + a, mine + a, (b - a) / 16);
       copy_tail(P.buf[peer] + a + (b - a) / 16 * 16, mine + a + (b - a) / 16 * 16, (int)((b - a) % 16));
       cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep);
     }
@@ -378,11 +506,13 @@ void* select_kernel(int which, int dtype, int world) {
 #undef SEL
 }
 
+int dynamic_smem(int which, int mover) { return (which == 1 && mover == MOVER_TMA) ? kTmaSmem : 0; }
+
 cudaError_t launch_plan_kernel(int which, int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream) {
   void* fn = select_kernel(which, dtype, P.world);
   if (!fn) return cudaErrorInvalidValue;
   void* args[] = {(void*)&P};
-  return cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(kThreads), args, 0, stream);
+  return cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(kThreads), args, dynamic_smem(which, P.mover), stream);
 }
 
 cudaError_t launch_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st, cudaStream_t stream) {
@@ -395,10 +525,15 @@ cudaError_t launch_barrier(const LaunchPlan& P, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
-cudaError_t occupancy_blocks_per_sm(int which, int dtype, int world, int* blocks) {
+cudaError_t occupancy_blocks_per_sm(int which, int dtype, int world, int mover, int* blocks) {
   void* fn = select_kernel(which, dtype, world);
   if (!fn) return cudaErrorInvalidValue;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fn, kThreads, 0);
+  const int smem = dynamic_smem(which, mover);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fn, kThreads, smem);
 }
 
 }  // namespace stragglar

@@ -36,6 +36,10 @@ struct DevState {
 
 enum ErrCode : uint32_t { ERR_TIMEOUT = 1, ERR_BAD_PLAN = 2 };
 
+// How k_complete moves bytes: SM load/store instructions (16-byte vectors) or
+// TMA bulk copies (cp.async.bulk through a shared-memory stage ring).
+enum Mover : int { MOVER_LSU = 0, MOVER_TMA = 1 };
+
 struct LaunchPlan {
   int world;
   int sigma;                 // physical straggler
@@ -50,6 +54,8 @@ struct LaunchPlan {
   uint64_t ce;               // elements per chunk (chunks start at j*ce)
   int nchunks;
   int esize;
+  int mover;
+  int pad1;
   uint64_t timeout_ns;
   DevState* state;
   int logical_of_phys[kMaxWorld];

@@ -1,0 +1,42 @@
+"""The per-process (CUDA IPC) communicator end to end: n processes, one rank
+each, all on cuda:0 (this run has one GPU).  Exercises stragglar_init /
+export / import / register_buffer / allreduce / allreduce_ring / barrier /
+inject_delay exactly as the NVLink mode uses them; results checked bit for bit
+against the oracle in tests/mp_worker.py."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world,sigma,count,dtype,mover", [
+    (2, 1, 100003, "float32", "lsu"),
+    (2, 0, 65536, "bfloat16", "tma"),
+    (4, 2, 250001, "int32", "tma"),
+    (4, 0, 99999, "float32", "lsu"),
+])
+def test_multiprocess_ipc(world, sigma, count, dtype, mover):
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    env = dict(os.environ, STRAGGLAR_MOVER=mover)
+    r = subprocess.run([sys.executable, os.path.join(HERE, "mp_worker.py"), str(world), str(sigma), str(count), dtype,
+                        str(_port())], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "OK" in r.stdout

@@ -7,6 +7,8 @@ canonical summation order makes fp32/bf16 reproducible); the north_star
 tolerances (1e-5 fp32, 1e-2 bf16 relative to sum|x|) are asserted
 too, as the acceptance bar.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -19,10 +21,12 @@ pytestmark = pytest.mark.gpu
 TOL = {"int32": 0.0, "float32": 1e-5, "bfloat16": 1e-2}
 
 
-@pytest.fixture(scope="module")
-def S():
+@pytest.fixture(scope="module", params=["lsu", "tma"])
+def S(request):
+    """Every test runs with both Phase-B data movers (SM 16-byte vectors, TMA bulk)."""
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
+    os.environ["STRAGGLAR_MOVER"] = request.param
     import __graft_entry__
 
     __graft_entry__.build()
