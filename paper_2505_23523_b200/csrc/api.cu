@@ -18,7 +18,7 @@
 #include "schedule.h"
 
 namespace stragglar {
-void* select_kernel(int which, int dtype, int world);
+void* select_kernel(int which, int dtype, int world, int mover);
 cudaError_t launch_plan_kernel(int which, int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream);
 cudaError_t launch_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st, cudaStream_t stream);
 cudaError_t launch_barrier(const LaunchPlan& P, cudaStream_t stream);
@@ -30,7 +30,7 @@ using namespace stragglar;
 namespace {
 
 enum { K_RS = 0, K_COMPLETE = 1, K_RING = 2 };
-constexpr int kDefaultMover = MOVER_LSU;
+constexpr int kDefaultMover = MOVER_TMA;   // measured faster (profiles/r01)
 
 std::atomic<uint64_t> g_launches{0};
 

@@ -167,6 +167,20 @@ struct Pipe {
   __device__ __forceinline__ char* buf(int s) const { return stage + (size_t)s * kStageBytes; }
 };
 
+// Shared-memory stage ring of the CTA (dynamic smem); mbarriers initialised once per launch.
+__device__ __forceinline__ Pipe make_pipe(bool active) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  Pipe p{reinterpret_cast<uint64_t*>(dsm), reinterpret_cast<char*>(dsm) + 128, 0u};
+  if (active) {
+    if (threadIdx.x == 0) {
+      for (int st = 0; st < kStages; ++st) mbar_init(&p.bar[st], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
+  return p;
+}
+
 __device__ __forceinline__ uint32_t advance_phase(uint32_t ph, uint32_t np) {
 #pragma unroll
   for (int s = 0; s < kStages; ++s) {
@@ -259,6 +273,61 @@ __device__ void tma_add2(Pipe& p, char* d0, char* d1, const char* a, const char*
   p.phase = ph;
 }
 
+// Phase A through shared memory: per stage, the W-1 non-straggler operands of
+// one piece (ascending physical order) are bulk-loaded, summed by the CTA in
+// canonical order into operand slot 0, and bulk-stored to the owner.
+template <int DT, int W>
+__device__ void tma_reduce(Pipe& p, char* dst, const char* const (&src)[W - 1], uint64_t lo_b, uint64_t nbytes) {
+  constexpr uint32_t kPiece = (kStageBytes / (W - 1)) / 16 * 16;
+  const uint32_t np = (uint32_t)((nbytes + kPiece - 1) / kPiece);
+  auto piece_len = [&](uint32_t i) -> uint32_t {
+    const uint64_t off = (uint64_t)i * kPiece;
+    return (uint32_t)((nbytes - off) < kPiece ? (nbytes - off) : kPiece);
+  };
+  auto issue = [&](uint32_t i) {
+    const int s = i % kStages;
+    const uint64_t off = lo_b + (uint64_t)i * kPiece;
+    const uint32_t len = piece_len(i);
+    mbar_expect_tx(&p.bar[s], (W - 1) * len);
+#pragma unroll
+    for (int j = 0; j < W - 1; ++j) bulk_load(p.buf(s) + j * kPiece, src[j] + off, len, &p.bar[s]);
+  };
+  if (threadIdx.x == 0 && np) {
+    fence_proxy_async_global();
+    for (uint32_t i = 0; i < np && i < (uint32_t)kStages; ++i) issue(i);
+  }
+  uint32_t ph = p.phase;
+  for (uint32_t i = 0; i < np; ++i) {
+    const int s = i % kStages;
+    const uint32_t len = piece_len(i);
+    mbar_wait(&p.bar[s], (ph >> s) & 1u);
+    ph ^= 1u << s;
+    char* base = p.buf(s);
+    for (uint32_t v = threadIdx.x; v < len / 16; v += blockDim.x) {
+      Acc<DT> acc;
+      acc.init(reinterpret_cast<const uint4*>(base)[v]);
+#pragma unroll
+      for (int j = 1; j < W - 1; ++j) acc.add(reinterpret_cast<const uint4*>(base + j * kPiece)[v]);
+      reinterpret_cast<uint4*>(base)[v] = acc.get();
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_store(dst + lo_b + (uint64_t)i * kPiece, base, len);
+      bulk_commit();
+      if (i + kStages < np) {
+        bulk_wait_read_all();
+        issue(i + kStages);
+      }
+    }
+  }
+  if (threadIdx.x == 0 && np) {
+    bulk_wait_all();
+    fence_proxy_async_global();
+  }
+  p.phase = ph;
+}
+
 // ---------------------------------------------------------------- Phase A
 // Canonical sum of the slice over the non-stragglers in ascending physical order.
 template <int DT, int W>
@@ -311,7 +380,7 @@ __device__ void rs_slice(const LaunchPlan& P, const char* const (&src)[W - 1], c
   }
 }
 
-template <int DT, int W>
+template <int DT, int W, int MV>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_reduce_scatter(const __grid_constant__ LaunchPlan P) {
   const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
   const int me = P.local_rank[li];
@@ -337,13 +406,23 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_reduce_scatter(const _
 #pragma unroll
   for (int j = 0; j < W - 1; ++j) src[j] = P.buf[j < P.sigma ? j : j + 1];
   // with two ranks the owner's chunk already is the non-straggler "sum"
-  if constexpr (W > 2) rs_slice<DT, W>(P, src, P.buf[me], r.lo * P.esize, r.hi * P.esize);
+  if constexpr (W > 2) {
+    if constexpr (MV == MOVER_TMA) {
+      Pipe pipe = make_pipe(true);
+      const uint64_t lo_b = r.lo * P.esize, hi_b = r.hi * P.esize;
+      const uint64_t body = (hi_b - lo_b) / 16 * 16;
+      tma_reduce<DT, W>(pipe, P.buf[me], src, lo_b, body);
+      rs_slice<DT, W>(P, src, P.buf[me], lo_b + body, hi_b);   // < 16-byte tail only
+    } else {
+      rs_slice<DT, W>(P, src, P.buf[me], r.lo * P.esize, r.hi * P.esize);
+    }
+  }
   // "partial ready" for the straggler's half of the exchange
   cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, G, s), P.epoch);
 }
 
 // ---------------------------------------------------------------- Phase B
-template <int DT, int W>
+template <int DT, int W, int MV>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_constant__ LaunchPlan P) {
   const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
   const int me = P.local_rank[li];
@@ -354,16 +433,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
   if (me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
     st_release_sys(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep);
 
-  extern __shared__ __align__(128) unsigned char dsm[];
-  Pipe pipe{reinterpret_cast<uint64_t*>(dsm), reinterpret_cast<char*>(dsm) + 128, 0u};
-  const bool tma = P.mover == MOVER_TMA;
-  if (tma) {
-    if (threadIdx.x == 0) {
-      for (int st = 0; st < kStages; ++st) mbar_init(&pipe.bar[st], 1);
-      fence_mbar_init();
-    }
-    __syncthreads();
-  }
+  constexpr bool tma = MV == MOVER_TMA;
+  Pipe pipe = make_pipe(tma);
   char* mine = P.buf[me];
   const int nops = P.nops[me];
   for (int k = 0; k < nops; ++k) {
@@ -377,7 +448,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
       // non-straggler r: [lo, mid) of c_r = partial_r (+) x_sigma, stored at both ends
       if (!cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, G, s), ep, P, 0x200 | k)) return;
       const uint64_t a = sl.lo * P.esize, b = mid * P.esize;
-      if (tma)
+      if constexpr (tma)
         tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, (b - a) / 16 * 16);
       else
         add2_vecs<DT>(mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, (b - a) / 16);
@@ -389,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
       // straggler: [mid, hi) of c_r; waits for rank r's Phase-A partial
       if (!cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, G, s), ep, P, 0x300 | k)) return;
       const uint64_t a = mid * P.esize, b = sl.hi * P.esize;
-      if (tma)
+      if constexpr (tma)
         tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, (b - a) / 16 * 16);
       else
         add2_vecs<DT>(mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, (b - a) / 16);
@@ -401,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
       // copy of a fully reduced chunk (push)
       if (!cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x400 | k)) return;
       const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
-      if (tma)
+      if constexpr (tma)
         tma_copy(pipe, P.buf[peer] + a, mine + a, (b - a) / 16 * 16);
       else
         copy_vecs(P.buf[peer] + a, mine + a, (b - a) / 16);
@@ -421,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
 // Physical ring 0 -> 1 -> ... -> n-1 -> 0 with n chunks.  Step t < n-1: pull
 // the left neighbour's partial of chunk (j-1-t) and add the own data (RS);
 // step t >= n-1: copy the left neighbour's final chunk (j-t+n-1) (AllGather).
-template <int DT, int W>
+template <int DT, int W, int MV>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_constant__ LaunchPlan P) {
   const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
   const int j = P.local_rank[li];
@@ -430,6 +501,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
   const uint32_t ep = P.epoch;
   const int left = (j + W - 1) % W, right = (j + 1) % W;
   if (threadIdx.x == 0) st_release_sys(flag_at(P.flags[right], SLOT_RING_ARRIVE, G, s), ep);
+  constexpr bool tma = MV == MOVER_TMA;
+  Pipe pipe = make_pipe(tma);
   char* mine = P.buf[j];
   const char* lbuf = P.buf[left];
   for (int t = 0; t < 2 * (W - 1); ++t) {
@@ -441,11 +514,17 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
     const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
     const uint64_t nv = (b - a) / 16;
     if (t < W - 1) {
-      add2_vecs<DT>(mine + a, nullptr, lbuf + a, mine + a, nv);
+      if constexpr (tma)
+        tma_add2<DT>(pipe, mine + a, nullptr, lbuf + a, mine + a, nv * 16);
+      else
+        add2_vecs<DT>(mine + a, nullptr, lbuf + a, mine + a, nv);
       add2_tail<DT>(mine + a + nv * 16, nullptr, lbuf + a + nv * 16, mine + a + nv * 16, (int)((b - a) % 16) / P.esize,
                     P.esize);
     } else {
-      copy_vecs(mine + a, lbuf + a, nv);
+      if constexpr (tma)
+        tma_copy(pipe, mine + a, lbuf + a, nv * 16);
+      else
+        copy_vecs(mine + a, lbuf + a, nv);
       copy_tail(mine + a + nv * 16, lbuf + a + nv * 16, (int)((b - a) % 16));
     }
     if (t < 2 * (W - 1) - 1) cta_signal(flag_at(P.flags[right], SLOT_RING_READY + t, G, s), ep);
@@ -481,21 +560,28 @@ __global__ void k_barrier(const __grid_constant__ LaunchPlan P) {
 
 // ---------------------------------------------------------------- host launchers
 template <int DT, int W>
-static void* kernel_ptr(int which) {
+static void* kernel_ptr(int which, int mover) {
+  if (mover == MOVER_TMA) {
+    switch (which) {
+      case 0: return (void*)k_reduce_scatter<DT, W, MOVER_TMA>;
+      case 1: return (void*)k_complete<DT, W, MOVER_TMA>;
+      default: return (void*)k_ring<DT, W, MOVER_TMA>;
+    }
+  }
   switch (which) {
-    case 0: return (void*)k_reduce_scatter<DT, W>;
-    case 1: return (void*)k_complete<DT, W>;
-    default: return (void*)k_ring<DT, W>;
+    case 0: return (void*)k_reduce_scatter<DT, W, MOVER_LSU>;
+    case 1: return (void*)k_complete<DT, W, MOVER_LSU>;
+    default: return (void*)k_ring<DT, W, MOVER_LSU>;
   }
 }
 
-void* select_kernel(int which, int dtype, int world) {
-#define SEL(DT)                                      \
-  switch (world) {                                   \
-    case 2: return kernel_ptr<DT, 2>(which);         \
-    case 4: return kernel_ptr<DT, 4>(which);         \
-    case 8: return kernel_ptr<DT, 8>(which);         \
-    default: return nullptr;                         \
+void* select_kernel(int which, int dtype, int world, int mover) {
+#define SEL(DT)                                             \
+  switch (world) {                                          \
+    case 2: return kernel_ptr<DT, 2>(which, mover);         \
+    case 4: return kernel_ptr<DT, 4>(which, mover);         \
+    case 8: return kernel_ptr<DT, 8>(which, mover);         \
+    default: return nullptr;                                \
   }
   switch (dtype) {
     case DT_I32: SEL(DT_I32);
@@ -506,10 +592,10 @@ void* select_kernel(int which, int dtype, int world) {
 #undef SEL
 }
 
-int dynamic_smem(int which, int mover) { return (which == 1 && mover == MOVER_TMA) ? kTmaSmem : 0; }
+int dynamic_smem(int which, int mover) { return (which <= 2 && mover == MOVER_TMA) ? kTmaSmem : 0; }
 
 cudaError_t launch_plan_kernel(int which, int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream) {
-  void* fn = select_kernel(which, dtype, P.world);
+  void* fn = select_kernel(which, dtype, P.world, P.mover);
   if (!fn) return cudaErrorInvalidValue;
   void* args[] = {(void*)&P};
   return cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(kThreads), args, dynamic_smem(which, P.mover), stream);
@@ -526,7 +612,7 @@ cudaError_t launch_barrier(const LaunchPlan& P, cudaStream_t stream) {
 }
 
 cudaError_t occupancy_blocks_per_sm(int which, int dtype, int world, int mover, int* blocks) {
-  void* fn = select_kernel(which, dtype, world);
+  void* fn = select_kernel(which, dtype, world, mover);
   if (!fn) return cudaErrorInvalidValue;
   const int smem = dynamic_smem(which, mover);
   if (smem > 48 * 1024) {
