@@ -181,6 +181,18 @@ void common_finalize(Comm& c) {
   c = Comm();
 }
 
+// Slices per call: about one slice per kSliceBytes of a chunk, at most the
+// communicator's G.  Small messages use few CTAs (less flag traffic per round),
+// large ones all of them.  Any G is safe call to call: flags hold monotone
+// epochs, so values left at other positions by earlier calls are stale (< epoch).
+int slices_for(const Comm& c, uint64_t chunk_bytes) {
+  const uint64_t per = env_u64("STRAGGLAR_SLICE_BYTES", 16384);
+  uint64_t g = per ? (chunk_bytes + per - 1) / per : (uint64_t)c.G;
+  if (g < 1) g = 1;
+  if (g > (uint64_t)c.G) g = c.G;
+  return (int)g;
+}
+
 LaunchPlan base_plan(const Comm& c, size_t count, int dtype, uint32_t epoch) {
   LaunchPlan P;
   std::memset(&P, 0, sizeof(P));
@@ -192,8 +204,10 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, uint32_t epoch) {
   P.esize = esize_of(dtype);
   P.ce = chunk_elems(count, c.world - 1, P.esize);
   P.nchunks = c.world - 1;
+  P.G = slices_for(c, P.ce * P.esize);
   P.timeout_ns = c.timeout_ns;
   P.mover = c.mover;
+  P.sys_scope = c.team ? (int)env_u64("STRAGGLAR_SYS_SCOPE", 0) : 1;
   P.state = c.state;
   for (int p = 0; p < c.world; ++p) {
     P.flags[p] = c.peer_flags[p];
@@ -241,7 +255,7 @@ int team_rs(void* const* bufs, size_t count, int dtype, void* stream, uint32_t e
   for (int p = 0; p < c.world; ++p)
     if (p != c.sigma) P.local_rank[k++] = p;
   P.nlocal = k;
-  return launch(K_RS, dtype, P, k * c.G, stream);
+  return launch(K_RS, dtype, P, k * P.G, stream);
 }
 
 int team_b(void* const* bufs, size_t count, int dtype, void* stream, uint32_t epoch) {
@@ -252,7 +266,7 @@ int team_b(void* const* bufs, size_t count, int dtype, void* stream, uint32_t ep
     P.local_rank[p] = p;
   }
   P.nlocal = c.world;
-  return launch(K_COMPLETE, dtype, P, c.world * c.G, stream);
+  return launch(K_COMPLETE, dtype, P, c.world * P.G, stream);
 }
 
 int read_error(Comm& c, int* code) {
@@ -445,8 +459,8 @@ int stragglar_allreduce(void* buf, size_t count, int dtype, int op, void* stream
   if ((st = proc_plan(buf, count, dtype, &P, c.epoch + 1))) return st;
   ++c.epoch;
   if (c.rank != c.sigma)
-    if ((st = launch(K_RS, dtype, P, c.G, stream))) return st;
-  return launch(K_COMPLETE, dtype, P, c.G, stream);
+    if ((st = launch(K_RS, dtype, P, P.G, stream))) return st;
+  return launch(K_COMPLETE, dtype, P, P.G, stream);
 }
 
 int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* stream) {
@@ -460,7 +474,8 @@ int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* s
   ++c.epoch;
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
-  return launch(K_RING, dtype, P, c.G, stream);
+  P.G = slices_for(c, P.ce * P.esize);
+  return launch(K_RING, dtype, P, P.G, stream);
 }
 
 int stragglar_barrier(void* stream) {
@@ -546,12 +561,13 @@ int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, in
   LaunchPlan P = base_plan(c, count, dtype, ++c.epoch);
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
+  P.G = slices_for(c, P.ce * P.esize);
   for (int p = 0; p < c.world; ++p) {
     P.buf[p] = (char*)bufs[p];
     P.local_rank[p] = p;
   }
   P.nlocal = c.world;
-  return launch(K_RING, dtype, P, c.world * c.G, stream);
+  return launch(K_RING, dtype, P, c.world * P.G, stream);
 }
 
 int stragglar_team_inject_delay(uint64_t ns, void* stream) {

@@ -29,6 +29,25 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
   asm volatile("fence.acq_rel.sys;\n\tst.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// GPU-scope variants: enough when every rank lives on this device (team mode)
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// scope-selected flag access: sys for CUDA-IPC peers on other GPUs, gpu for one device
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p, bool sys) {
+  return sys ? ld_acquire_sys(p) : ld_acquire_gpu(p);
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v, bool sys) {
+  if (sys)
+    st_release_sys(p, v);
+  else
+    st_release_gpu(p, v);
+}
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

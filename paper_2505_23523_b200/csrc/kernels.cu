@@ -30,11 +30,12 @@ __device__ __forceinline__ bool flag_ok(uint32_t v, uint32_t epoch) { return int
 // Spin (one thread) until *f >= epoch.  Bounded by the watchdog; gives up
 // early if another CTA of this process already reported an error.
 __device__ bool spin_wait(const uint32_t* f, uint32_t epoch, const LaunchPlan& P, uint32_t where) {
-  if (flag_ok(ld_acquire_sys(f), epoch)) return true;
+  const bool sys = P.sys_scope;
+  if (flag_ok(ld_acquire(f, sys), epoch)) return true;
   const uint64_t t0 = globaltimer();
   for (uint32_t it = 1;; ++it) {
-    if (flag_ok(ld_acquire_sys(f), epoch)) return true;
-    if (it > 64) __nanosleep(40);
+    if (flag_ok(ld_acquire(f, sys), epoch)) return true;
+    if (it > 2048) __nanosleep(32);
     if ((it & 127) == 0) {
       if (*(volatile uint32_t*)&P.state->err) return false;
       if (globaltimer() - t0 > P.timeout_ns) {
@@ -53,9 +54,9 @@ __device__ __forceinline__ bool cta_wait(const uint32_t* f, uint32_t epoch, cons
 }
 
 // Whole-CTA signal: all prior stores of the CTA happen-before the flag store.
-__device__ __forceinline__ void cta_signal(uint32_t* f, uint32_t epoch) {
+__device__ __forceinline__ void cta_signal(uint32_t* f, uint32_t epoch, bool sys) {
   __syncthreads();
-  if (threadIdx.x == 0) st_release_sys(f, epoch);
+  if (threadIdx.x == 0) st_release(f, epoch, sys);
 }
 
 __device__ __forceinline__ uint32_t* flag_at(uint32_t* base, int slot, int G, int s) {
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_reduce_scatter(const _
   if (blockIdx.x == 0 && threadIdx.x == 0) P.state->t_rs_start = globaltimer();
   // barrier (1) among the non-stragglers, per slice
   if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
-    st_release_sys(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), P.epoch);
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), P.epoch, P.sys_scope);
   if (threadIdx.x == 0) {
     bool ok = true;
     for (int p = 0; p < W && ok; ++p)
@@ -418,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_reduce_scatter(const _
     }
   }
   // "partial ready" for the straggler's half of the exchange
-  cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, G, s), P.epoch);
+  cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, G, s), P.epoch, P.sys_scope);
 }
 
 // ---------------------------------------------------------------- Phase B
@@ -431,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
   const uint32_t ep = P.epoch;
   // the straggler reaches barrier (2): announce per slice to the others
   if (me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
-    st_release_sys(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep);
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep, P.sys_scope);
 
   constexpr bool tma = MV == MOVER_TMA;
   Pipe pipe = make_pipe(tma);
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
       add2_tail<DT>(mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
                     mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
                     (int)((b - a) % 16) / P.esize, P.esize);
-      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep);
+      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep, P.sys_scope);
     } else if (op.kind == OP_EXCH_HIGH) {
       // straggler: [mid, hi) of c_r; waits for rank r's Phase-A partial
       if (!cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, G, s), ep, P, 0x300 | k)) return;
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
       add2_tail<DT>(mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
                     P.buf[peer] + a + (b - a) / 16 * 16, mine + a + (b - a) / 16 * 16,
                     (int)((b - a) % 16) / P.esize, P.esize);
-      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep);
+      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep, P.sys_scope);
     } else {
       // copy of a fully reduced chunk (push)
       if (!cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x400 | k)) return;
@@ -477,7 +478,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
       else
         copy_vecs(P.buf[peer] + a, mine + a, (b - a) / 16);
       copy_tail(P.buf[peer] + a + (b - a) / 16 * 16, mine + a + (b - a) / 16 * 16, (int)((b - a) % 16));
-      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep);
+      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep, P.sys_scope);
     }
   }
   // postcondition: every chunk has landed here
@@ -500,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
   const int V = 16 / P.esize;
   const uint32_t ep = P.epoch;
   const int left = (j + W - 1) % W, right = (j + 1) % W;
-  if (threadIdx.x == 0) st_release_sys(flag_at(P.flags[right], SLOT_RING_ARRIVE, G, s), ep);
+  if (threadIdx.x == 0) st_release(flag_at(P.flags[right], SLOT_RING_ARRIVE, G, s), ep, P.sys_scope);
   constexpr bool tma = MV == MOVER_TMA;
   Pipe pipe = make_pipe(tma);
   char* mine = P.buf[j];
@@ -527,10 +528,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
         copy_vecs(mine + a, lbuf + a, nv);
       copy_tail(mine + a + nv * 16, lbuf + a + nv * 16, (int)((b - a) % 16));
     }
-    if (t < 2 * (W - 1) - 1) cta_signal(flag_at(P.flags[right], SLOT_RING_READY + t, G, s), ep);
+    if (t < 2 * (W - 1) - 1) cta_signal(flag_at(P.flags[right], SLOT_RING_READY + t, G, s), ep, P.sys_scope);
   }
   // I am done reading the left buffer; wait until the right neighbour is done with mine
-  cta_signal(flag_at(P.flags[left], SLOT_RING_DONE, G, s), ep);
+  cta_signal(flag_at(P.flags[left], SLOT_RING_DONE, G, s), ep, P.sys_scope);
   cta_wait(flag_at(P.flags[j], SLOT_RING_DONE, G, s), ep, P, 0x700);
 }
 
@@ -552,7 +553,7 @@ __global__ void k_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st) {
 __global__ void k_barrier(const __grid_constant__ LaunchPlan P) {
   const int me = P.local_rank[0];
   if (threadIdx.x < P.world && (int)threadIdx.x != me)
-    st_release_sys(flag_at(P.flags[threadIdx.x], SLOT_BARRIER + me, P.G, 0), P.epoch);
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_BARRIER + me, P.G, 0), P.epoch, P.sys_scope);
   if (threadIdx.x < P.world && (int)threadIdx.x != me)
     spin_wait(flag_at(P.flags[me], SLOT_BARRIER + threadIdx.x, P.G, 0), P.epoch, P, 0x800 | threadIdx.x);
   __syncthreads();

@@ -55,7 +55,7 @@ struct LaunchPlan {
   int nchunks;
   int esize;
   int mover;
-  int pad1;
+  int sys_scope;             // 1: flags/fences at system scope (peers on other GPUs); 0: gpu scope (team)
   uint64_t timeout_ns;
   DevState* state;
   int logical_of_phys[kMaxWorld];

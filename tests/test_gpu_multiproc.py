@@ -40,3 +40,16 @@ def test_multiprocess_ipc(world, sigma, count, dtype, mover):
                         str(_port())], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "OK" in r.stdout
+
+
+def test_watchdog_reports_missing_peer():
+    """A rank that never arrives: the spin-waits time out (STRAGGLAR_TIMEOUT_MS),
+    the kernel exits and stragglar_check_error reports ERR_TIMEOUT (no hang)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    r = subprocess.run([sys.executable, os.path.join(HERE, "mp_timeout.py"), str(_port())],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
