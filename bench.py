@@ -227,6 +227,7 @@ def bench_team(args):
     t_start, t_end = ev(), ev()
     with ClockSampler(0) as clk:
         torch.cuda.synchronize()
+        torch.cuda._sleep(4_000_000)   # GPU busy ~2 ms while the host queues the timed steps
         t_start.record()
         for evs in steps:
             sar_step(evs)
@@ -246,6 +247,7 @@ def bench_team(args):
         S.stragglar_team_allreduce_ring(ring)
     torch.cuda.synchronize()
     rs = [(ev(), ev()) for _ in range(args.steps)]
+    torch.cuda._sleep(4_000_000)
     for e0, e1 in rs:
         e0.record()
         S.stragglar_team_allreduce_ring(ring)

@@ -31,6 +31,13 @@ def ev():
     return torch.cuda.Event(enable_timing=True)
 
 
+def blocker():
+    """Queue ~3 ms of GPU spin so the launches that follow are submitted while
+    the GPU is busy: event intervals then measure device time, not Python /
+    launch-API submission time (which is ~15 us per call through ctypes)."""
+    torch.cuda._sleep(6_000_000)
+
+
 def measure(n, sigma, count, dtype, iters, warm, delay_factor=1.25):
     S.stragglar_team_init(n, sigma)
     bufs = [torch.randn(count, device="cuda").to(dtype) for _ in range(n)]
@@ -52,6 +59,7 @@ def measure(n, sigma, count, dtype, iters, warm, delay_factor=1.25):
     torch.cuda.synchronize()
     # no delay: Phase A then Phase B back to back
     E = [[ev() for _ in range(4)] for _ in range(iters)]
+    blocker()
     for e in E:
         run_split(None, e)
     torch.cuda.synchronize()
@@ -61,6 +69,7 @@ def measure(n, sigma, count, dtype, iters, warm, delay_factor=1.25):
     # masked delay
     D = int((delay_factor * T_A + 20.0) * 1e3)
     E = [[ev() for _ in range(4)] for _ in range(iters)]
+    blocker()
     for e in E:
         run_split(D, e)
     torch.cuda.synchronize()
@@ -69,6 +78,7 @@ def measure(n, sigma, count, dtype, iters, warm, delay_factor=1.25):
     D_meas = statistics.median(e[0].elapsed_time(e[2]) * 1e3 for e in E)
     # ring
     R = [(ev(), ev()) for _ in range(iters)]
+    blocker()
     for a, b in R:
         a.record()
         S.stragglar_team_allreduce_ring(ring)
@@ -102,6 +112,7 @@ def delay_sweep(n, sigma, count, dtype, iters, warm):
         S.stragglar_team_allreduce_ring(ring)
     torch.cuda.synchronize()
     E = [[ev() for _ in range(4)] for _ in range(iters)]
+    blocker()
     for e in E:
         e[0].record()
         S.stragglar_team_reduce_scatter(bufs)
@@ -109,6 +120,7 @@ def delay_sweep(n, sigma, count, dtype, iters, warm):
         S.stragglar_team_complete(bufs)
         e[3].record()
     R = [(ev(), ev()) for _ in range(iters)]
+    blocker()
     for a, b in R:
         a.record()
         S.stragglar_team_allreduce_ring(ring)
@@ -121,6 +133,7 @@ def delay_sweep(n, sigma, count, dtype, iters, warm):
     for f in [0.0, 0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.8, 0.9, 1.0, 1.1, 1.25, 1.5]:
         D = int(f * T_RS * 1e3)
         E = [[ev() for _ in range(4)] for _ in range(iters)]
+        blocker()
         for e in E:
             e[0].record()
             S.stragglar_team_reduce_scatter(bufs)

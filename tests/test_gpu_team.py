@@ -186,3 +186,22 @@ def test_argument_errors(S):
     S.stragglar_team_allreduce([torch.zeros(0, device="cuda") for _ in range(4)])  # count 0: no-op
     with pytest.raises(S.StragglarError):
         S.stragglar_team_init(3, 0)
+
+
+@pytest.mark.parametrize("n,sigma,count,dtype", [
+    (8, 0, 13_107_200, "bfloat16"),   # BASELINE configs[3]: 25 MiB bf16 DP bucket
+    (8, 3, 524_288, "bfloat16"),      # BASELINE configs[4]: [64 x 8192] bf16 TP activation, straggler 3
+    (4, 0, 1 << 20, "float32"),       # BASELINE configs[0]
+])
+def test_baseline_configs_exact(S, n, sigma, count, dtype):
+    """The BASELINE workloads at their exact sizes, split phases + delay as
+    bench.py/sweep.py time them, every element vs the oracle's replay."""
+    xs = make_inputs(n, count, dtype, config=4)
+    bufs = [to_dev(x, dtype) for x in xs]
+    S.stragglar_team_init(n, sigma)
+    S.stragglar_team_reduce_scatter(bufs)
+    S.stragglar_team_inject_delay(50_000)
+    S.stragglar_team_complete(bufs)
+    torch.cuda.synchronize()
+    assert S.stragglar_team_check_error() == 0
+    check_equal([to_host(b, dtype) for b in bufs], N.stragglar_allreduce(xs, sigma, dtype), xs, dtype, "config")
