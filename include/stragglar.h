@@ -153,6 +153,28 @@ int stragglar_team_slices(int* slices);
 int stragglar_team_check_error(int* code);
 int stragglar_team_finalize(void);
 
+/* ---- algorithm selection for an expected delay ------
+ * PAPER.md §4.2: StragglAR beats a baseline B iff
+ *     T_delay >= T_RS - max{T_B - T_SAR, 0}.
+ * stragglar_select evaluates it with the alpha-beta model of this
+ * implementation, per port, for a buffer of `bytes` at `world` ranks:
+ *     T_RS   = alpha + (n-2)/(n-1) * bytes * beta     (Phase A: one direct-pull step)
+ *     T_SAR  = R alpha + R/(n-1) * bytes * beta        (R = n + log2 n - 2)
+ *     T_Ring = 2(n-1) alpha + 2(n-1)/n * bytes * beta
+ * Outputs the critical delay (s, >= 0) and use_stragglar = (delay_s >= critical).
+ * Host only; world must be 2, 4 or 8 (or any power of two up to 64). */
+int stragglar_select(int world, double bytes, double delay_s, double alpha_s, double beta_s_per_byte,
+                     int* use_stragglar, double* critical_delay_s);
+/* Cost-model constants of the per-process communicator used by
+ * stragglar_allreduce_auto (defaults: alpha = 3 us; beta = 1/(770 GB/s),
+ * the measured B200 peer-copy bandwidth per direction). */
+int stragglar_set_cost_model(double alpha_s, double beta_s_per_byte);
+/* Collective: every rank passes the same expected straggler delay; runs
+ * StragglAR if stragglar_select says so, else the Ring; *used_stragglar tells
+ * which (may be NULL). */
+int stragglar_allreduce_auto(void* buf, size_t count, int dtype, int op, void* stream, uint64_t expected_delay_ns,
+                             int* used_stragglar);
+
 /* Number of kernel launches the library enqueued since load (bench evidence). */
 int stragglar_launch_count(uint64_t* launches);
 

@@ -61,6 +61,8 @@ struct Comm {
   RankPrograms progs;
   uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
   int mover = MOVER_LSU;
+  double alpha_s = 3e-6;               // P:450 per-message latency used in the paper's model
+  double beta_s_per_byte = 1.0 / 770e9; // measured B200 peer copy per direction (B200_PROFILING.md)
   std::vector<Registration> regs;
   std::vector<void*> opened;   // IPC mappings to close
 };
@@ -476,6 +478,53 @@ int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* s
   P.nchunks = c.world;
   P.G = slices_for(c, P.ce * P.esize);
   return launch(K_RING, dtype, P, P.G, stream);
+}
+
+int stragglar_select(int world, double bytes, double delay_s, double alpha_s, double beta, int* use_stragglar,
+                     double* critical_delay_s) {
+  if (world < 2 || world > 64 || (world & (world - 1))) return STRAGGLAR_ERR_UNSUPPORTED;
+  if (!(bytes >= 0) || !(alpha_s >= 0) || !(beta >= 0)) return STRAGGLAR_ERR_INVALID_ARG;
+  int L = 0;
+  while ((1 << L) < world) ++L;
+  const double n = world, R = world + L - 2;
+  const double t_rs = (world > 2 ? alpha_s : 0.0) + (n - 2) / (n - 1) * bytes * beta;
+  const double t_sar = R * alpha_s + R / (n - 1) * bytes * beta;
+  const double t_ring = 2 * (n - 1) * alpha_s + 2 * (n - 1) / n * bytes * beta;
+  const double gain = t_ring - t_sar > 0 ? t_ring - t_sar : 0.0;
+  double crit = t_rs - gain;
+  if (crit < 0) crit = 0;
+  if (critical_delay_s) *critical_delay_s = crit;
+  if (use_stragglar) *use_stragglar = delay_s >= crit ? 1 : 0;
+  return STRAGGLAR_OK;
+}
+
+int stragglar_set_cost_model(double alpha_s, double beta) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_proc.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (!(alpha_s >= 0) || !(beta > 0)) return STRAGGLAR_ERR_INVALID_ARG;
+  g_proc.alpha_s = alpha_s;
+  g_proc.beta_s_per_byte = beta;
+  return STRAGGLAR_OK;
+}
+
+int stragglar_allreduce_auto(void* buf, size_t count, int dtype, int op, void* stream, uint64_t expected_delay_ns,
+                             int* used_stragglar) {
+  double a, b;
+  int world;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!g_proc.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+    a = g_proc.alpha_s;
+    b = g_proc.beta_s_per_byte;
+    world = g_proc.world;
+  }
+  const int es = esize_of(dtype);
+  if (!es) return STRAGGLAR_ERR_UNSUPPORTED;
+  int use = 1;
+  int st = stragglar_select(world, (double)count * es, expected_delay_ns * 1e-9, a, b, &use, nullptr);
+  if (st) return st;
+  if (used_stragglar) *used_stragglar = use;
+  return use ? stragglar_allreduce(buf, count, dtype, op, stream) : stragglar_allreduce_ring(buf, count, dtype, op, stream);
 }
 
 int stragglar_barrier(void* stream) {

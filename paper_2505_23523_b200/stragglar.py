@@ -59,6 +59,10 @@ _SIGS = {
     "stragglar_inject_delay": ([_c_u64, _vp], _c_int),
     "stragglar_check_error": ([ctypes.POINTER(_c_int)], _c_int),
     "stragglar_finalize": ([], _c_int),
+    "stragglar_select": ([_c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                          ctypes.POINTER(_c_int), ctypes.POINTER(ctypes.c_double)], _c_int),
+    "stragglar_set_cost_model": ([ctypes.c_double, ctypes.c_double], _c_int),
+    "stragglar_allreduce_auto": ([_vp, _c_size, _c_int, _c_int, _vp, _c_u64, ctypes.POINTER(_c_int)], _c_int),
     "stragglar_team_init": ([_c_int, _c_int], _c_int),
     "stragglar_team_allreduce": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_team_reduce_scatter": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
@@ -189,6 +193,27 @@ def stragglar_allreduce(t, stream=None) -> None:
 def stragglar_allreduce_ring(t, stream=None) -> None:
     _ck("stragglar_allreduce_ring",
         _lib.stragglar_allreduce_ring(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream)))
+
+
+def stragglar_select(world: int, nbytes: float, delay_s: float, alpha_s: float, beta_s_per_byte: float):
+    """-> (use_stragglar: bool, critical_delay_s: float)"""
+    use, crit = _c_int(0), ctypes.c_double(0.0)
+    _ck("stragglar_select", _lib.stragglar_select(world, float(nbytes), float(delay_s), float(alpha_s),
+                                                  float(beta_s_per_byte), ctypes.byref(use), ctypes.byref(crit)))
+    return bool(use.value), crit.value
+
+
+def stragglar_set_cost_model(alpha_s: float, beta_s_per_byte: float) -> None:
+    _ck("stragglar_set_cost_model", _lib.stragglar_set_cost_model(float(alpha_s), float(beta_s_per_byte)))
+
+
+def stragglar_allreduce_auto(t, expected_delay_ns: int, stream=None) -> bool:
+    """Returns True if StragglAR ran, False if the Ring did."""
+    used = _c_int(0)
+    _ck("stragglar_allreduce_auto",
+        _lib.stragglar_allreduce_auto(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream),
+                                      int(expected_delay_ns), ctypes.byref(used)))
+    return bool(used.value)
 
 
 def stragglar_barrier(stream=None) -> None:

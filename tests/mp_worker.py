@@ -34,11 +34,16 @@ def worker(rank, world, sigma, count, dtype, port, q):
         tdt = {"float32": torch.float32, "int32": torch.int32, "bfloat16": torch.bfloat16}[dtype]
         t = torch.empty(count, dtype=tdt, device="cuda")
         ring = torch.empty(count, dtype=tdt, device="cuda")
+        autos = [torch.empty(count, dtype=tdt, device="cuda") for _ in range(2)]
         comm.register(t)
         comm.register(ring)
+        for a in autos:
+            comm.register(a)
         host = torch.from_numpy(x.view(np.int16) if dtype == "bfloat16" else x)
         t.view(host.dtype).copy_(host)
         ring.view(host.dtype).copy_(host)
+        for a in autos:
+            a.view(host.dtype).copy_(host)
         torch.cuda.synchronize()
         dist.barrier()
         S.stragglar_barrier()
@@ -46,16 +51,19 @@ def worker(rank, world, sigma, count, dtype, port, q):
             S.stragglar_inject_delay(200_000)
         comm.allreduce(t)
         comm.allreduce_ring(ring)
+        # NEXT row N2: selection for an expected delay (0 and 10 ms)
+        used = [S.stragglar_allreduce_auto(autos[0], 0), S.stragglar_allreduce_auto(autos[1], 10_000_000)]
         torch.cuda.synchronize()
         err = S.stragglar_check_error()
         out = t.view(host.dtype).cpu().numpy()
         rout = ring.view(host.dtype).cpu().numpy()
+        aout = [(u, a.view(host.dtype).cpu().numpy().tobytes()) for u, a in zip(used, autos)]
         dist.barrier()
         comm.close()
-        q.put((rank, err, out.tobytes(), rout.tobytes()))
+        q.put((rank, err, out.tobytes(), rout.tobytes(), aout))
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover - reported to the parent
-        q.put((rank, repr(e), None, None))
+        q.put((rank, repr(e), None, None, None))
 
 
 def run(world, sigma, count, dtype, port):
@@ -66,8 +74,8 @@ def run(world, sigma, count, dtype, port):
         p.start()
     res = {}
     for _ in range(world):
-        r, err, out, rout = q.get(timeout=600)
-        res[r] = (err, out, rout)
+        r, err, out, rout, aout = q.get(timeout=600)
+        res[r] = (err, out, rout, aout)
     for p in procs:
         p.join(timeout=60)
     from oracle import numerics as N
@@ -78,7 +86,7 @@ def run(world, sigma, count, dtype, port):
     rwant = N.ring_allreduce(xs, dtype)
     ok = True
     for r in range(world):
-        err, out, rout = res[r]
+        err, out, rout, aout = res[r]
         if out is None or err:
             print(f"rank {r}: error {err}")
             ok = False
@@ -88,6 +96,13 @@ def run(world, sigma, count, dtype, port):
             ok = False
         if rout != rwant[r].tobytes():
             print(f"rank {r}: ring result differs from the oracle")
+            ok = False
+        for used, b in aout:
+            if b != (want[r] if used else rwant[r]).tobytes():
+                print(f"rank {r}: auto ({'stragglar' if used else 'ring'}) result differs from the oracle")
+                ok = False
+        if not aout[1][0]:
+            print(f"rank {r}: a 10 ms expected delay did not select StragglAR")
             ok = False
     return ok
 

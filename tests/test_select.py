@@ -1,0 +1,61 @@
+"""Algorithm selection for an expected delay (NEXT row N2) against the
+paper's §4.2 condition as the oracle states it (CPU only)."""
+import math
+
+import pytest
+
+from oracle import cost as C
+
+
+@pytest.fixture(scope="module")
+def S():
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_2505_23523_b200 import stragglar
+
+    return stragglar
+
+
+@pytest.mark.parametrize("n", [2, 4, 8, 16, 64])
+@pytest.mark.parametrize("nbytes", [2 ** 20, 25 * 2 ** 20, 2 ** 28, 2 ** 30, 4 * 2 ** 30])
+def test_critical_delay_matches_paper_beta_terms(S, n, nbytes):
+    """alpha = 0: the library's critical delay equals P:423-424 evaluated with
+    the oracle's Table-1 costs (the ReduceScatter moves (m-1)/m of the buffer
+    among m = n-1 ranks in both)."""
+    beta = 1 / 770e9
+    _, crit = S.stragglar_select(n, nbytes, 0.0, 0.0, beta)
+    want = C.critical_delay(n, nbytes, 0.0, beta, C.t_ring(n, nbytes, 0.0, beta))
+    assert crit == pytest.approx(want, rel=1e-12, abs=1e-15)
+
+
+@pytest.mark.parametrize("n", [4, 8])
+def test_choice_flips_at_the_critical_delay(S, n):
+    """StragglAR is chosen iff delay >= critical; the end-to-end model times
+    (P:417 measured from the non-stragglers' start) tie at the critical delay."""
+    alpha, beta, s = 3e-6, 1 / 770e9, 2 ** 30
+    _, crit = S.stragglar_select(n, s, 0.0, alpha, beta)
+    assert S.stragglar_select(n, s, crit * 1.001 + 1e-9, alpha, beta)[0]
+    if crit > 0:
+        assert not S.stragglar_select(n, s, crit * 0.999, alpha, beta)[0]
+        L = int(math.log2(n))
+        R = n + L - 2
+        t_rs = alpha + (n - 2) / (n - 1) * s * beta
+        t_sar = R * alpha + R / (n - 1) * s * beta
+        t_ring = 2 * (n - 1) * alpha + 2 * (n - 1) / n * s * beta
+        assert max(crit, t_rs) + t_sar == pytest.approx(crit + t_ring, rel=1e-9)
+
+
+def test_large_buffers_without_delay_prefer_ring_at_n8(S):
+    """with no delay StragglAR pays the whole ReduceScatter (15/7 vs
+    7/4 s*beta at n=8) and loses; with a delay that masks the ReduceScatter it
+    wins (Table 1)."""
+    use0, crit = S.stragglar_select(8, 2 ** 30, 0.0, 3e-6, 1 / 770e9)
+    assert not use0 and crit > 0
+    use1, _ = S.stragglar_select(8, 2 ** 30, 0.0015, 3e-6, 1 / 770e9)
+    assert use1
+
+
+def test_select_rejects_bad_world(S):
+    with pytest.raises(S.StragglarError):
+        S.stragglar_select(6, 1.0, 0.0, 0.0, 1.0)
