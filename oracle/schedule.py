@@ -198,6 +198,100 @@ def generate_stragglar(n: int) -> Schedule:
 
 
 # --------------------------------------------------------------------------
+# Appendix B: even, non-power-of-2 n
+# --------------------------------------------------------------------------
+def max_weight_matching(vertices: List[int], weight) -> Tuple[int, List[Tuple[int, int]]]:
+    """Maximum-weight matching by exhaustive search (exact; n <= 8 here).
+
+    P:684 names Edmonds' algorithm; for a handful of vertices enumerating every
+    matching is the same optimum with no room for error.  Enumeration order
+    (the tie-break between equal-weight optima): take the lowest unmatched
+    vertex u, try partners v > u in ascending order, then u unmatched; the
+    first maximum found wins.
+    """
+    best = [-1, []]
+
+    def rec(rest: List[int], cur: List[Tuple[int, int]], w: int) -> None:
+        if not rest:
+            if w > best[0]:
+                best[0], best[1] = w, list(cur)
+            return
+        u, tail = rest[0], rest[1:]
+        for i, v in enumerate(tail):
+            wt = weight(u, v)
+            if wt > 0:
+                cur.append((u, v))
+                rec(tail[:i] + tail[i + 1:], cur, w + wt)
+                cur.pop()
+        rec(tail, cur, w)
+
+    rec(sorted(vertices), [], 0)
+    return best[0], best[1]
+
+
+def generate_stragglar_even(n: int, max_rounds: Optional[int] = None) -> Schedule:
+    """Appendix B for even n that is not a power of two.
+
+    Readings (DESIGN.md "Readings" 18-21, after SPEC S:216-243):
+    * Phase A and the straggler pairing are kept: round r < n-1 exchanges c_r
+      between rank r and sigma, both reducing (P:163-164 carries over).
+    * Every other rank (and sigma once it is free, r >= n-1) is a vertex; u
+      "needs" chunk c from v iff v holds c fully reduced and u does not (only
+      fully reduced chunks propagate).  Edge weight 2 if each needs
+      something from the other, 1 if only one direction.
+    * A maximum-weight matching is taken per round; each matched rank sends the
+      oldest (lowest-index) chunk its partner needs.
+    * Rounds continue until every rank holds every chunk.
+    """
+    if n < 4 or n % 2 or not (n & (n - 1)):
+        raise ScheduleError(f"n={n}: Appendix B covers even n that are not powers of two")
+    sigma = n - 1
+    full = {h: set() for h in range(n)}          # fully reduced chunks held
+    sched = Schedule("stragglar", n, sigma, n - 1)
+    limit = max_rounds if max_rounds is not None else 4 * n
+    r = 0
+    while any(len(full[h]) < n - 1 for h in range(n)):
+        if r >= limit:
+            raise ScheduleError(f"n={n}: no completion within {limit} rounds")
+        tx: List[Transfer] = []
+        busy = set()
+        if r < n - 1:
+            tx += [Transfer(r, sigma, r, REDUCE), Transfer(sigma, r, r, REDUCE)]
+            busy = {r, sigma}
+        verts = [h for h in range(n) if h not in busy]
+
+        def needs(u: int, v: int) -> List[int]:
+            return sorted(full[v] - full[u])
+
+        def weight(u: int, v: int) -> int:
+            return (1 if needs(u, v) else 0) + (1 if needs(v, u) else 0)
+
+        _, matching = max_weight_matching(verts, weight)
+        for u, v in matching:
+            for a, b in ((u, v), (v, u)):
+                nd = needs(b, a)                  # what b needs from a
+                if nd:
+                    tx.append(Transfer(a, b, nd[0], REPLACE))
+        sched.rounds.append(tx)
+        new = {h: set(c) for h, c in full.items()}
+        for t in tx:
+            new[t.dst].add(t.chunk) if t.kind == REPLACE else new[t.dst].add(t.chunk)
+        if r < n - 1:
+            new[r].add(r)
+            new[sigma].add(r)
+        full = new
+        r += 1
+    return sched
+
+
+def generate(n: int) -> Schedule:
+    """Algorithm 1 for powers of two, Appendix B for other even n."""
+    if n >= 2 and not (n & (n - 1)):
+        return generate_stragglar(n)
+    return generate_stragglar_even(n)
+
+
+# --------------------------------------------------------------------------
 # Baseline: Ring (P:359-361); S:257 fixes the transfer pattern
 # --------------------------------------------------------------------------
 def generate_ring(n: int) -> Schedule:
