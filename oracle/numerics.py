@@ -203,7 +203,7 @@ def stragglar_allreduce(inputs: Sequence[np.ndarray], sigma_phys: int, dtype: st
     if n == 1:
         return bufs
     if sched is None:
-        sched = S.generate_stragglar(n)
+        sched = S.generate(n)      # Algorithm 1 (powers of two) or Appendix B (even n)
     phys = logical_to_physical(n, sigma_phys)
     phase_a_reduce_scatter(bufs, sigma_phys, dtype)
     replay_schedule(bufs, sched, phys, dtype, chunk_bounds(bufs[0].size, n - 1, dtype))

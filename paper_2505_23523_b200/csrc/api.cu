@@ -86,7 +86,7 @@ int esize_of(int dtype) {
   }
 }
 
-bool pow2_world(int w) { return w == 2 || w == 4 || w == 8; }
+bool pow2_world(int w) { return w == 2 || w == 4 || w == 6 || w == 8; }  // 6: Appendix B schedule
 
 uint64_t chunk_elems(uint64_t count, int parts, int esize) {
   const uint64_t v = 16 / esize;
@@ -295,7 +295,7 @@ const char* stragglar_status_string(int s) {
   switch (s) {
     case STRAGGLAR_OK: return "ok";
     case STRAGGLAR_ERR_INVALID_ARG: return "invalid argument";
-    case STRAGGLAR_ERR_UNSUPPORTED: return "unsupported (world must be 2, 4 or 8; dtype int32/float32/bfloat16; op SUM)";
+    case STRAGGLAR_ERR_UNSUPPORTED: return "unsupported (world must be 2, 4, 6 or 8; dtype int32/float32/bfloat16; op SUM)";
     case STRAGGLAR_ERR_NOT_INITIALIZED: return "communicator not initialized (or peer handles not imported)";
     case STRAGGLAR_ERR_NOT_REGISTERED: return "buffer is not inside a registered, peer-mapped allocation";
     case STRAGGLAR_ERR_CUDA: return "CUDA error";
@@ -315,7 +315,7 @@ int stragglar_launch_count(uint64_t* n) {
 int stragglar_schedule_rounds(int world, int* rounds) {
   if (!rounds) return STRAGGLAR_ERR_INVALID_ARG;
   try {
-    *rounds = (int)generate_schedule(world).size();
+    *rounds = (int)generate_any(world).size();
   } catch (const std::exception&) {
     return STRAGGLAR_ERR_UNSUPPORTED;
   }
@@ -325,7 +325,7 @@ int stragglar_schedule_rounds(int world, int* rounds) {
 int stragglar_schedule_round(int world, int round, int* out, int max_transfers, int* n_transfers) {
   if (!n_transfers || (!out && max_transfers > 0)) return STRAGGLAR_ERR_INVALID_ARG;
   try {
-    auto s = generate_schedule(world);
+    auto s = generate_any(world);
     if (round < 0 || round >= (int)s.size()) return STRAGGLAR_ERR_INVALID_ARG;
     const auto& rd = s[round];
     *n_transfers = (int)rd.size();
@@ -482,11 +482,15 @@ int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* s
 
 int stragglar_select(int world, double bytes, double delay_s, double alpha_s, double beta, int* use_stragglar,
                      double* critical_delay_s) {
-  if (world < 2 || world > 64 || (world & (world - 1))) return STRAGGLAR_ERR_UNSUPPORTED;
+  if (world < 2 || world > 64 || (world & 1)) return STRAGGLAR_ERR_UNSUPPORTED;
   if (!(bytes >= 0) || !(alpha_s >= 0) || !(beta >= 0)) return STRAGGLAR_ERR_INVALID_ARG;
-  int L = 0;
-  while ((1 << L) < world) ++L;
-  const double n = world, R = world + L - 2;
+  double Rr;
+  try {
+    Rr = (double)generate_any(world).size();     // n + log2 n - 2 for powers of two (Thm 1)
+  } catch (const std::exception&) {
+    return STRAGGLAR_ERR_UNSUPPORTED;
+  }
+  const double n = world, R = Rr;
   const double t_rs = (world > 2 ? alpha_s : 0.0) + (n - 2) / (n - 1) * bytes * beta;
   const double t_sar = R * alpha_s + R / (n - 1) * bytes * beta;
   const double t_ring = 2 * (n - 1) * alpha_s + 2 * (n - 1) / n * bytes * beta;

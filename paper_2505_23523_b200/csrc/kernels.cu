@@ -581,6 +581,7 @@ void* select_kernel(int which, int dtype, int world, int mover) {
   switch (world) {                                          \
     case 2: return kernel_ptr<DT, 2>(which, mover);         \
     case 4: return kernel_ptr<DT, 4>(which, mover);         \
+    case 6: return kernel_ptr<DT, 6>(which, mover);         \
     case 8: return kernel_ptr<DT, 8>(which, mover);         \
     default: return nullptr;                                \
   }

@@ -144,8 +144,97 @@ std::vector<Round> generate_schedule(int n) {
   return sched;
 }
 
+// ---------------------------------------------------------------------------
+// Appendix B: even n that is not a power of two.  Per round the
+// straggler pairing of round r < n-1 is kept; every other rank (and the
+// straggler once it is free) is a vertex; u needs chunk c from v iff v holds
+// c fully reduced and u does not.  Edge weight = number of directions with a
+// need (2 or 1).  A maximum-weight matching is found by exhaustive
+// search (n <= 14 here; P:684 cites Edmonds, same optimum); ties go to the
+// first optimum in the order "lowest free vertex u, partners v > u ascending,
+// then u unmatched".  Each matched rank sends the lowest-index chunk its
+// partner needs.  DESIGN.md readings 18-21.
+namespace {
+
+struct Matcher {
+  int nv = 0;
+  int verts[64];
+  int w[64][64];
+  int best_w = -1;
+  std::vector<std::pair<int, int>> best, cur;
+
+  void rec(uint64_t rest, int acc) {
+    if (!rest) {
+      if (acc > best_w) {
+        best_w = acc;
+        best = cur;
+      }
+      return;
+    }
+    const int ui = __builtin_ctzll(rest);
+    const uint64_t tail = rest & (rest - 1);
+    for (uint64_t t = tail; t; t &= t - 1) {
+      const int vi = __builtin_ctzll(t);
+      if (w[ui][vi] > 0) {
+        cur.push_back({verts[ui], verts[vi]});
+        rec(tail & ~(1ull << vi), acc + w[ui][vi]);
+        cur.pop_back();
+      }
+    }
+    rec(tail, acc);
+  }
+};
+
+std::vector<Round> generate_even(int n) {
+  if (n < 6 || n > 14 || (n & 1) || !(n & (n - 1))) throw std::runtime_error("even non-power-of-two world must be in [6, 14]");
+  const int sigma = n - 1;
+  std::vector<uint64_t> full(n, 0);             // fully reduced chunks held, per rank
+  const uint64_t all = (1ull << (n - 1)) - 1;
+  std::vector<Round> sched;
+  for (int r = 0;; ++r) {
+    bool done = true;
+    for (int h = 0; h < n; ++h) done &= full[h] == all;
+    if (done) break;
+    if (r >= 4 * n) throw std::runtime_error("appendix-B schedule did not complete");
+    Round rd;
+    Matcher m;
+    for (int h = 0; h < n; ++h) {
+      if (r < n - 1 && (h == r || h == sigma)) continue;
+      m.verts[m.nv++] = h;
+    }
+    if (r < n - 1) {
+      rd.push_back({r, sigma, r, true});
+      rd.push_back({sigma, r, r, true});
+    }
+    for (int i = 0; i < m.nv; ++i)
+      for (int j = 0; j < m.nv; ++j) {
+        const int a = m.verts[i], b = m.verts[j];
+        m.w[i][j] = (i == j) ? 0 : ((full[b] & ~full[a]) ? 1 : 0) + ((full[a] & ~full[b]) ? 1 : 0);
+      }
+    m.rec(m.nv == 64 ? ~0ull : ((1ull << m.nv) - 1), 0);
+    for (auto [u, v] : m.best)
+      for (int d = 0; d < 2; ++d) {
+        const int a = d ? v : u, b = d ? u : v;  // a sends to b
+        const uint64_t need = full[a] & ~full[b];
+        if (need) rd.push_back({a, b, __builtin_ctzll(need), false});
+      }
+    sched.push_back(rd);
+    std::vector<uint64_t> nf = full;
+    for (const Xfer& x : rd) nf[x.dst] |= 1ull << x.chunk;
+    full = nf;
+  }
+  return sched;
+}
+
+}  // namespace
+
+std::vector<Round> generate_any(int n) {
+  if (n >= 2 && !(n & (n - 1))) return generate_schedule(n);
+  return generate_even(n);
+}
+
 RankPrograms build_programs(int n, int sigma_phys) {
-  if (n < 2 || n > kMaxWorld || (n & (n - 1))) throw std::runtime_error("world must be 2, 4 or 8");
+  if (n < 2 || n > kMaxWorld || (n & 1)) throw std::runtime_error("world must be 2, 4, 6 or 8");
   if (sigma_phys < 0 || sigma_phys >= n) throw std::runtime_error("straggler rank out of range");
   RankPrograms pr;
   pr.n = n;
@@ -157,7 +246,7 @@ RankPrograms build_programs(int n, int sigma_phys) {
   for (int p = 0; p < kMaxWorld; ++p) pr.nops[p] = 0;
 
   const int lsig = n - 1;
-  auto sched = generate_schedule(n);
+  auto sched = generate_any(n);
   for (size_t r = 0; r < sched.size(); ++r) {
     for (const Xfer& x : sched[r]) {
       Op op{};

@@ -16,6 +16,8 @@ using Round = std::vector<Xfer>;
 // Algorithm 1 in logical ranks (straggler = n-1).  n: power of two in [2, 64].
 // Throws std::runtime_error if n is unsupported or an internal invariant fails.
 std::vector<Round> generate_schedule(int n);
+// Algorithm 1 for powers of two, Appendix B (max-weight matching) for even n in [6, 14].
+std::vector<Round> generate_any(int n);
 
 // One step of a rank's program in the Phase-B kernel.
 enum OpKind : uint8_t {

@@ -77,7 +77,7 @@ def test_cpp_schedule_verifies(S, world):
     assert rep.valid, rep.violations[:3]
 
 
-@pytest.mark.parametrize("world", [3, 6, 0, 128])
+@pytest.mark.parametrize("world", [3, 5, 0, 128, 16 + 2])
 def test_cpp_schedule_rejects(S, world):
     with pytest.raises(S.StragglarError):
         S.stragglar_schedule_rounds(world)
@@ -98,10 +98,22 @@ def test_init_without_gpu_reports_error(S):
     """On this CPU box the runtime finds no device: CUDA error, not a crash.
     Unsupported worlds are rejected before touching CUDA."""
     assert S._lib.stragglar_team_init(3, 0) == 2
-    assert S._lib.stragglar_init(0, 6, 0) == 2
+    assert S._lib.stragglar_init(0, 5, 0) == 2
+    assert S._lib.stragglar_init(0, 16, 0) == 2
     assert S._lib.stragglar_init(5, 4, 0) == 1
     assert S._lib.stragglar_team_init(4, 9) == 1
     st = S._lib.stragglar_team_init(4, 0)
     assert st in (0, 5)
     if st == 0:
         S.stragglar_team_finalize()
+
+
+@pytest.mark.parametrize("world", [6, 10, 12])
+def test_cpp_appendix_b_equals_oracle(S, world):
+    """Even non-power-of-2 n: the library's C++ Appendix-B generator vs the oracle."""
+    o = OS.generate_stragglar_even(world)
+    assert S.stragglar_schedule_rounds(world) == o.num_rounds
+    for r in range(o.num_rounds):
+        got = {(a, b, c, "reduce" if k == 0 else "replace") for a, b, c, k in S.stragglar_schedule_round(world, r)}
+        want = {(t.src, t.dst, t.chunk, t.kind) for t in o.rounds[r]}
+        assert got == want, (world, r)

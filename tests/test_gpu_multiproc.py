@@ -28,6 +28,7 @@ def _port():
     (2, 0, 65536, "bfloat16", "tma"),
     (4, 2, 250001, "int32", "tma"),
     (4, 0, 99999, "float32", "lsu"),
+    (6, 4, 123457, "bfloat16", "tma"),   # Appendix-B schedule (even non-power-of-2 n)
 ])
 def test_multiprocess_ipc(world, sigma, count, dtype, mover):
     if not torch.cuda.is_available():

@@ -74,7 +74,7 @@ def run_team(S, n, sigma, dtype, count, pattern="normal", config=1, algo="stragg
 
 
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("n", [2, 4, 6, 8])
 def test_every_straggler_small(S, dtype, n):
     """Every straggler rank; ragged counts (tails, fewer elements than chunks)."""
     for sigma in range(n):
@@ -84,7 +84,7 @@ def test_every_straggler_small(S, dtype, n):
 
 
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-@pytest.mark.parametrize("n,sigma", [(2, 1), (4, 0), (8, 0), (8, 3), (8, 7)])
+@pytest.mark.parametrize("n,sigma", [(2, 1), (4, 0), (6, 2), (8, 0), (8, 3), (8, 7)])
 def test_medium_spans_many_slices(S, dtype, n, sigma):
     """Sizes spanning every slice of every chunk plus a ragged tail."""
     for count in [(1 << 20) + 5, 10 ** 6 + 3]:
@@ -107,7 +107,7 @@ def test_patterns(S, pattern, dtype):
 
 
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("n", [2, 4, 6, 8])
 def test_ring_baseline(S, dtype, n):
     """The hand-written Ring against the ring-order oracle (per-hop rounding)."""
     for count in [3, 1001, (1 << 18) + 7]:
@@ -186,6 +186,8 @@ def test_argument_errors(S):
     S.stragglar_team_allreduce([torch.zeros(0, device="cuda") for _ in range(4)])  # count 0: no-op
     with pytest.raises(S.StragglarError):
         S.stragglar_team_init(3, 0)
+    with pytest.raises(S.StragglarError):
+        S.stragglar_team_init(10, 0)
 
 
 @pytest.mark.parametrize("n,sigma,count,dtype", [

@@ -58,4 +58,4 @@ def test_large_buffers_without_delay_prefer_ring_at_n8(S):
 
 def test_select_rejects_bad_world(S):
     with pytest.raises(S.StragglarError):
-        S.stragglar_select(6, 1.0, 0.0, 0.0, 1.0)
+        S.stragglar_select(5, 1.0, 0.0, 0.0, 1.0)
