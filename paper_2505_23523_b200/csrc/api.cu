@@ -51,9 +51,7 @@ struct Comm {
   bool team = false;
   int world = 0, rank = -1, sigma = -1, device = -1;
   int G = 0;
-  uint32_t epoch = 0;
-  uint32_t rs_epoch = 0;       // team: epoch of a Phase A awaiting its Phase B
-  bool rs_pending = false;
+  bool rs_pending = false;     // team: a Phase A awaits its Phase B (same call epoch)
   uint32_t* flags = nullptr;   // own flag array(s); team: world arrays back to back
   uint32_t* peer_flags[kMaxWorld] = {nullptr};
   bool imported = false;
@@ -150,7 +148,6 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   c.rank = team ? -1 : rank;
   c.sigma = sigma;
   c.team = team;
-  c.epoch = 0;
   c.rs_pending = false;
   c.timeout_ns = env_u64("STRAGGLAR_TIMEOUT_MS", 10000) * 1000000ull;
   const size_t per_rank = (size_t)kSlots * G * sizeof(uint32_t);
@@ -195,13 +192,15 @@ int slices_for(const Comm& c, uint64_t chunk_bytes) {
   return (int)g;
 }
 
-LaunchPlan base_plan(const Comm& c, size_t count, int dtype, uint32_t epoch) {
+// The call's epoch is not a launch parameter: kernels read state->epoch + 1 and
+// the last CTA of the call's final kernel bumps it (graph-capturable).
+LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
   LaunchPlan P;
   std::memset(&P, 0, sizeof(P));
   P.world = c.world;
   P.sigma = c.sigma;
   P.G = c.G;
-  P.epoch = epoch;
+  P.last_kernel = last_kernel ? 1 : 0;
   P.count = count;
   P.esize = esize_of(dtype);
   P.ce = chunk_elems(count, c.world - 1, P.esize);
@@ -249,9 +248,9 @@ int launch(int which, int dtype, const LaunchPlan& P, int nblocks, void* stream)
 }
 
 // team: Phase A over the non-stragglers (all in one launch)
-int team_rs(void* const* bufs, size_t count, int dtype, void* stream, uint32_t epoch) {
+int team_rs(void* const* bufs, size_t count, int dtype, void* stream) {
   Comm& c = g_team;
-  LaunchPlan P = base_plan(c, count, dtype, epoch);
+  LaunchPlan P = base_plan(c, count, dtype, false);
   for (int p = 0; p < c.world; ++p) P.buf[p] = (char*)bufs[p];
   int k = 0;
   for (int p = 0; p < c.world; ++p)
@@ -260,9 +259,9 @@ int team_rs(void* const* bufs, size_t count, int dtype, void* stream, uint32_t e
   return launch(K_RS, dtype, P, k * P.G, stream);
 }
 
-int team_b(void* const* bufs, size_t count, int dtype, void* stream, uint32_t epoch) {
+int team_b(void* const* bufs, size_t count, int dtype, void* stream) {
   Comm& c = g_team;
-  LaunchPlan P = base_plan(c, count, dtype, epoch);
+  LaunchPlan P = base_plan(c, count, dtype, true);
   for (int p = 0; p < c.world; ++p) {
     P.buf[p] = (char*)bufs[p];
     P.local_rank[p] = p;
@@ -436,7 +435,7 @@ int stragglar_import_buffer(void* buf, const void* blobs, int world) {
   return STRAGGLAR_OK;
 }
 
-static int proc_plan(void* buf, size_t count, int dtype, LaunchPlan* P, uint32_t epoch) {
+static int proc_plan(void* buf, size_t count, int dtype, LaunchPlan* P) {
   Comm& c = g_proc;
   const size_t bytes = count * esize_of(dtype);
   const Registration* reg = nullptr;
@@ -444,7 +443,7 @@ static int proc_plan(void* buf, size_t count, int dtype, LaunchPlan* P, uint32_t
     if ((char*)buf >= r.local && (char*)buf + bytes <= r.local + r.bytes) reg = &r;
   if (!reg) return STRAGGLAR_ERR_NOT_REGISTERED;
   const size_t delta = (char*)buf - reg->local;
-  *P = base_plan(c, count, dtype, epoch);
+  *P = base_plan(c, count, dtype, true);
   for (int p = 0; p < c.world; ++p) P->buf[p] = reg->peer[p] + delta;
   P->nlocal = 1;
   P->local_rank[0] = c.rank;
@@ -458,10 +457,12 @@ int stragglar_allreduce(void* buf, size_t count, int dtype, int op, void* stream
   int st = check_args(buf, count, dtype, op);
   if (st || count == 0) return st;
   LaunchPlan P;
-  if ((st = proc_plan(buf, count, dtype, &P, c.epoch + 1))) return st;
-  ++c.epoch;
-  if (c.rank != c.sigma)
+  if ((st = proc_plan(buf, count, dtype, &P))) return st;
+  if (c.rank != c.sigma) {
+    P.last_kernel = 0;
     if ((st = launch(K_RS, dtype, P, P.G, stream))) return st;
+    P.last_kernel = 1;
+  }
   return launch(K_COMPLETE, dtype, P, P.G, stream);
 }
 
@@ -472,8 +473,7 @@ int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* s
   int st = check_args(buf, count, dtype, op);
   if (st || count == 0) return st;
   LaunchPlan P;
-  if ((st = proc_plan(buf, count, dtype, &P, c.epoch + 1))) return st;
-  ++c.epoch;
+  if ((st = proc_plan(buf, count, dtype, &P))) return st;
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
   P.G = slices_for(c, P.ce * P.esize);
@@ -535,7 +535,7 @@ int stragglar_barrier(void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   Comm& c = g_proc;
   if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
-  LaunchPlan P = base_plan(c, 0, STRAGGLAR_INT32, ++c.epoch);
+  LaunchPlan P = base_plan(c, 0, STRAGGLAR_INT32, true);
   P.nlocal = 1;
   P.local_rank[0] = c.rank;
   if (launch_barrier(P, (cudaStream_t)stream) != cudaSuccess) return STRAGGLAR_ERR_CUDA;
@@ -580,9 +580,7 @@ int stragglar_team_reduce_scatter(void* const* bufs, size_t count, int dtype, in
   std::lock_guard<std::mutex> lk(g_mu);
   int st = team_check(bufs, count, dtype, op);
   if (st || count == 0) return st;
-  const uint32_t ep = ++g_team.epoch;
-  if ((st = team_rs(bufs, count, dtype, stream, ep))) return st;
-  g_team.rs_epoch = ep;
+  if ((st = team_rs(bufs, count, dtype, stream))) return st;
   g_team.rs_pending = true;
   return STRAGGLAR_OK;
 }
@@ -593,17 +591,16 @@ int stragglar_team_complete(void* const* bufs, size_t count, int dtype, int op, 
   if (st || count == 0) return st;
   if (!g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;   // Phase B needs its Phase A
   g_team.rs_pending = false;
-  return team_b(bufs, count, dtype, stream, g_team.rs_epoch);
+  return team_b(bufs, count, dtype, stream);
 }
 
 int stragglar_team_allreduce(void* const* bufs, size_t count, int dtype, int op, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   int st = team_check(bufs, count, dtype, op);
   if (st || count == 0) return st;
-  const uint32_t ep = ++g_team.epoch;
-  g_team.rs_pending = false;
-  if ((st = team_rs(bufs, count, dtype, stream, ep))) return st;
-  return team_b(bufs, count, dtype, stream, ep);
+  if (g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;   // finish the pending Phase A first
+  if ((st = team_rs(bufs, count, dtype, stream))) return st;
+  return team_b(bufs, count, dtype, stream);
 }
 
 int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, int op, void* stream) {
@@ -611,7 +608,8 @@ int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, in
   int st = team_check(bufs, count, dtype, op);
   if (st || count == 0) return st;
   Comm& c = g_team;
-  LaunchPlan P = base_plan(c, count, dtype, ++c.epoch);
+  if (c.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;   // a Phase A awaits its Phase B
+  LaunchPlan P = base_plan(c, count, dtype, true);
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
   P.G = slices_for(c, P.ce * P.esize);

@@ -59,6 +59,26 @@ __device__ __forceinline__ void cta_signal(uint32_t* f, uint32_t epoch, bool sys
   if (threadIdx.x == 0) st_release(f, epoch, sys);
 }
 
+// The call's epoch lives in device memory (state->epoch + 1), so a captured
+// CUDA graph replays correctly: the last CTA to leave the call's final kernel
+// increments it, after every CTA of every kernel of the call has read it.
+__device__ __forceinline__ uint32_t call_epoch(const LaunchPlan& P) {
+  return *(volatile const uint32_t*)&P.state->epoch + 1u;
+}
+__device__ __forceinline__ void finish_call(const LaunchPlan& P) {
+  if (!P.last_kernel) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t prev = atomicAdd(&P.state->exit_count, 1u);
+    if (prev == gridDim.x - 1) {
+      P.state->exit_count = 0;
+      __threadfence();
+      atomicAdd(&P.state->epoch, 1u);
+    }
+  }
+}
+
 __device__ __forceinline__ uint32_t* flag_at(uint32_t* base, int slot, int G, int s) {
   return base + (size_t)slot * G + s;
 }
@@ -386,15 +406,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_reduce_scatter(const _
   const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
   const int me = P.local_rank[li];
   const int G = P.G;
+  const uint32_t ep = call_epoch(P);
   if (blockIdx.x == 0 && threadIdx.x == 0) P.state->t_rs_start = globaltimer();
   // barrier (1) among the non-stragglers, per slice
   if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
-    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), P.epoch, P.sys_scope);
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep, P.sys_scope);
   if (threadIdx.x == 0) {
     bool ok = true;
     for (int p = 0; p < W && ok; ++p)
       if (p != me && p != P.sigma)
-        ok = spin_wait(flag_at(P.flags[me], SLOT_ARRIVE + p, G, s), P.epoch, P, 0x100 | p);
+        ok = spin_wait(flag_at(P.flags[me], SLOT_ARRIVE + p, G, s), ep, P, 0x100 | p);
     (void)ok;
   }
   if (!__syncthreads_and(*(volatile uint32_t*)&P.state->err == 0)) return;
@@ -419,7 +440,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_reduce_scatter(const _
     }
   }
   // "partial ready" for the straggler's half of the exchange
-  cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, G, s), P.epoch, P.sys_scope);
+  cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, G, s), ep, P.sys_scope);
 }
 
 // ---------------------------------------------------------------- Phase B
@@ -429,7 +450,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
   const int me = P.local_rank[li];
   const int G = P.G;
   const int V = 16 / P.esize;
-  const uint32_t ep = P.epoch;
+  const uint32_t ep = call_epoch(P);
   // the straggler reaches barrier (2): announce per slice to the others
   if (me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
     st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep, P.sys_scope);
@@ -447,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
     const uint64_t mid = sl.lo + (nvec_total / 2) * V < sl.hi ? sl.lo + (nvec_total / 2) * V : sl.hi;
     if (op.kind == OP_EXCH_LOW) {
       // non-straggler r: [lo, mid) of c_r = partial_r (+) x_sigma, stored at both ends
-      if (!cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, G, s), ep, P, 0x200 | k)) return;
+      if (!cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, G, s), ep, P, 0x200 | k)) break;
       const uint64_t a = sl.lo * P.esize, b = mid * P.esize;
       if constexpr (tma)
         tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, (b - a) / 16 * 16);
@@ -459,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
       cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep, P.sys_scope);
     } else if (op.kind == OP_EXCH_HIGH) {
       // straggler: [mid, hi) of c_r; waits for rank r's Phase-A partial
-      if (!cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, G, s), ep, P, 0x300 | k)) return;
+      if (!cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, G, s), ep, P, 0x300 | k)) break;
       const uint64_t a = mid * P.esize, b = sl.hi * P.esize;
       if constexpr (tma)
         tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, (b - a) / 16 * 16);
@@ -471,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
       cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep, P.sys_scope);
     } else {
       // copy of a fully reduced chunk (push)
-      if (!cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x400 | k)) return;
+      if (!cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x400 | k)) break;
       const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
       if constexpr (tma)
         tma_copy(pipe, P.buf[peer] + a, mine + a, (b - a) / 16 * 16);
@@ -486,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
     for (int c = 0; c < P.nchunks; ++c)
       if (!spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x500 | c)) break;
   }
-  __syncthreads();
+  finish_call(P);
 }
 
 // ---------------------------------------------------------------- Ring
@@ -499,7 +520,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
   const int j = P.local_rank[li];
   const int G = P.G;
   const int V = 16 / P.esize;
-  const uint32_t ep = P.epoch;
+  const uint32_t ep = call_epoch(P);
   const int left = (j + W - 1) % W, right = (j + 1) % W;
   if (threadIdx.x == 0) st_release(flag_at(P.flags[right], SLOT_RING_ARRIVE, G, s), ep, P.sys_scope);
   constexpr bool tma = MV == MOVER_TMA;
@@ -508,7 +529,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
   const char* lbuf = P.buf[left];
   for (int t = 0; t < 2 * (W - 1); ++t) {
     const int wslot = (t == 0) ? SLOT_RING_ARRIVE : SLOT_RING_READY + t - 1;
-    if (!cta_wait(flag_at(P.flags[j], wslot, G, s), ep, P, 0x600 | t)) return;
+    if (!cta_wait(flag_at(P.flags[j], wslot, G, s), ep, P, 0x600 | t)) {
+      finish_call(P);
+      return;
+    }
     const int k = (t < W - 1) ? ((j - 1 - t) % W + 2 * W) % W : ((j - t + W - 1) % W + 2 * W) % W;
     const Range cr = chunk_range(P, k);
     const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
@@ -533,6 +557,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
   // I am done reading the left buffer; wait until the right neighbour is done with mine
   cta_signal(flag_at(P.flags[left], SLOT_RING_DONE, G, s), ep, P.sys_scope);
   cta_wait(flag_at(P.flags[j], SLOT_RING_DONE, G, s), ep, P, 0x700);
+  finish_call(P);
 }
 
 // ---------------------------------------------------------------- delay / barrier
@@ -552,11 +577,12 @@ __global__ void k_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st) {
 
 __global__ void k_barrier(const __grid_constant__ LaunchPlan P) {
   const int me = P.local_rank[0];
+  const uint32_t ep = call_epoch(P);
   if (threadIdx.x < P.world && (int)threadIdx.x != me)
-    st_release(flag_at(P.flags[threadIdx.x], SLOT_BARRIER + me, P.G, 0), P.epoch, P.sys_scope);
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_BARRIER + me, P.G, 0), ep, P.sys_scope);
   if (threadIdx.x < P.world && (int)threadIdx.x != me)
-    spin_wait(flag_at(P.flags[me], SLOT_BARRIER + threadIdx.x, P.G, 0), P.epoch, P, 0x800 | threadIdx.x);
-  __syncthreads();
+    spin_wait(flag_at(P.flags[me], SLOT_BARRIER + threadIdx.x, P.G, 0), ep, P, 0x800 | threadIdx.x);
+  finish_call(P);
 }
 
 // ---------------------------------------------------------------- host launchers
@@ -600,7 +626,20 @@ cudaError_t launch_plan_kernel(int which, int dtype, const LaunchPlan& P, int nb
   void* fn = select_kernel(which, dtype, P.world, P.mover);
   if (!fn) return cudaErrorInvalidValue;
   void* args[] = {(void*)&P};
-  return cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(kThreads), args, dynamic_smem(which, P.mover), stream);
+  // cudaLaunchKernelEx with the cooperative attribute: co-residency of every
+  // CTA is guaranteed (they spin on each other's flags) and the launch can be
+  // captured into a CUDA graph.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nblocks);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = dynamic_smem(which, P.mover);
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 cudaError_t launch_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st, cudaStream_t stream) {

@@ -31,7 +31,9 @@ struct DevState {
   uint32_t err_info;
   uint64_t t_rs_start;   // %globaltimer at the start of the last Phase-A launch (team)
   uint64_t t_release;    // when the last injected delay released
-  uint64_t pad[5];
+  uint32_t epoch;        // calls completed; the running call uses epoch + 1
+  uint32_t exit_count;   // CTAs that finished the call's last kernel (reset by the last one)
+  uint64_t pad[4];
 };
 
 enum ErrCode : uint32_t { ERR_TIMEOUT = 1, ERR_BAD_PLAN = 2 };
@@ -48,7 +50,7 @@ struct LaunchPlan {
   int local_rank[kMaxWorld]; // physical rank of local index i (blockIdx.x / G)
   char* buf[kMaxWorld];      // data buffer of each physical rank (local or peer mapping)
   uint32_t* flags[kMaxWorld];// flag array of each physical rank
-  uint32_t epoch;
+  int last_kernel;            // 1: the call's final kernel; its last CTA to exit bumps state->epoch
   uint32_t pad0;
   uint64_t count;            // elements
   uint64_t ce;               // elements per chunk (chunks start at j*ce)

@@ -171,12 +171,56 @@ def test_host_entry_point(S):
     check_equal(outs, N.stragglar_allreduce(xs, sigma, dtype), xs, dtype, "host")
 
 
+def test_cuda_graph_replay(S):
+    """The call epoch lives in device memory, so a captured CUDA graph of the
+    whole AllReduce (Phase A, delay, Phase B) replays correctly; inputs are
+    refreshed in the static buffers between replays."""
+    n, sigma, dtype, count = 8, 6, "bfloat16", 200003
+    S.stragglar_team_init(n, sigma)
+    bufs = [torch.empty(count, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+    ring = [torch.empty_like(b) for b in bufs]
+    for b in bufs + ring:
+        b.zero_()
+    S.stragglar_team_allreduce(bufs)          # warm up outside capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            S.stragglar_team_reduce_scatter(bufs, side)
+            S.stragglar_team_inject_delay(5_000, side)
+            S.stragglar_team_complete(bufs, side)
+            S.stragglar_team_allreduce_ring(ring, side)
+    for it in range(3):
+        xs = make_inputs(n, count, dtype, config=30 + it)
+        for b, r, x in zip(bufs, ring, xs):
+            b.copy_(to_dev(x, dtype))
+            r.copy_(to_dev(x, dtype))
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        assert S.stragglar_team_check_error() == 0
+        check_equal([to_host(b, dtype) for b in bufs], N.stragglar_allreduce(xs, sigma, dtype), xs, dtype, f"graph {it}")
+        check_equal([to_host(b, dtype) for b in ring], N.ring_allreduce(xs, dtype), xs, dtype, f"graph ring {it}")
+    # eager calls still work after the replays (shared device epoch)
+    xs = make_inputs(n, count, dtype, config=40)
+    for b, x in zip(bufs, xs):
+        b.copy_(to_dev(x, dtype))
+    S.stragglar_team_allreduce(bufs)
+    torch.cuda.synchronize()
+    check_equal([to_host(b, dtype) for b in bufs], N.stragglar_allreduce(xs, sigma, dtype), xs, dtype, "eager after graph")
+
+
 def test_argument_errors(S):
     S.stragglar_team_init(4, 0)
     bufs = [torch.zeros(64, device="cuda") for _ in range(4)]
     with pytest.raises(S.StragglarError) as e:
         S.stragglar_team_complete(bufs)       # Phase B without Phase A
     assert e.value.status == 1
+    S.stragglar_team_reduce_scatter(bufs)
+    with pytest.raises(S.StragglarError):
+        S.stragglar_team_allreduce(bufs)      # Phase A pending: complete it first
+    S.stragglar_team_complete(bufs)
     mis = [torch.zeros(65, device="cuda")[1:] for _ in range(4)]
     with pytest.raises(S.StragglarError) as e:
         S.stragglar_team_allreduce(mis)       # not 16-byte aligned
