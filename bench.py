@@ -343,8 +343,17 @@ def bench_multi(args):
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    ndev = torch.cuda.device_count()
+    # more ranks than GPUs: a functional test of this path with ranks sharing a
+    # device (kernels time-slice; gloo plumbing; no NCCL baseline; numbers are
+    # not performance numbers)
+    shared = ndev < world
+    local = local % ndev
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     _, _, dtype, count, desc = WORKLOADS[args.workload]
     sigma = 0
     esize = ESIZE[dtype]
@@ -374,8 +383,9 @@ def bench_multi(args):
             res.append((e0, ea, e1))
         return res
 
-    algos = {"stragglar": lambda: comm.allreduce(buf), "ring": lambda: comm.allreduce_ring(ring),
-             "nccl": lambda: dist.all_reduce(nccl_buf)}
+    algos = {"stragglar": lambda: comm.allreduce(buf), "ring": lambda: comm.allreduce_ring(ring)}
+    if not shared:
+        algos["nccl"] = lambda: dist.all_reduce(nccl_buf)
     results = {}
     for name, fn in algos.items():
         timed(fn, args.warmup)
@@ -386,8 +396,9 @@ def bench_multi(args):
             evs = timed(fn, args.steps)
             torch.cuda.synchronize()
         launches = S.stragglar_launch_count() - l0
-        tot = torch.tensor([statistics.mean(e0.elapsed_time(e1) for e0, _, e1 in evs) * 1e3], device="cuda")
-        dly = torch.tensor([statistics.mean(e0.elapsed_time(ea) for e0, ea, _ in evs) * 1e3], device="cuda")
+        dev = "cpu" if shared else "cuda"
+        tot = torch.tensor([statistics.mean(e0.elapsed_time(e1) for e0, _, e1 in evs) * 1e3], device=dev)
+        dly = torch.tensor([statistics.mean(e0.elapsed_time(ea) for e0, ea, _ in evs) * 1e3], device=dev)
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
         dist.all_reduce(dly, op=dist.ReduceOp.MAX)
         results[name] = (tot.item(), dly.item(), launches, clk.summary())
@@ -412,9 +423,10 @@ def bench_multi(args):
             "algbw_GBps": round(S_bytes / (T_post * 1e-6) / 1e9, 1),
             "busbw_GBps": round(S_bytes / (T_post * 1e-6) / 1e9 * 2 * (world - 1) / world, 1),
             "ring_us": round(results["ring"][0] - results["ring"][1], 2),
-            "nccl_us": round(results["nccl"][0] - results["nccl"][1], 2),
+            "nccl_us": round(results["nccl"][0] - results["nccl"][1], 2) if "nccl" in results else None,
             "speedup_vs_ring_post": round((results["ring"][0] - results["ring"][1]) / T_post, 3),
-            "speedup_vs_nccl_post": round((results["nccl"][0] - results["nccl"][1]) / T_post, 3),
+            "speedup_vs_nccl_post": round((results["nccl"][0] - results["nccl"][1]) / T_post, 3) if "nccl" in results else None,
+            "shared_device_test": shared,
             "roofline": {"bound": "nvlink", "kernel": "k_complete (Phase B)", "achieved": round(achieved, 1),
                          "peak": NVLINK_PEER_MEASURED, "unit": "GB/s", "frac": round(achieved / NVLINK_PEER_MEASURED, 3),
                          "traffic": None, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction"},

@@ -19,30 +19,50 @@ FLAGS = [
 ]
 
 
+def source_digest(defines=()) -> str:
+    """Content hash of everything the library is built from (mtimes do not
+    survive the copy to the GPU box, contents do)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    deps = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC))
+    deps += [os.path.join(HERE, "..", "include", "stragglar.h"), os.path.abspath(__file__)]
+    for d in deps:
+        if os.path.isfile(d):
+            h.update(os.path.basename(d).encode())
+            h.update(open(d, "rb").read())
+    h.update(repr((FLAGS, tuple(defines))).encode())
+    return h.hexdigest()
+
+
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    stamp = LIB + ".sha256"
+    if not os.path.exists(LIB) or not os.path.exists(stamp):
         return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
-    deps.append(os.path.join(HERE, "..", "include", "stragglar.h"))
-    deps.append(os.path.abspath(__file__))
-    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+    return open(stamp).read().strip() != source_digest()
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB) -> str:
+    """defines: extra -D tuning knobs (STRAGGLAR_STAGES, STRAGGLAR_STAGE_BYTES,
+    STRAGGLAR_THREADS, STRAGGLAR_MIN_BLOCKS) for tuning variants built to `out`."""
+    if not force and not defines and out == LIB and not needs_build():
         return LIB
-    cmd = [NVCC, *FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
+    tmp = f"{out}.{os.getpid()}.tmp"        # concurrent builders (torchrun ranks) never share a temp file
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building libstragglar.so")
-    with open(os.path.join(HERE, "ptxas_report.txt"), "w") as f:
-        f.write(res.stderr)
+    if out == LIB:
+        with open(os.path.join(HERE, "ptxas_report.txt"), "w") as f:
+            f.write(res.stderr)
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(tmp, out)
+    if out == LIB:
+        with open(LIB + ".sha256", "w") as f:
+            f.write(source_digest())
+    return out
 
 
 if __name__ == "__main__":

@@ -109,7 +109,10 @@ __device__ __forceinline__ Range chunk_range(const LaunchPlan& P, int c) {
 
 // ---------------------------------------------------------------- data movers
 constexpr int kUnroll = 8;
-constexpr int kMinBlocks = 4;  // <= 64 registers: 4 CTAs of 256 threads per SM
+#ifndef STRAGGLAR_MIN_BLOCKS
+#define STRAGGLAR_MIN_BLOCKS 4
+#endif
+constexpr int kMinBlocks = STRAGGLAR_MIN_BLOCKS;  // 4 x 256 threads: <= 64 registers
 
 // dst <- src for 16-byte vectors [0, nv)
 __device__ __forceinline__ void copy_vecs(char* __restrict__ dst, const char* __restrict__ src, uint64_t nv) {
@@ -177,8 +180,14 @@ __device__ __forceinline__ void copy_tail(char* dst, const char* src, int nbytes
 // for the fused exchange every thread adds the two staged operands in shared
 // memory before the stores.  All threads track the per-stage mbarrier parity
 // identically, so the ring persists across the ops of a kernel.
-constexpr int kStages = 3;
-constexpr uint32_t kStageBytes = 16384;
+#ifndef STRAGGLAR_STAGES
+#define STRAGGLAR_STAGES 3
+#endif
+#ifndef STRAGGLAR_STAGE_BYTES
+#define STRAGGLAR_STAGE_BYTES 16384
+#endif
+constexpr int kStages = STRAGGLAR_STAGES;
+constexpr uint32_t kStageBytes = STRAGGLAR_STAGE_BYTES;
 constexpr int kTmaSmem = 128 + kStages * kStageBytes;
 
 struct Pipe {

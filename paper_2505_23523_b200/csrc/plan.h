@@ -22,7 +22,10 @@ enum Slot : int {
   kSlots = 48
 };
 
-constexpr int kThreads = 256;   // CTA size of the data kernels
+#ifndef STRAGGLAR_THREADS
+#define STRAGGLAR_THREADS 256
+#endif
+constexpr int kThreads = STRAGGLAR_THREADS;   // CTA size of the data kernels
 constexpr int kMaxSlices = 1024;
 
 // Device-resident per-communicator state (in the launching process's memory).

@@ -14,7 +14,7 @@ import os
 from typing import List, Optional, Sequence, Tuple
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libstragglar.so")
+LIB_PATH = os.environ.get("STRAGGLAR_LIB") or os.path.join(HERE, "libstragglar.so")  # override: tuning variants
 
 INT32, FLOAT32, BFLOAT16 = 0, 1, 2
 SUM = 0

@@ -1,0 +1,24 @@
+"""Build tuning variants of libstragglar.so into build/variants/ (travels with gpurun)."""
+import os
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2505_23523_b200 import build as B  # noqa: E402
+
+VARIANTS = {
+    "s3_16k": ["STRAGGLAR_STAGES=3", "STRAGGLAR_STAGE_BYTES=16384"],
+    "s4_12k": ["STRAGGLAR_STAGES=4", "STRAGGLAR_STAGE_BYTES=12288"],
+    "s6_8k": ["STRAGGLAR_STAGES=6", "STRAGGLAR_STAGE_BYTES=8192"],
+    "s2_24k": ["STRAGGLAR_STAGES=2", "STRAGGLAR_STAGE_BYTES=24576"],
+    "s4_16k": ["STRAGGLAR_STAGES=4", "STRAGGLAR_STAGE_BYTES=16384"],
+    "s3_32k": ["STRAGGLAR_STAGES=3", "STRAGGLAR_STAGE_BYTES=32768"],
+    "s3_16k_t512": ["STRAGGLAR_STAGES=3", "STRAGGLAR_STAGE_BYTES=16384", "STRAGGLAR_THREADS=512", "STRAGGLAR_MIN_BLOCKS=2"],
+    "s3_8k_t128": ["STRAGGLAR_STAGES=3", "STRAGGLAR_STAGE_BYTES=8192", "STRAGGLAR_THREADS=128", "STRAGGLAR_MIN_BLOCKS=8"],
+}
+os.makedirs(os.path.join(ROOT, "build", "variants"), exist_ok=True)
+with ThreadPoolExecutor(4) as ex:
+    futs = {k: ex.submit(B.build, True, False, v, os.path.join(ROOT, "build", "variants", f"lib_{k}.so")) for k, v in VARIANTS.items()}
+    for k, f in futs.items():
+        print(k, f.result())
