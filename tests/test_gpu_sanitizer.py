@@ -1,0 +1,32 @@
+"""compute-sanitizer memcheck and racecheck over small team-mode calls of
+every kernel (both movers), results checked against the oracle inside."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+@pytest.mark.parametrize("mover", ["tma", "lsu"])
+def test_sanitizer_clean(tool, mover):
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not installed")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    env = dict(os.environ, STRAGGLAR_MOVER=mover, STRAGGLAR_TIMEOUT_MS="120000")
+    r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "9", sys.executable,
+                        os.path.join(ROOT, "scripts", "sanitize_step.py")],
+                       env=env, capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-3000:]
+    assert "sanitize step ok" in out
