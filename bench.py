@@ -242,6 +242,24 @@ def bench_team(args):
     T_post = statistics.mean(e[2].elapsed_time(e[3]) * 1e3 for e in steps)
     T_post_sd = statistics.pstdev(e[2].elapsed_time(e[3]) * 1e3 for e in steps)
 
+    # NEXT row N1(ii): direct completion after the same Phase A and delay
+    def direct_step(evs):
+        evs[0].record()
+        S.stragglar_team_reduce_scatter(bufs)
+        S.stragglar_team_inject_delay(D_ns)
+        evs[1].record()
+        S.stragglar_team_complete_direct(bufs)
+        evs[2].record()
+
+    for _ in range(args.warmup):
+        direct_step([ev() for _ in range(3)])
+    dsteps = [[ev() for _ in range(3)] for _ in range(args.steps)]
+    torch.cuda._sleep(4_000_000)
+    for evs in dsteps:
+        direct_step(evs)
+    torch.cuda.synchronize()
+    T_direct = statistics.mean(e[1].elapsed_time(e[2]) * 1e3 for e in dsteps)
+
     # hand-written Ring, same buffers layout (bulk synchronous: starts after the straggler)
     for _ in range(args.warmup):
         S.stragglar_team_allreduce_ring(ring)
@@ -312,6 +330,13 @@ def bench_team(args):
         "speedup_vs_ring_post": round(T_ring / T_post, 3),
         "speedup_vs_ring_total": round((D_meas + T_ring) / T_tot, 3),
         "nccl": {"value": None, "why": "NCCL cannot run 8 ranks on one GPU; measured only in the N>1 mode"},
+        "direct_completion": {
+            "what": "NEXT row N1(ii): same Phase A + delay, then one-round direct completion (not the paper's schedule)",
+            "T_post_us": round(T_direct, 2),
+            "hbm_bytes": (world + 2) * (world - 1) * chunk_bytes(count, world - 1, esize),
+            "hbm_GBps": round((world + 2) * (world - 1) * chunk_bytes(count, world - 1, esize) / (T_direct * 1e-6) / 1e9, 1),
+            "speedup_vs_schedule_post": round(T_post / T_direct, 3),
+        },
         "phaseA_hbm_GBps": round(bytes_A / (T_A * 1e-6) / 1e9, 1),
         "ring_hbm_GBps": round(bytes_ring / (T_ring * 1e-6) / 1e9, 1),
         "roofline": {"bound": "hbm", "kernel": "k_complete (Phase B)", "achieved": round(achieved, 1),

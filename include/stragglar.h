@@ -117,6 +117,15 @@ int stragglar_allreduce(void* buf, size_t count, int dtype, int op, void* stream
 /* Hand-written Ring AllReduce baseline on the same transport:
  * 2(n-1) pull steps of ~count/n elements; bf16 partials rounded per hop. */
 int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* stream);
+/* NEXT row N1(ii): the same Phase A, then a one-round
+ * "direct completion" — each non-straggler owner g adds x_sigma to its
+ * partial c_g (the straggler exchange's single add) and stores
+ * the fully reduced chunk to every rank.  Valid on switched fabrics where a
+ * GPU can feed several peers at once (the paper's single-port model, P:149-150,
+ * does not hold on NVSwitch): ~S bytes per port instead of
+ * (n+log2 n-2)/(n-1)*S, one round instead of n+log2 n-2.  Result identical
+ * to stragglar_allreduce, bit for bit. */
+int stragglar_allreduce_direct(void* buf, size_t count, int dtype, int op, void* stream);
 /* Device-side barrier among all ranks of the communicator (bench start line). */
 int stragglar_barrier(void* stream);
 /* Bench only: a one-thread kernel that spins on %globaltimer for `ns`
@@ -139,6 +148,10 @@ int stragglar_team_allreduce(void* const* bufs, size_t count, int dtype, int op,
 int stragglar_team_reduce_scatter(void* const* bufs, size_t count, int dtype, int op, void* stream);
 int stragglar_team_complete(void* const* bufs, size_t count, int dtype, int op, void* stream);
 int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, int op, void* stream);
+/* Direct completion (see stragglar_allreduce_direct) after a team Phase A,
+ * and the whole direct-completion AllReduce. */
+int stragglar_team_complete_direct(void* const* bufs, size_t count, int dtype, int op, void* stream);
+int stragglar_team_allreduce_direct(void* const* bufs, size_t count, int dtype, int op, void* stream);
 /* Bench only: spin until `ns` nanoseconds after the start of the most
  * recent team Phase A launch (the straggler's arrival time). */
 int stragglar_team_inject_delay(uint64_t ns, void* stream);

@@ -210,6 +210,29 @@ def stragglar_allreduce(inputs: Sequence[np.ndarray], sigma_phys: int, dtype: st
     return bufs
 
 
+def direct_completion_allreduce(inputs: Sequence[np.ndarray], sigma_phys: int, dtype: str) -> List[np.ndarray]:
+    """NEXT row N1(ii): Phase A as in the paper, then one
+    round in which each owner g fully reduces its chunk (partial_g + x_sigma,
+    the same single add as the straggler exchange of P:164/P:206) and copies
+    it to every rank.  Valid when the fabric lets a rank send to several peers
+    at once (NVSwitch), which the paper's single-port model excludes
+    (P:149-150).  Same result as the pairwise schedule, bit for bit."""
+    n = len(inputs)
+    bufs = [np.array(x, copy=True) for x in inputs]
+    if n == 1:
+        return bufs
+    phys = logical_to_physical(n, sigma_phys)
+    phase_a_reduce_scatter(bufs, sigma_phys, dtype)
+    bounds = chunk_bounds(bufs[0].size, n - 1, dtype)
+    snapshot = [b.copy() for b in bufs]
+    for g in range(n - 1):
+        lo, hi = bounds[g]
+        full = add(snapshot[phys[g]][lo:hi], snapshot[sigma_phys][lo:hi], dtype)
+        for q in range(n):
+            bufs[q][lo:hi] = full
+    return bufs
+
+
 # --------------------------------------------------------------------------
 # Ring baseline (P:359-361), ring-order oracle
 # --------------------------------------------------------------------------

@@ -29,7 +29,7 @@ using namespace stragglar;
 
 namespace {
 
-enum { K_RS = 0, K_COMPLETE = 1, K_RING = 2 };
+enum { K_RS = 0, K_COMPLETE = 1, K_RING = 2, K_DIRECT = 3 };
 constexpr int kDefaultMover = MOVER_TMA;   // measured faster (profiles/r01)
 
 std::atomic<uint64_t> g_launches{0};
@@ -105,7 +105,7 @@ int resident_ctas(int world, int mover, int* sm_count) {
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
   int best = 1 << 30;
-  for (int which = 0; which < 3; ++which)
+  for (int which = 0; which < 4; ++which)
     for (int dt = 0; dt < 3; ++dt) {
       int b = 0;
       if (occupancy_blocks_per_sm(which, dt, world, mover, &b) != cudaSuccess) return -1;
@@ -259,7 +259,7 @@ int team_rs(void* const* bufs, size_t count, int dtype, void* stream) {
   return launch(K_RS, dtype, P, k * P.G, stream);
 }
 
-int team_b(void* const* bufs, size_t count, int dtype, void* stream) {
+int team_b(void* const* bufs, size_t count, int dtype, void* stream, int which = K_COMPLETE) {
   Comm& c = g_team;
   LaunchPlan P = base_plan(c, count, dtype, true);
   for (int p = 0; p < c.world; ++p) {
@@ -267,7 +267,7 @@ int team_b(void* const* bufs, size_t count, int dtype, void* stream) {
     P.local_rank[p] = p;
   }
   P.nlocal = c.world;
-  return launch(K_COMPLETE, dtype, P, c.world * P.G, stream);
+  return launch(which, dtype, P, c.world * P.G, stream);
 }
 
 int read_error(Comm& c, int* code) {
@@ -466,6 +466,22 @@ int stragglar_allreduce(void* buf, size_t count, int dtype, int op, void* stream
   return launch(K_COMPLETE, dtype, P, P.G, stream);
 }
 
+int stragglar_allreduce_direct(void* buf, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  int st = check_args(buf, count, dtype, op);
+  if (st || count == 0) return st;
+  LaunchPlan P;
+  if ((st = proc_plan(buf, count, dtype, &P))) return st;
+  if (c.rank != c.sigma) {
+    P.last_kernel = 0;
+    if ((st = launch(K_RS, dtype, P, P.G, stream))) return st;
+    P.last_kernel = 1;
+  }
+  return launch(K_DIRECT, dtype, P, P.G, stream);
+}
+
 int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   Comm& c = g_proc;
@@ -601,6 +617,24 @@ int stragglar_team_allreduce(void* const* bufs, size_t count, int dtype, int op,
   if (g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;   // finish the pending Phase A first
   if ((st = team_rs(bufs, count, dtype, stream))) return st;
   return team_b(bufs, count, dtype, stream);
+}
+
+int stragglar_team_complete_direct(void* const* bufs, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int st = team_check(bufs, count, dtype, op);
+  if (st || count == 0) return st;
+  if (!g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;
+  g_team.rs_pending = false;
+  return team_b(bufs, count, dtype, stream, K_DIRECT);
+}
+
+int stragglar_team_allreduce_direct(void* const* bufs, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int st = team_check(bufs, count, dtype, op);
+  if (st || count == 0) return st;
+  if (g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;
+  if ((st = team_rs(bufs, count, dtype, stream))) return st;
+  return team_b(bufs, count, dtype, stream, K_DIRECT);
 }
 
 int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, int op, void* stream) {

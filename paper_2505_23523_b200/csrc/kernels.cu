@@ -358,6 +358,84 @@ __device__ void tma_reduce(Pipe& p, char* dst, const char* const (&src)[W - 1], 
   p.phase = ph;
 }
 
+// a (+) b through shared memory, stored at offset lo_b of all W buffers
+template <int DT, int W>
+__device__ void tma_add_bcast(Pipe& p, char* const* dst, const char* a, const char* b, uint64_t lo_b,
+                              uint64_t nbytes) {
+  constexpr uint32_t kPiece = kStageBytes / 2;
+  const uint32_t np = (uint32_t)((nbytes + kPiece - 1) / kPiece);
+  auto piece_len = [&](uint32_t i) -> uint32_t {
+    const uint64_t off = (uint64_t)i * kPiece;
+    return (uint32_t)((nbytes - off) < kPiece ? (nbytes - off) : kPiece);
+  };
+  auto issue = [&](uint32_t i) {
+    const int s = i % kStages;
+    const uint64_t off = lo_b + (uint64_t)i * kPiece;
+    const uint32_t len = piece_len(i);
+    mbar_expect_tx(&p.bar[s], 2 * len);
+    bulk_load(p.buf(s), a + off, len, &p.bar[s]);
+    bulk_load(p.buf(s) + kPiece, b + off, len, &p.bar[s]);
+  };
+  if (threadIdx.x == 0 && np) {
+    fence_proxy_async_global();
+    for (uint32_t i = 0; i < np && i < (uint32_t)kStages; ++i) issue(i);
+  }
+  uint32_t ph = p.phase;
+  for (uint32_t i = 0; i < np; ++i) {
+    const int s = i % kStages;
+    const uint32_t len = piece_len(i);
+    mbar_wait(&p.bar[s], (ph >> s) & 1u);
+    ph ^= 1u << s;
+    uint4* A = reinterpret_cast<uint4*>(p.buf(s));
+    const uint4* B = reinterpret_cast<const uint4*>(p.buf(s) + kPiece);
+    for (uint32_t v = threadIdx.x; v < len / 16; v += blockDim.x) A[v] = add_vec<DT>(A[v], B[v]);
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint64_t off = lo_b + (uint64_t)i * kPiece;
+#pragma unroll
+      for (int d = 0; d < W; ++d) bulk_store(dst[d] + off, A, len);
+      bulk_commit();
+      if (i + kStages < np) {
+        bulk_wait_read_all();
+        issue(i + kStages);
+      }
+    }
+  }
+  if (threadIdx.x == 0 && np) {
+    bulk_wait_all();
+    fence_proxy_async_global();
+  }
+  p.phase = ph;
+}
+
+// LSU version of the same
+template <int DT, int W>
+__device__ void lsu_add_bcast(char* const* dst, const char* a, const char* b, uint64_t lo_b, uint64_t nbytes) {
+  const uint64_t nv = nbytes / 16;
+  constexpr int U = 4;
+  uint64_t i = threadIdx.x;
+  for (; i + (U - 1) * blockDim.x < nv; i += (uint64_t)U * blockDim.x) {
+    uint4 va[U], vb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      va[u] = ld_vec(a + lo_b + (i + u * blockDim.x) * 16);
+      vb[u] = ld_vec(b + lo_b + (i + u * blockDim.x) * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint4 z = add_vec<DT>(va[u], vb[u]);
+#pragma unroll
+      for (int d = 0; d < W; ++d) st_vec(dst[d] + lo_b + (i + u * blockDim.x) * 16, z);
+    }
+  }
+  for (; i < nv; i += blockDim.x) {
+    const uint4 z = add_vec<DT>(ld_vec(a + lo_b + i * 16), ld_vec(b + lo_b + i * 16));
+#pragma unroll
+    for (int d = 0; d < W; ++d) st_vec(dst[d] + lo_b + i * 16, z);
+  }
+}
+
 // ---------------------------------------------------------------- Phase A
 // Canonical sum of the slice over the non-stragglers in ascending physical order.
 template <int DT, int W>
@@ -519,6 +597,65 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
   finish_call(P);
 }
 
+// ---------------------------------------------------------------- direct completion (NEXT N1(ii))
+// One round instead of Algorithm 1's n + log n - 2: owner g (non-straggler)
+// fully reduces its chunk (partial + x_sigma, the straggler exchange's single
+// add) and stores the result to every rank.  On NVSwitch every
+// port then carries about S bytes (vs R*C = 9/7 S for the pairwise schedule at
+// n = 8): the fabric is not single-port (P:149-150 assumption).
+template <int DT, int W, int MV>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_direct(const __grid_constant__ LaunchPlan P) {
+  const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
+  const int me = P.local_rank[li];
+  const int G = P.G;
+  const int V = 16 / P.esize;
+  const uint32_t ep = call_epoch(P);
+  constexpr bool tma = MV == MOVER_TMA;
+  Pipe pipe = make_pipe(tma);
+  int own = -1;
+  if (me == P.sigma) {
+    // the straggler arrives: its buffer may now be read by every owner
+    if (threadIdx.x < W && (int)threadIdx.x != me)
+      st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep, P.sys_scope);
+  } else {
+    own = P.logical_of_phys[me];
+    if (cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + P.sigma, G, s), ep, P, 0x900)) {
+      const Range cr = chunk_range(P, own);
+      const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
+      const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
+      const uint64_t body = (b - a) / 16 * 16;
+      // every rank's buffer, own included, receives the fully reduced slice
+      if constexpr (tma)
+        tma_add_bcast<DT, W>(pipe, P.buf, P.buf[me], P.buf[P.sigma], a, body);
+      else
+        lsu_add_bcast<DT, W>(P.buf, P.buf[me], P.buf[P.sigma], a, body);
+      const int tail = (int)((b - a) % 16) / P.esize;
+      if ((int)threadIdx.x < tail) {
+        // read both operands before any store (the own buffer is a destination)
+        const uint64_t o = a + body + threadIdx.x * P.esize;
+        char tmp[4];
+        scalar_add_store<DT>(tmp, nullptr, P.buf[me] + o, P.buf[P.sigma] + o);
+#pragma unroll
+        for (int d = 0; d < W; ++d) {
+          if (P.esize == 2)
+            *(volatile uint16_t*)(P.buf[d] + o) = *reinterpret_cast<uint16_t*>(tmp);
+          else
+            *(volatile uint32_t*)(P.buf[d] + o) = *reinterpret_cast<uint32_t*>(tmp);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x < W && (int)threadIdx.x != me)
+        st_release(flag_at(P.flags[threadIdx.x], SLOT_HAVE + own, G, s), ep, P.sys_scope);
+    }
+  }
+  // postcondition: every other chunk has landed here
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < P.nchunks; ++c)
+      if (c != own && !spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0xA00 | c)) break;
+  }
+  finish_call(P);
+}
+
 // ---------------------------------------------------------------- Ring
 // Physical ring 0 -> 1 -> ... -> n-1 -> 0 with n chunks.  Step t < n-1: pull
 // the left neighbour's partial of chunk (j-1-t) and add the own data (RS);
@@ -601,13 +738,15 @@ static void* kernel_ptr(int which, int mover) {
     switch (which) {
       case 0: return (void*)k_reduce_scatter<DT, W, MOVER_TMA>;
       case 1: return (void*)k_complete<DT, W, MOVER_TMA>;
-      default: return (void*)k_ring<DT, W, MOVER_TMA>;
+      case 2: return (void*)k_ring<DT, W, MOVER_TMA>;
+      default: return (void*)k_direct<DT, W, MOVER_TMA>;
     }
   }
   switch (which) {
     case 0: return (void*)k_reduce_scatter<DT, W, MOVER_LSU>;
     case 1: return (void*)k_complete<DT, W, MOVER_LSU>;
-    default: return (void*)k_ring<DT, W, MOVER_LSU>;
+    case 2: return (void*)k_ring<DT, W, MOVER_LSU>;
+    default: return (void*)k_direct<DT, W, MOVER_LSU>;
   }
 }
 
@@ -629,7 +768,7 @@ void* select_kernel(int which, int dtype, int world, int mover) {
 #undef SEL
 }
 
-int dynamic_smem(int which, int mover) { return (which <= 2 && mover == MOVER_TMA) ? kTmaSmem : 0; }
+int dynamic_smem(int which, int mover) { return (which <= 3 && mover == MOVER_TMA) ? kTmaSmem : 0; }
 
 cudaError_t launch_plan_kernel(int which, int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream) {
   void* fn = select_kernel(which, dtype, P.world, P.mover);

@@ -55,6 +55,7 @@ _SIGS = {
     "stragglar_import_buffer": ([_vp, _vp, _c_int], _c_int),
     "stragglar_allreduce": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_allreduce_ring": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_allreduce_direct": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_barrier": ([_vp], _c_int),
     "stragglar_inject_delay": ([_c_u64, _vp], _c_int),
     "stragglar_check_error": ([ctypes.POINTER(_c_int)], _c_int),
@@ -68,6 +69,8 @@ _SIGS = {
     "stragglar_team_reduce_scatter": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_team_complete": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_team_allreduce_ring": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_team_complete_direct": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_team_allreduce_direct": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_team_inject_delay": ([_c_u64, _vp], _c_int),
     "stragglar_team_allreduce_host": ([_PP, _PP, _PP, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_team_slices": ([ctypes.POINTER(_c_int)], _c_int),
@@ -216,6 +219,11 @@ def stragglar_allreduce_auto(t, expected_delay_ns: int, stream=None) -> bool:
     return bool(used.value)
 
 
+def stragglar_allreduce_direct(t, stream=None) -> None:
+    _ck("stragglar_allreduce_direct",
+        _lib.stragglar_allreduce_direct(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream)))
+
+
 def stragglar_barrier(stream=None) -> None:
     _ck("stragglar_barrier", _lib.stragglar_barrier(_stream_ptr(stream)))
 
@@ -266,6 +274,14 @@ def stragglar_team_complete(bufs, stream=None) -> None:
 
 def stragglar_team_allreduce_ring(bufs, stream=None) -> None:
     _team_call("stragglar_team_allreduce_ring", bufs, stream)
+
+
+def stragglar_team_complete_direct(bufs, stream=None) -> None:
+    _team_call("stragglar_team_complete_direct", bufs, stream)
+
+
+def stragglar_team_allreduce_direct(bufs, stream=None) -> None:
+    _team_call("stragglar_team_allreduce_direct", bufs, stream)
 
 
 def stragglar_team_inject_delay(ns: int, stream=None) -> None:

@@ -34,7 +34,7 @@ def worker(rank, world, sigma, count, dtype, port, q):
         tdt = {"float32": torch.float32, "int32": torch.int32, "bfloat16": torch.bfloat16}[dtype]
         t = torch.empty(count, dtype=tdt, device="cuda")
         ring = torch.empty(count, dtype=tdt, device="cuda")
-        autos = [torch.empty(count, dtype=tdt, device="cuda") for _ in range(2)]
+        autos = [torch.empty(count, dtype=tdt, device="cuda") for _ in range(3)]
         comm.register(t)
         comm.register(ring)
         for a in autos:
@@ -53,6 +53,8 @@ def worker(rank, world, sigma, count, dtype, port, q):
         comm.allreduce_ring(ring)
         # NEXT row N2: selection for an expected delay (0 and 10 ms)
         used = [S.stragglar_allreduce_auto(autos[0], 0), S.stragglar_allreduce_auto(autos[1], 10_000_000)]
+        S.stragglar_allreduce_direct(autos[2])     # NEXT row N1(ii): same result as the schedule
+        used.append(True)
         torch.cuda.synchronize()
         err = S.stragglar_check_error()
         out = t.view(host.dtype).cpu().numpy()

@@ -65,6 +65,8 @@ def run_team(S, n, sigma, dtype, count, pattern="normal", config=1, algo="stragg
     S.stragglar_team_init(n, sigma)
     if algo == "stragglar":
         S.stragglar_team_allreduce(bufs)
+    elif algo == "direct":
+        S.stragglar_team_allreduce_direct(bufs)
     else:
         S.stragglar_team_allreduce_ring(bufs)
     torch.cuda.synchronize()
@@ -115,21 +117,39 @@ def test_ring_baseline(S, dtype, n):
         check_equal(outs, N.ring_allreduce(xs, dtype), xs, dtype, f"ring n={n} count={count}")
 
 
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+@pytest.mark.parametrize("n", [2, 4, 6, 8])
+def test_direct_completion(S, dtype, n):
+    """NEXT row N1(ii): Phase A + one-round direct completion; same bits as
+    the paper's schedule (oracle.numerics.direct_completion_allreduce =
+    plain definition), every straggler rank, ragged counts."""
+    for sigma in range(n):
+        for count in [3, 8 * (n - 1) + 5, 70001]:
+            xs, outs = run_team(S, n, sigma, dtype, count, algo="direct")
+            check_equal(outs, N.direct_completion_allreduce(xs, sigma, dtype), xs, dtype, f"direct n={n} s={sigma}")
+    xs, outs = run_team(S, n, n - 1, dtype, (1 << 20) + 3, algo="direct")
+    check_equal(outs, N.direct_completion_allreduce(xs, n - 1, dtype), xs, dtype, "direct large")
+
+
 def test_repeated_calls_and_phases(S):
     """Epoch flags across back-to-back calls (no reset, no cross-call hazard);
     Phase A + injected delay + Phase B as separate calls equals the one-call
     allreduce; ring calls interleaved."""
     n, sigma, dtype, count = 8, 2, "float32", 300001
     S.stragglar_team_init(n, sigma)
-    for it in range(4):
+    for it in range(6):
         xs = make_inputs(n, count, dtype, config=10 + it)
         bufs = [to_dev(x, dtype) for x in xs]
-        if it % 2 == 0:
+        if it % 3 == 0:
             S.stragglar_team_allreduce(bufs)
-        else:
+        elif it % 3 == 1:
             S.stragglar_team_reduce_scatter(bufs)
             S.stragglar_team_inject_delay(20_000)
             S.stragglar_team_complete(bufs)
+        else:
+            S.stragglar_team_reduce_scatter(bufs)
+            S.stragglar_team_inject_delay(20_000)
+            S.stragglar_team_complete_direct(bufs)
         ring = [to_dev(x, dtype) for x in xs]
         S.stragglar_team_allreduce_ring(ring)
         torch.cuda.synchronize()

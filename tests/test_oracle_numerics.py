@@ -207,3 +207,15 @@ def test_tolerance_function():
     ref = np.array([4.0, 0.0], np.float32)
     got = np.array([4.0, 4e-6], np.float32)
     assert N.rel_error_vs_abs_sum(got, ref, xs, "float32") == pytest.approx(1e-6, rel=1e-3)
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("n", [2, 4, 6, 8])
+def test_direct_completion_equals_definition(dtype, n):
+    """N1(ii): Phase A + one direct completion round reaches the plain
+    definition bitwise (and therefore the pairwise schedule's result)."""
+    xs = make_inputs(n, 2049, dtype, config=99)
+    for sig in range(n):
+        want = N.plain_allreduce(xs, sig, dtype)
+        for o in N.direct_completion_allreduce(xs, sig, dtype):
+            assert np.array_equal(_bits(o), _bits(want))
