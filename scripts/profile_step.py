@@ -25,6 +25,8 @@ for _ in range(steps):
     S.stragglar_team_inject_delay(10_000)
     S.stragglar_team_complete(bufs)
     S.stragglar_team_allreduce_ring(bufs)
+    S.stragglar_team_reduce_scatter(bufs)
+    S.stragglar_team_complete_direct(bufs)
 torch.cuda.synchronize()
 assert S.stragglar_team_check_error() == 0
 print("profile step ok", S.stragglar_launch_count())
