@@ -271,3 +271,52 @@ def test_baseline_configs_exact(S, n, sigma, count, dtype):
     torch.cuda.synchronize()
     assert S.stragglar_team_check_error() == 0
     check_equal([to_host(b, dtype) for b in bufs], N.stragglar_allreduce(xs, sigma, dtype), xs, dtype, "config")
+
+
+def test_huge_buffers_sampled(S):
+    """Maximum sizes: 3 GiB per rank (> 2^31 bytes, 24 GiB over the 8 ranks),
+    inputs drawn on the device from seeded generators; the plain definition
+    is evaluated by the oracle on 200k sampled indices (chunk and slice
+    boundaries included) and every rank must be bitwise identical."""
+    n, sigma = 8, 2
+    count = (3 << 30) // 4 + 7
+    S.stragglar_team_init(n, sigma)
+    bufs = []
+    for p in range(n):
+        g = torch.Generator(device="cuda").manual_seed(2505_23523 + p)
+        bufs.append(torch.randn(count, device="cuda", generator=g))
+    ce = N.chunk_elems(count, n - 1, "float32")
+    edges = [0, 1, count - 1, count - 2, (1 << 29) - 1, 1 << 29, (1 << 31) // 4, ((1 << 31) // 4) + 1]
+    edges += [j * ce + d for j in range(1, n - 1) for d in (-1, 0, 1)]
+    rng = np.random.default_rng(7)
+    idx = np.unique(np.concatenate([np.array(edges), rng.integers(0, count, 200_000)]))
+    tidx = torch.from_numpy(idx).cuda()
+    xs = [b[tidx].cpu().numpy() for b in bufs]
+    S.stragglar_team_reduce_scatter(bufs)
+    S.stragglar_team_inject_delay(100_000)
+    S.stragglar_team_complete(bufs)
+    torch.cuda.synchronize()
+    assert S.stragglar_team_check_error() == 0
+    want = N.plain_allreduce(xs, sigma, "float32")
+    for p in range(n):
+        got = bufs[p][tidx].cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), p
+    for p in range(1, n):
+        assert torch.equal(bufs[p].view(torch.int32), bufs[0].view(torch.int32))
+    del bufs
+    torch.cuda.empty_cache()
+
+
+def test_randomized_cases(S):
+    """Seeded random sweep: world, straggler, dtype, count, pattern, algorithm."""
+    rng = np.random.default_rng(2505)
+    for case in range(40):
+        n = int(rng.choice([2, 4, 6, 8]))
+        sigma = int(rng.integers(0, n))
+        dtype = str(rng.choice(["int32", "float32", "bfloat16"]))
+        count = int(rng.choice([rng.integers(1, 64), rng.integers(64, 5000), rng.integers(5000, 600_000)]))
+        pattern = str(rng.choice(["normal", "intval", "bitmask"]))
+        algo = str(rng.choice(["stragglar", "direct", "ring"]))
+        xs, outs = run_team(S, n, sigma, dtype, count, pattern=pattern, config=60 + case, algo=algo)
+        want = N.ring_allreduce(xs, dtype) if algo == "ring" else N.stragglar_allreduce(xs, sigma, dtype)
+        check_equal(outs, want, xs, dtype, f"case {case}: n={n} s={sigma} {dtype} {count} {pattern} {algo}")
