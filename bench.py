@@ -339,7 +339,7 @@ def bench_team(args):
         },
         "phaseA_hbm_GBps": round(bytes_A / (T_A * 1e-6) / 1e9, 1),
         "ring_hbm_GBps": round(bytes_ring / (T_ring * 1e-6) / 1e9, 1),
-        "roofline": {"bound": "hbm", "kernel": "k_complete (Phase B)", "achieved": round(achieved, 1),
+        "roofline": {"bound": "hbm", "kernel": "k_phase<..., KIND=1> (Phase B, Algorithm 1 schedule)", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 3), "traffic": traffic,
                      "algorithmic_bytes": bytes_B, "peak_source": peak_src},
         "cpu_baseline": cpu,
@@ -452,7 +452,7 @@ def bench_multi(args):
             "speedup_vs_ring_post": round((results["ring"][0] - results["ring"][1]) / T_post, 3),
             "speedup_vs_nccl_post": round((results["nccl"][0] - results["nccl"][1]) / T_post, 3) if "nccl" in results else None,
             "shared_device_test": shared,
-            "roofline": {"bound": "nvlink", "kernel": "k_complete (Phase B)", "achieved": round(achieved, 1),
+            "roofline": {"bound": "nvlink", "kernel": "k_phase<..., KIND=4> (Phase A + B)", "achieved": round(achieved, 1),
                          "peak": NVLINK_PEER_MEASURED, "unit": "GB/s", "frac": round(achieved / NVLINK_PEER_MEASURED, 3),
                          "traffic": None, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction"},
             "cpu_baseline": None,

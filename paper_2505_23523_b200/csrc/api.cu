@@ -29,7 +29,7 @@ using namespace stragglar;
 
 namespace {
 
-enum { K_RS = 0, K_COMPLETE = 1, K_RING = 2, K_DIRECT = 3 };
+enum { K_RS = 0, K_COMPLETE = 1, K_RING = 2, K_DIRECT = 3, K_FUSED = 4, K_FUSED_DIRECT = 5 };
 constexpr int kDefaultMover = MOVER_TMA;   // measured faster (profiles/r01)
 
 std::atomic<uint64_t> g_launches{0};
@@ -105,7 +105,7 @@ int resident_ctas(int world, int mover, int* sm_count) {
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
   int best = 1 << 30;
-  for (int which = 0; which < 4; ++which)
+  for (int which = 0; which < 6; ++which)
     for (int dt = 0; dt < 3; ++dt) {
       int b = 0;
       if (occupancy_blocks_per_sm(which, dt, world, mover, &b) != cudaSuccess) return -1;
@@ -458,12 +458,9 @@ int stragglar_allreduce(void* buf, size_t count, int dtype, int op, void* stream
   if (st || count == 0) return st;
   LaunchPlan P;
   if ((st = proc_plan(buf, count, dtype, &P))) return st;
-  if (c.rank != c.sigma) {
-    P.last_kernel = 0;
-    if ((st = launch(K_RS, dtype, P, P.G, stream))) return st;
-    P.last_kernel = 1;
-  }
-  return launch(K_COMPLETE, dtype, P, P.G, stream);
+  // one persistent launch: non-stragglers run Phase A then Phase B, the
+  // straggler Phase B only (its delay is whatever precedes it on its stream)
+  return launch(K_FUSED, dtype, P, P.G, stream);
 }
 
 int stragglar_allreduce_direct(void* buf, size_t count, int dtype, int op, void* stream) {
@@ -474,12 +471,7 @@ int stragglar_allreduce_direct(void* buf, size_t count, int dtype, int op, void*
   if (st || count == 0) return st;
   LaunchPlan P;
   if ((st = proc_plan(buf, count, dtype, &P))) return st;
-  if (c.rank != c.sigma) {
-    P.last_kernel = 0;
-    if ((st = launch(K_RS, dtype, P, P.G, stream))) return st;
-    P.last_kernel = 1;
-  }
-  return launch(K_DIRECT, dtype, P, P.G, stream);
+  return launch(K_FUSED_DIRECT, dtype, P, P.G, stream);
 }
 
 int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* stream) {
@@ -615,8 +607,7 @@ int stragglar_team_allreduce(void* const* bufs, size_t count, int dtype, int op,
   int st = team_check(bufs, count, dtype, op);
   if (st || count == 0) return st;
   if (g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;   // finish the pending Phase A first
-  if ((st = team_rs(bufs, count, dtype, stream))) return st;
-  return team_b(bufs, count, dtype, stream);
+  return team_b(bufs, count, dtype, stream, K_FUSED);        // Phase A + B in one launch
 }
 
 int stragglar_team_complete_direct(void* const* bufs, size_t count, int dtype, int op, void* stream) {
@@ -633,8 +624,7 @@ int stragglar_team_allreduce_direct(void* const* bufs, size_t count, int dtype, 
   int st = team_check(bufs, count, dtype, op);
   if (st || count == 0) return st;
   if (g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;
-  if ((st = team_rs(bufs, count, dtype, stream))) return st;
-  return team_b(bufs, count, dtype, stream, K_DIRECT);
+  return team_b(bufs, count, dtype, stream, K_FUSED_DIRECT);
 }
 
 int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, int op, void* stream) {

@@ -1,14 +1,18 @@
 // StragglAR kernels for sm_100a.
 //
-//   k_reduce_scatter  Phase A: owner g pulls its chunk
-//                     from the n-2 other non-stragglers, sums in canonical
-//                     order (ascending physical rank, fp32 accumulation) and
-//                     stores in place.  Replaces ncclReduceScatter.
-//   k_complete        Phase B (Algorithm 1): a persistent round
-//                     executor.  Each CTA owns one slice of every chunk and
-//                     walks its rank's op list in round order.  The straggler
-//                     exchange is fused with its reduction (P:347
-//                     "separate kernels for reduction" become one pass).
+//   k_phase<..., KIND> one persistent kernel template for the method:
+//     KIND 0  Phase A: owner g pulls its chunk from the
+//             n-2 other non-stragglers, sums in canonical order (ascending
+//             physical rank, fp32 accumulation), stores in place.  Replaces
+//             ncclReduceScatter.                      [rs_body]
+//     KIND 1  Phase B (Algorithm 1): round executor; each CTA owns
+//             one slice of every chunk and walks its rank's op list in round
+//             order; the straggler exchange is fused with its
+//             reduction (P:347's separate reduction kernels become one pass).
+//                                                              [complete_body]
+//     KIND 3  Phase B as a one-round direct completion (NEXT N1(ii)). [direct_body]
+//     KIND 4  Phase A then Phase B (schedule) in one launch (single-call API).
+//     KIND 5  Phase A then direct completion in one launch.
 //   k_ring            hand-written Ring baseline, pull-based.
 //   k_delay           the paper's idle kernel on %globaltimer.
 //   k_barrier         device barrier among ranks (bench start line).
@@ -488,12 +492,10 @@ __device__ void rs_slice(const LaunchPlan& P, const char* const (&src)[W - 1], c
   }
 }
 
+// Phase A body for non-straggler `me`, slice s.
 template <int DT, int W, int MV>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_reduce_scatter(const __grid_constant__ LaunchPlan P) {
-  const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
-  const int me = P.local_rank[li];
+__device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
   const int G = P.G;
-  const uint32_t ep = call_epoch(P);
   if (blockIdx.x == 0 && threadIdx.x == 0) P.state->t_rs_start = globaltimer();
   // barrier (1) among the non-stragglers, per slice
   if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
@@ -517,7 +519,6 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_reduce_scatter(const _
   // with two ranks the owner's chunk already is the non-straggler "sum"
   if constexpr (W > 2) {
     if constexpr (MV == MOVER_TMA) {
-      Pipe pipe = make_pipe(true);
       const uint64_t lo_b = r.lo * P.esize, hi_b = r.hi * P.esize;
       const uint64_t body = (hi_b - lo_b) / 16 * 16;
       tma_reduce<DT, W>(pipe, P.buf[me], src, lo_b, body);
@@ -530,20 +531,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_reduce_scatter(const _
   cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, G, s), ep, P.sys_scope);
 }
 
-// ---------------------------------------------------------------- Phase B
+// Phase B body (Algorithm 1 round executor) for rank `me`, slice s.
 template <int DT, int W, int MV>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_constant__ LaunchPlan P) {
-  const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
-  const int me = P.local_rank[li];
+__device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
   const int G = P.G;
   const int V = 16 / P.esize;
-  const uint32_t ep = call_epoch(P);
+  constexpr bool tma = MV == MOVER_TMA;
   // the straggler reaches barrier (2): announce per slice to the others
   if (me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
     st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep, P.sys_scope);
-
-  constexpr bool tma = MV == MOVER_TMA;
-  Pipe pipe = make_pipe(tma);
   char* mine = P.buf[me];
   const int nops = P.nops[me];
   for (int k = 0; k < nops; ++k) {
@@ -594,24 +590,19 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_complete(const __grid_
     for (int c = 0; c < P.nchunks; ++c)
       if (!spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x500 | c)) break;
   }
-  finish_call(P);
 }
 
-// ---------------------------------------------------------------- direct completion (NEXT N1(ii))
-// One round instead of Algorithm 1's n + log n - 2: owner g (non-straggler)
-// fully reduces its chunk (partial + x_sigma, the straggler exchange's single
-// add) and stores the result to every rank.  On NVSwitch every
-// port then carries about S bytes (vs R*C = 9/7 S for the pairwise schedule at
-// n = 8): the fabric is not single-port (P:149-150 assumption).
+// Direct completion body (NEXT N1(ii)): one round instead of Algorithm 1's
+// n + log n - 2.  Owner g (non-straggler) fully reduces its chunk (partial +
+// x_sigma, the straggler exchange's single add) and stores the
+// result to every rank.  On NVSwitch every port then carries about S bytes
+// (vs R*C = 9/7 S for the pairwise schedule at n = 8): the fabric is not
+// single-port (the P:149-150 assumption).
 template <int DT, int W, int MV>
-__global__ void __launch_bounds__(kThreads, kMinBlocks) k_direct(const __grid_constant__ LaunchPlan P) {
-  const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
-  const int me = P.local_rank[li];
+__device__ void direct_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
   const int G = P.G;
   const int V = 16 / P.esize;
-  const uint32_t ep = call_epoch(P);
   constexpr bool tma = MV == MOVER_TMA;
-  Pipe pipe = make_pipe(tma);
   int own = -1;
   if (me == P.sigma) {
     // the straggler arrives: its buffer may now be read by every owner
@@ -653,6 +644,20 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_direct(const __grid_co
     for (int c = 0; c < P.nchunks; ++c)
       if (c != own && !spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0xA00 | c)) break;
   }
+}
+
+// KIND: 0 Phase A only, 1 Phase B (schedule), 3 Phase B (direct),
+//       4 Phase A + schedule in one launch, 5 Phase A + direct in one launch.
+template <int DT, int W, int MV, int KIND>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_constant__ LaunchPlan P) {
+  const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
+  const int me = P.local_rank[li];
+  const uint32_t ep = call_epoch(P);
+  Pipe pipe = make_pipe(MV == MOVER_TMA);
+  if constexpr (KIND == 0 || KIND == 4 || KIND == 5)
+    if (me != P.sigma) rs_body<DT, W, MV>(P, pipe, s, me, ep);
+  if constexpr (KIND == 1 || KIND == 4) complete_body<DT, W, MV>(P, pipe, s, me, ep);
+  if constexpr (KIND == 3 || KIND == 5) direct_body<DT, W, MV>(P, pipe, s, me, ep);
   finish_call(P);
 }
 
@@ -732,22 +737,22 @@ __global__ void k_barrier(const __grid_constant__ LaunchPlan P) {
 }
 
 // ---------------------------------------------------------------- host launchers
+template <int DT, int W, int MV>
+static void* kernel_ptr_mv(int which) {
+  switch (which) {
+    case 0: return (void*)k_phase<DT, W, MV, 0>;   // Phase A
+    case 1: return (void*)k_phase<DT, W, MV, 1>;   // Phase B, Algorithm 1 schedule
+    case 2: return (void*)k_ring<DT, W, MV>;
+    case 3: return (void*)k_phase<DT, W, MV, 3>;   // Phase B, direct completion
+    case 4: return (void*)k_phase<DT, W, MV, 4>;   // A + B (schedule), one launch
+    case 5: return (void*)k_phase<DT, W, MV, 5>;   // A + B (direct), one launch
+    default: return nullptr;
+  }
+}
+
 template <int DT, int W>
 static void* kernel_ptr(int which, int mover) {
-  if (mover == MOVER_TMA) {
-    switch (which) {
-      case 0: return (void*)k_reduce_scatter<DT, W, MOVER_TMA>;
-      case 1: return (void*)k_complete<DT, W, MOVER_TMA>;
-      case 2: return (void*)k_ring<DT, W, MOVER_TMA>;
-      default: return (void*)k_direct<DT, W, MOVER_TMA>;
-    }
-  }
-  switch (which) {
-    case 0: return (void*)k_reduce_scatter<DT, W, MOVER_LSU>;
-    case 1: return (void*)k_complete<DT, W, MOVER_LSU>;
-    case 2: return (void*)k_ring<DT, W, MOVER_LSU>;
-    default: return (void*)k_direct<DT, W, MOVER_LSU>;
-  }
+  return mover == MOVER_TMA ? kernel_ptr_mv<DT, W, MOVER_TMA>(which) : kernel_ptr_mv<DT, W, MOVER_LSU>(which);
 }
 
 void* select_kernel(int which, int dtype, int world, int mover) {
@@ -768,7 +773,7 @@ void* select_kernel(int which, int dtype, int world, int mover) {
 #undef SEL
 }
 
-int dynamic_smem(int which, int mover) { return (which <= 3 && mover == MOVER_TMA) ? kTmaSmem : 0; }
+int dynamic_smem(int which, int mover) { return (which <= 5 && mover == MOVER_TMA) ? kTmaSmem : 0; }
 
 cudaError_t launch_plan_kernel(int which, int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream) {
   void* fn = select_kernel(which, dtype, P.world, P.mover);

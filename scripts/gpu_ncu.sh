@@ -9,7 +9,10 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 # the launch list of the bench command itself (cold-cache, serialised: shares, not absolutes)
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_bench_launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/${TAG}_bench_under_ncu.log 2>&1; echo "bench launches rc=$?"
-for k in k_complete k_reduce_scatter k_ring k_direct; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
+# kernel-name regexes on the demangled names: k_phase<dtype, world, mover, KIND>
+declare -A PAT=( [phaseB]='k_phase<.*, 1>' [phaseA]='k_phase<.*, 0>' [ring]='k_ring<' [direct]='k_phase<.*, 3>' )
+for k in phaseB phaseA ring direct; do
+  timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+      -k "regex:${PAT[$k]}" -s 1 -c 1 \
       -o gpurun_out/${TAG}_$k python scripts/profile_step.py > gpurun_out/${TAG}_$k.log 2>&1; echo "$k rc=$?"
 done
