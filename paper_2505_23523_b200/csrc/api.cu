@@ -663,16 +663,51 @@ int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_
     if ((st = team_check(bufs, count, dtype, op))) return st;
   }
   if (count == 0) return STRAGGLAR_OK;
-  const size_t bytes = count * esize_of(dtype);
-  cudaStream_t s = (cudaStream_t)stream;
-  for (int p = 0; p < g_team.world; ++p) {
+  const int world = g_team.world;
+  for (int p = 0; p < world; ++p)
     if (!host_in[p] || !host_out[p]) return STRAGGLAR_ERR_INVALID_ARG;
-    CK(cudaMemcpyAsync(bufs[p], host_in[p], bytes, cudaMemcpyHostToDevice, s));
+  const int es = esize_of(dtype);
+  cudaStream_t s = (cudaStream_t)stream;
+  // The SUM is elementwise, so the buffer is processed in pieces through a
+  // three-stage pipeline: H2D of piece k+1 (copy engine, one direction), the
+  // AllReduce of piece k (SMs) and D2H of piece k-1 (copy engine, the other
+  // direction) overlap.  Pieces keep 16-byte alignment.
+  const uint64_t v = 16 / es;
+  uint64_t piece = env_u64("STRAGGLAR_E2E_PIECE_BYTES", 32ull << 20) / es;
+  piece = piece / v * v;
+  if (piece == 0) piece = v;
+  const uint64_t npieces = (count + piece - 1) / piece;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  CK(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> ev(3 * npieces + 1, nullptr);
+  for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev.back(), s));               // everything earlier on `stream` first
+  CK(cudaStreamWaitEvent(h2d, ev.back(), 0));
+  std::vector<void*> sub(world);
+  st = STRAGGLAR_OK;
+  for (uint64_t k = 0; k < npieces && st == STRAGGLAR_OK; ++k) {
+    const uint64_t off = k * piece, n = (count - off) < piece ? (count - off) : piece;
+    const size_t boff = off * es, bytes = n * es;
+    for (int p = 0; p < world; ++p)
+      CK(cudaMemcpyAsync((char*)bufs[p] + boff, (const char*)host_in[p] + boff, bytes, cudaMemcpyHostToDevice, h2d));
+    CK(cudaEventRecord(ev[3 * k], h2d));
+    CK(cudaStreamWaitEvent(s, ev[3 * k], 0));
+    for (int p = 0; p < world; ++p) sub[p] = (char*)bufs[p] + boff;
+    st = stragglar_team_allreduce(sub.data(), n, dtype, op, stream);
+    CK(cudaEventRecord(ev[3 * k + 1], s));
+    CK(cudaStreamWaitEvent(d2h, ev[3 * k + 1], 0));
+    for (int p = 0; p < world; ++p)
+      CK(cudaMemcpyAsync((char*)host_out[p] + boff, (char*)bufs[p] + boff, bytes, cudaMemcpyDeviceToHost, d2h));
+    CK(cudaEventRecord(ev[3 * k + 2], d2h));
   }
-  if ((st = stragglar_team_allreduce(bufs, count, dtype, op, stream))) return st;
-  for (int p = 0; p < g_team.world; ++p) CK(cudaMemcpyAsync(host_out[p], bufs[p], bytes, cudaMemcpyDeviceToHost, s));
+  if (npieces) CK(cudaStreamWaitEvent(s, ev[3 * (npieces - 1) + 2], 0));
   CK(cudaStreamSynchronize(s));
-  return STRAGGLAR_OK;
+  CK(cudaStreamSynchronize(d2h));
+  for (auto& e : ev) cudaEventDestroy(e);
+  cudaStreamDestroy(h2d);
+  cudaStreamDestroy(d2h);
+  return st;
 }
 
 int stragglar_team_check_error(int* code) {

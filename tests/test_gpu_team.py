@@ -178,17 +178,31 @@ def test_all_ranks_identical_full_size(S):
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
-def test_host_entry_point(S):
-    """End-to-end C-ABI call from pinned host buffers."""
+@pytest.mark.parametrize("piece_bytes", [None, "4096", "100000"])
+def test_host_entry_point(S, piece_bytes):
+    """End-to-end C-ABI call from pinned host buffers; with small pieces the
+    H2D / AllReduce / D2H pipeline runs many overlapped pieces (ragged last
+    piece included) and must give the same bits."""
     n, sigma, dtype, count = 4, 1, "bfloat16", 123457
     xs = make_inputs(n, count, dtype, config=3)
     host = [torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory() for x in xs]
     out = [torch.empty_like(h).pin_memory() for h in host]
     dev = [torch.empty(count, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
     S.stragglar_team_init(n, sigma)
-    S.stragglar_team_allreduce_host(host, out, dev)
+    old = os.environ.pop("STRAGGLAR_E2E_PIECE_BYTES", None)
+    if piece_bytes:
+        os.environ["STRAGGLAR_E2E_PIECE_BYTES"] = piece_bytes
+    try:
+        S.stragglar_team_allreduce_host(host, out, dev)
+    finally:
+        os.environ.pop("STRAGGLAR_E2E_PIECE_BYTES", None)
+        if old is not None:
+            os.environ["STRAGGLAR_E2E_PIECE_BYTES"] = old
     outs = [o.view(torch.int16).numpy().view(np.uint16) for o in out]
     check_equal(outs, N.stragglar_allreduce(xs, sigma, dtype), xs, dtype, "host")
+    S.stragglar_team_allreduce_host(host, host, dev)          # in place on the host
+    check_equal([h.view(torch.int16).numpy().view(np.uint16) for h in host],
+                N.stragglar_allreduce(xs, sigma, dtype), xs, dtype, "host in place")
 
 
 def test_cuda_graph_replay(S):
