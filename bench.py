@@ -345,7 +345,8 @@ def bench_team(args):
         "cpu_baseline": cpu,
         "e2e": {"value": round(E2E, 1), "unit": "us", "h2d_bytes_per_step": world * S_bytes,
                 "d2h_bytes_per_step": world * S_bytes,
-                "what": "stragglar_team_allreduce_host: pinned host -> HBM, Phase A+B, HBM -> host (no delay)"},
+                "what": "stragglar_team_allreduce_host: pinned host -> HBM, Phase A+B, HBM -> host (no delay), "
+                        "pipelined over 8 MiB pieces (H2D / AllReduce / D2H overlap)"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

@@ -158,7 +158,7 @@ int stragglar_team_inject_delay(uint64_t ns, void* stream);
 /* End to end from host memory: copies host_in[p] -> bufs[p] (H2D), runs the
  * StragglAR AllReduce, copies bufs[p] -> host_out[p] (D2H), and synchronizes
  * `stream`.  The elementwise SUM lets the buffer go through a pipeline of
- * pieces (default 32 MiB, STRAGGLAR_E2E_PIECE_BYTES): H2D, AllReduce and D2H
+ * pieces (default 8 MiB, STRAGGLAR_E2E_PIECE_BYTES): H2D, AllReduce and D2H
  * of consecutive pieces overlap on two copy-engine streams and `stream`.
  * host_in/host_out should be pinned for full PCIe bandwidth; host_out may
  * equal host_in. */

@@ -673,7 +673,7 @@ int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_
   // AllReduce of piece k (SMs) and D2H of piece k-1 (copy engine, the other
   // direction) overlap.  Pieces keep 16-byte alignment.
   const uint64_t v = 16 / es;
-  uint64_t piece = env_u64("STRAGGLAR_E2E_PIECE_BYTES", 32ull << 20) / es;
+  uint64_t piece = env_u64("STRAGGLAR_E2E_PIECE_BYTES", 8ull << 20) / es;   // 8 MiB: measured best (profiles/r01)
   piece = piece / v * v;
   if (piece == 0) piece = v;
   const uint64_t npieces = (count + piece - 1) / piece;
