@@ -116,12 +116,6 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ helpers
-def torch_dtype(name):
-    import torch
-
-    return {"float32": torch.float32, "int32": torch.int32, "bfloat16": torch.bfloat16}[name]
-
-
 def to_tensor(x, dtype):
     import numpy as np
     import torch
@@ -171,7 +165,6 @@ def oracle_cpu_baseline(world, sigma, dtype, count, max_count=1 << 26):
 
 # ------------------------------------------------------------------ N = 1: single-device team
 def bench_team(args):
-    import numpy as np
     import torch
 
     import __graft_entry__
@@ -356,7 +349,6 @@ def bench_team(args):
 
 # ------------------------------------------------------------------ N > 1: one process per GPU
 def bench_multi(args):
-    import numpy as np
     import torch
     import torch.distributed as dist
 

@@ -80,7 +80,6 @@ __device__ __forceinline__ uint4 add_vec(const uint4& a, const uint4& b) {
 // Accumulator for the Phase-A reduction: fp32 lanes for float types, u32 for int.
 template <int DT>
 struct Acc {
-  static constexpr int kLanes = (DT == DT_BF16) ? 8 : 4;
   uint32_t u[4];
   float f[8];
   __device__ __forceinline__ void init(const uint4& v) {

@@ -21,8 +21,6 @@
 // of them in the single-device team mode (block b works for local rank b/G,
 // slice b%G).  All CTAs of a launch must be co-resident (cooperative launch),
 // because they spin on flags produced by CTAs of other ranks.
-#include <cooperative_groups.h>
-
 #include "device.cuh"
 #include "plan.h"
 

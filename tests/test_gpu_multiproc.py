@@ -29,6 +29,7 @@ def _port():
     (4, 2, 250001, "int32", "tma"),
     (4, 0, 99999, "float32", "lsu"),
     (6, 4, 123457, "bfloat16", "tma"),   # Appendix-B schedule (even non-power-of-2 n)
+    (8, 3, 500001, "float32", "tma"),    # the full n = 8 schedule across 8 processes
 ])
 def test_multiprocess_ipc(world, sigma, count, dtype, mover):
     if not torch.cuda.is_available():
