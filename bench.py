@@ -428,6 +428,17 @@ def bench_multi(args):
         R = world + (world.bit_length() - 1) - 2
         port_bytes = R * C
         achieved = port_bytes / (T_post * 1e-6) / 1e9
+        if shared:
+            # every rank on one GPU: the links are HBM; Phase B moves 2n(n-1)C bytes in total
+            hbm, hsrc = hbm_peak()
+            hb = 2 * world * (world - 1) * C / (T_post * 1e-6) / 1e9
+            roof = {"bound": "hbm", "kernel": "k_phase<..., KIND=4> (Phase A + B), ranks sharing one GPU",
+                    "achieved": round(hb, 1), "peak": hbm, "unit": "GB/s", "frac": round(hb / hbm, 3),
+                    "traffic": None, "peak_source": hsrc}
+        else:
+            roof = {"bound": "nvlink", "kernel": "k_phase<..., KIND=4> (Phase A + B)", "achieved": round(achieved, 1),
+                    "peak": NVLINK_PEER_MEASURED, "unit": "GB/s", "frac": round(achieved / NVLINK_PEER_MEASURED, 3),
+                    "traffic": None, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction"}
         out = {
             "metric": METRIC, "value": round(T_post, 2), "unit": "us", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(T_tot / 1e3, 4), "higher_is_better": False,
@@ -445,9 +456,7 @@ def bench_multi(args):
             "speedup_vs_ring_post": round((results["ring"][0] - results["ring"][1]) / T_post, 3),
             "speedup_vs_nccl_post": round((results["nccl"][0] - results["nccl"][1]) / T_post, 3) if "nccl" in results else None,
             "shared_device_test": shared,
-            "roofline": {"bound": "nvlink", "kernel": "k_phase<..., KIND=4> (Phase A + B)", "achieved": round(achieved, 1),
-                         "peak": NVLINK_PEER_MEASURED, "unit": "GB/s", "frac": round(achieved / NVLINK_PEER_MEASURED, 3),
-                         "traffic": None, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction"},
+            "roofline": roof,
             "cpu_baseline": None,
             "e2e": None,
             "gpu_launches": launches,
