@@ -420,8 +420,9 @@ def bench_multi(args):
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
         dist.all_reduce(dly, op=dist.ReduceOp.MAX)
         results[name] = (tot.item(), dly.item(), launches, clk.summary())
-    if S.stragglar_check_error():
-        raise RuntimeError("device watchdog fired")
+    code, where = S.stragglar_check_error_where(False)
+    if code:
+        raise RuntimeError(f"device watchdog fired (where=0x{where:x})")
     if rank == 0:
         T_tot, D_meas, launches, clocks = results["stragglar"]
         T_post = T_tot - D_meas

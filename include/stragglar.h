@@ -134,6 +134,12 @@ int stragglar_inject_delay(uint64_t ns, void* stream);
 /* Reads and clears the device error word (watchdog timeouts, bad arguments
  * seen on the device).  *code = 0 if none.  Synchronizes the device. */
 int stragglar_check_error(int* code);
+/* Same, for the team (team != 0) or the per-process communicator, also
+ * returning where the first failing spin-wait was: (kind << 8) | index with
+ * kind 0x1 Phase-A arrival, 0x2 exchange (non-straggler side), 0x3 exchange
+ * (straggler side), 0x4 copy, 0x5 completion, 0x6/0x7 ring, 0x8 barrier,
+ * 0x9/0xA direct completion. */
+int stragglar_check_error_where(int team, int* code, uint32_t* where);
 int stragglar_finalize(void);
 
 /* ---- single-device team (all ranks on the current device) ---------------

@@ -270,13 +270,14 @@ int team_b(void* const* bufs, size_t count, int dtype, void* stream, int which =
   return launch(which, dtype, P, c.world * P.G, stream);
 }
 
-int read_error(Comm& c, int* code) {
+int read_error(Comm& c, int* code, uint32_t* where = nullptr) {
   if (!code) return STRAGGLAR_ERR_INVALID_ARG;
   if (!c.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
   CK(cudaDeviceSynchronize());
   DevState h;
   CK(cudaMemcpy(&h, c.state, sizeof(h), cudaMemcpyDeviceToHost));
   *code = (int)h.err;
+  if (where) *where = h.err_info;
   if (h.err) {
     uint32_t z[2] = {0, 0};
     CK(cudaMemcpy(c.state, z, sizeof(z), cudaMemcpyHostToDevice));
@@ -562,6 +563,11 @@ int stragglar_inject_delay(uint64_t ns, void* stream) {
 int stragglar_check_error(int* code) {
   std::lock_guard<std::mutex> lk(g_mu);
   return read_error(g_proc, code);
+}
+
+int stragglar_check_error_where(int team, int* code, uint32_t* where) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return read_error(team ? g_team : g_proc, code, where);
 }
 
 int stragglar_finalize(void) {

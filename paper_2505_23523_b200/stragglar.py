@@ -60,6 +60,7 @@ _SIGS = {
     "stragglar_inject_delay": ([_c_u64, _vp], _c_int),
     "stragglar_check_error": ([ctypes.POINTER(_c_int)], _c_int),
     "stragglar_finalize": ([], _c_int),
+    "stragglar_check_error_where": ([_c_int, ctypes.POINTER(_c_int), ctypes.POINTER(ctypes.c_uint32)], _c_int),
     "stragglar_select": ([_c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                           ctypes.POINTER(_c_int), ctypes.POINTER(ctypes.c_double)], _c_int),
     "stragglar_set_cost_model": ([ctypes.c_double, ctypes.c_double], _c_int),
@@ -238,6 +239,15 @@ def stragglar_check_error() -> int:
     if st not in (0, 6):
         _ck("stragglar_check_error", st)
     return code.value
+
+
+def stragglar_check_error_where(team: bool = False):
+    """-> (code, where): the device error word and the failing wait's location."""
+    code, where = _c_int(0), ctypes.c_uint32(0)
+    st = _lib.stragglar_check_error_where(1 if team else 0, ctypes.byref(code), ctypes.byref(where))
+    if st not in (0, 6):
+        _ck("stragglar_check_error_where", st)
+    return code.value, where.value
 
 
 def stragglar_finalize() -> None:
