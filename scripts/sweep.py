@@ -155,6 +155,58 @@ def delay_sweep(n, sigma, count, dtype, iters, warm):
             "first_winning_delay_measured_us": crit_meas, "rows": rows}
 
 
+def dp_buckets(n=8, sigma=0, count=13_107_200, k=16, iters=5, warm=2):
+    """BASELINE configs[3] as SURVEY.md §8(d) states it: K = 16 back-to-back
+    25 MiB bf16 buckets; the straggler delays only the first one (P:744-748:
+    later buckets are synchronised by the previous AllReduce).  Total from the
+    non-stragglers' start of bucket 0 to the end of bucket K-1."""
+    S.stragglar_team_init(n, sigma)
+    bufs = [[torch.randn(count, device="cuda").to(torch.bfloat16) for _ in range(n)] for _ in range(k)]
+    # Phase A time of one bucket -> masking delay for bucket 0
+    S.stragglar_team_allreduce(bufs[0])
+    torch.cuda.synchronize()
+    a, b = ev(), ev()
+    blocker()
+    a.record()
+    S.stragglar_team_reduce_scatter(bufs[0])
+    b.record()
+    S.stragglar_team_complete(bufs[0])
+    torch.cuda.synchronize()
+    T_A = a.elapsed_time(b) * 1e3
+    D = int((1.25 * T_A + 20.0) * 1e3)
+
+    res = {}
+    for kind in ("stragglar", "direct", "ring"):
+        times = []
+        for it in range(warm + iters):
+            e0, e1 = ev(), ev()
+            blocker()
+            e0.record()
+            for i in range(k):
+                if kind == "ring":
+                    if i == 0:
+                        S.stragglar_team_inject_delay(D)   # bulk-synchronous: waits for the straggler
+                    S.stragglar_team_allreduce_ring(bufs[i])
+                else:
+                    S.stragglar_team_reduce_scatter(bufs[i])
+                    if i == 0:
+                        S.stragglar_team_inject_delay(D)
+                    if kind == "direct":
+                        S.stragglar_team_complete_direct(bufs[i])
+                    else:
+                        S.stragglar_team_complete(bufs[i])
+            e1.record()
+            torch.cuda.synchronize()
+            if it >= warm:
+                times.append(e0.elapsed_time(e1) * 1e3)
+        res[kind] = round(statistics.median(times), 1)
+    assert S.stragglar_team_check_error() == 0
+    S.stragglar_team_finalize()
+    return {"n": n, "buckets": k, "bucket_bytes": count * 2, "delay_us": round(D / 1e3, 1),
+            "total_us": res, "speedup_vs_ring": round(res["ring"] / res["stragglar"], 3),
+            "speedup_direct_vs_ring": round(res["ring"] / res["direct"], 3)}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=10)
@@ -171,6 +223,7 @@ def main():
     out["configs"]["config1_n4_1M_fp32"] = measure(4, 0, 1 << 20, torch.float32, args.iters, args.warmup)
     out["configs"]["config2_n8_256MiB_fp32"] = measure(8, 0, 1 << 26, torch.float32, args.iters, args.warmup)
     out["delay_sweep"] = delay_sweep(8, 0, 1 << 26, torch.float32, args.iters, args.warmup)
+    out["dp_buckets"] = dp_buckets()
     print(json.dumps(out))
 
 

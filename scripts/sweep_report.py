@@ -48,6 +48,14 @@ def main(path, out):
           "| delay / T_RS | delay us | StragglAR total us | Ring total us |", "|---|---|---|---|"]
     for r in ds["rows"]:
         L.append(f"| {r['delay_frac_of_T_RS']} | {r['delay_us']} | {r['T_total_stragglar_us']} | {r['T_total_ring_us']} |")
+    if d.get("dp_buckets"):
+        b = d["dp_buckets"]
+        L += ["", "## Config 4: 16 back-to-back 25 MiB bf16 buckets, straggler delays bucket 0 only (n = 8)", "",
+              f"delay {b['delay_us']} us before bucket 0; total from bucket-0 start to the end of bucket 15:", "",
+              "| StragglAR (schedule) | StragglAR (direct completion) | Ring | speedup schedule | speedup direct |",
+              "|---|---|---|---|---|",
+              f"| {b['total_us']['stragglar']} us | {b['total_us']['direct']} us | {b['total_us']['ring']} us | "
+              f"{b['speedup_vs_ring']} | {b['speedup_direct_vs_ring']} |"]
     open(out, "w").write("\n".join(L) + "\n")
 
 
