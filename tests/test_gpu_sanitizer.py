@@ -25,7 +25,7 @@ def test_sanitizer_clean(tool, mover):
     __graft_entry__.build()
     env = dict(os.environ, STRAGGLAR_MOVER=mover, STRAGGLAR_TIMEOUT_MS="120000")
     r = subprocess.run([cs, "--tool", tool, "--error-exitcode", "9", sys.executable,
-                        os.path.join(ROOT, "scripts", "sanitize_step.py")],
+                        os.path.join(ROOT, "tests", "sanitize_step.py")],
                        env=env, capture_output=True, text=True, timeout=900)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-3000:]
