@@ -4,13 +4,16 @@ set -u
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 TAG=${TAG:-r01}
+if [ -z "$SKIP_LISTS" ]; then
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
     python scripts/profile_step.py > gpurun_out/${TAG}_launches.log 2>&1; echo "launches rc=$?"
+# (demangled names read "k_phase<(int)1, (int)8, (int)1, (int)1>")
 # the launch list of the bench command itself (cold-cache, serialised: shares, not absolutes)
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_bench_launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/${TAG}_bench_under_ncu.log 2>&1; echo "bench launches rc=$?"
+fi
 # kernel-name regexes on the demangled names: k_phase<dtype, world, mover, KIND>
-declare -A PAT=( [phaseB]='k_phase<.*, 1>' [phaseA]='k_phase<.*, 0>' [ring]='k_ring<' [direct]='k_phase<.*, 3>' )
+declare -A PAT=( [phaseB]='k_phase<.*\(int\)1>' [phaseA]='k_phase<.*\(int\)0>' [ring]='k_ring<' [direct]='k_phase<.*\(int\)3>' )
 for k in phaseB phaseA ring direct; do
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
       -k "regex:${PAT[$k]}" -s 1 -c 1 \

@@ -73,7 +73,8 @@ def main():
                     f"{', '.join(f'{k} {v}%' for k, v in r['top_stalls_pct'].items())} |\n")
     if "--traffic" in sys.argv:
         for r in res:
-            if "k_complete" in r["kernel"] or ("k_phase<" in r["kernel"] and r["kernel"].rstrip(")").split("(")[0].endswith(", 1>")):
+            name = r["kernel"].replace("(int)", "")
+            if "k_complete" in name or ("k_phase<" in name and name.split(">")[0].endswith(", 1")):
                 tr = r["dram__bytes_read.sum"]["value"] + r["dram__bytes_write.sum"]["value"]
                 json.dump({"workload": "config2", "k_complete_dram_bytes": tr, "source": f"profiles/{tag}/ncu_summary.json",
                            "kernel": r["kernel"]}, open(os.path.join(ROOT, "profiles", "latest_traffic.json"), "w"), indent=1)
