@@ -19,3 +19,8 @@ for k in phaseB phaseA ring direct; do
       -k "regex:${PAT[$k]}" -s 1 -c 1 \
       -o gpurun_out/${TAG}_$k python scripts/profile_step.py > gpurun_out/${TAG}_$k.log 2>&1; echo "$k rc=$?"
 done
+# summaries on the box (the .ncu-rep files are large); keep only the Phase-B report
+NCU_SUMMARY_DIR=gpurun_out/ncu_summary python scripts/ncu_summary.py $TAG gpurun_out/${TAG}_phaseB.ncu-rep \
+    gpurun_out/${TAG}_phaseA.ncu-rep gpurun_out/${TAG}_ring.ncu-rep gpurun_out/${TAG}_direct.ncu-rep --traffic > /dev/null
+rm -f gpurun_out/${TAG}_phaseA.ncu-rep gpurun_out/${TAG}_ring.ncu-rep gpurun_out/${TAG}_direct.ncu-rep
+du -sh gpurun_out

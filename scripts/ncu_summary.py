@@ -59,7 +59,8 @@ def main():
     tag = sys.argv[1]
     reps = [a for a in sys.argv[2:] if not a.startswith("--")]
     res = [summarise(r) for r in reps]
-    d = os.path.join(ROOT, "profiles", tag)
+    outdir = os.environ.get("NCU_SUMMARY_DIR", os.path.join(ROOT, "profiles"))
+    d = os.path.join(outdir, tag)
     os.makedirs(d, exist_ok=True)
     json.dump(res, open(os.path.join(d, "ncu_summary.json"), "w"), indent=1)
     with open(os.path.join(d, "ncu_summary.md"), "w") as f:
@@ -77,7 +78,7 @@ def main():
             if "k_complete" in name or ("k_phase<" in name and name.split(">")[0].endswith(", 1")):
                 tr = r["dram__bytes_read.sum"]["value"] + r["dram__bytes_write.sum"]["value"]
                 json.dump({"workload": "config2", "k_complete_dram_bytes": tr, "source": f"profiles/{tag}/ncu_summary.json",
-                           "kernel": r["kernel"]}, open(os.path.join(ROOT, "profiles", "latest_traffic.json"), "w"), indent=1)
+                           "kernel": r["kernel"]}, open(os.path.join(outdir, "latest_traffic.json"), "w"), indent=1)
     print(open(os.path.join(d, "ncu_summary.md")).read())
 
 
