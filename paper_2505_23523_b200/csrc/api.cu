@@ -52,8 +52,11 @@ struct Comm {
   int world = 0, rank = -1, sigma = -1, device = -1;
   int G = 0;
   bool rs_pending = false;     // team: a Phase A awaits its Phase B (same call epoch)
-  uint32_t* flags = nullptr;   // own flag array(s); team: world arrays back to back
+  uint32_t* flags = nullptr;   // own flag array(s) + LL area(s); team: world of them back to back
   uint32_t* peer_flags[kMaxWorld] = {nullptr};
+  uint64_t* peer_ll[kMaxWorld] = {nullptr};
+  size_t flags_bytes = 0;      // per rank, before its LL area
+  size_t rank_bytes = 0;       // per rank: flags + LL
   bool imported = false;
   DevState* state = nullptr;
   RankPrograms progs;
@@ -150,19 +153,28 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   c.team = team;
   c.rs_pending = false;
   c.timeout_ns = env_u64("STRAGGLAR_TIMEOUT_MS", 10000) * 1000000ull;
-  const size_t per_rank = (size_t)kSlots * G * sizeof(uint32_t);
-  const size_t nbytes = team ? per_rank * world : per_rank;
+  c.flags_bytes = ((size_t)kSlots * G * sizeof(uint32_t) + 255) / 256 * 256;
+  c.rank_bytes = c.flags_bytes + (size_t)(kMaxWorld - 1) * kLLChunkWords * sizeof(uint64_t);
+  const size_t nbytes = team ? c.rank_bytes * world : c.rank_bytes;
   CK(cudaMalloc(&c.flags, nbytes));
   CK(cudaMemset(c.flags, 0, nbytes));
   CK(cudaMalloc(&c.state, sizeof(DevState)));
   CK(cudaMemset(c.state, 0, sizeof(DevState)));
   CK(cudaDeviceSynchronize());
-  for (int p = 0; p < kMaxWorld; ++p) c.peer_flags[p] = nullptr;
+  for (int p = 0; p < kMaxWorld; ++p) {
+    c.peer_flags[p] = nullptr;
+    c.peer_ll[p] = nullptr;
+  }
+  auto ll_of = [&](uint32_t* f) { return reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(f) + c.flags_bytes); };
   if (team) {
-    for (int p = 0; p < world; ++p) c.peer_flags[p] = c.flags + (size_t)p * kSlots * G;
+    for (int p = 0; p < world; ++p) {
+      c.peer_flags[p] = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(c.flags) + (size_t)p * c.rank_bytes);
+      c.peer_ll[p] = ll_of(c.peer_flags[p]);
+    }
     c.imported = true;
   } else {
     c.peer_flags[rank] = c.flags;
+    c.peer_ll[rank] = ll_of(c.flags);
     c.imported = (world == 1);
   }
   c.active = true;
@@ -208,10 +220,18 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
   P.G = slices_for(c, P.ce * P.esize);
   P.timeout_ns = c.timeout_ns;
   P.mover = c.mover;
+  {
+    // LL Phase B for small chunks (latency-bound): STRAGGLAR_LL_MAX_CHUNK bytes, 0 disables
+    const uint64_t chunk_bytes = P.ce * P.esize;
+    uint64_t lim = env_u64("STRAGGLAR_LL_MAX_CHUNK", 64 * 1024);
+    if (lim > kLLChunkBytes) lim = kLLChunkBytes;
+    P.use_ll = (chunk_bytes > 0 && chunk_bytes <= lim) ? 1 : 0;
+  }
   P.sys_scope = c.team ? (int)env_u64("STRAGGLAR_SYS_SCOPE", 0) : 1;
   P.state = c.state;
   for (int p = 0; p < c.world; ++p) {
     P.flags[p] = c.peer_flags[p];
+    P.ll[p] = c.peer_ll[p];
     P.logical_of_phys[p] = c.progs.logical_of_phys[p];
     P.nops[p] = c.progs.nops[p];
     for (int k = 0; k < c.progs.nops[p]; ++k) P.ops[p][k] = c.progs.ops[p][k];
@@ -363,7 +383,7 @@ int stragglar_export_handle(void* blob) {
   std::memset(&b, 0, sizeof(b));
   CK(cudaIpcGetMemHandle(&b.handle, g_proc.flags));
   b.offset = 0;
-  b.bytes = (uint64_t)kSlots * g_proc.G * sizeof(uint32_t);
+  b.bytes = g_proc.rank_bytes;
   std::memcpy(blob, &b, sizeof(b));
   return STRAGGLAR_OK;
 }
@@ -379,7 +399,9 @@ int stragglar_import_handles(const void* blobs, int world) {
     void* ptr = nullptr;
     CK(cudaIpcOpenMemHandle(&ptr, b[p].handle, cudaIpcMemLazyEnablePeerAccess));
     c.opened.push_back(ptr);
+    if (b[p].bytes != c.rank_bytes) return STRAGGLAR_ERR_INVALID_ARG;   // ranks disagree on G
     c.peer_flags[p] = reinterpret_cast<uint32_t*>(static_cast<char*>(ptr) + b[p].offset);
+    c.peer_ll[p] = reinterpret_cast<uint64_t*>(static_cast<char*>(ptr) + b[p].offset + c.flags_bytes);
   }
   c.imported = true;
   return STRAGGLAR_OK;

@@ -529,12 +529,175 @@ __device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t
   cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, G, s), ep, P.sys_scope);
 }
 
+// ---------------------------------------------------------------- LL Phase B (small chunks)
+// Low-latency variant of complete_body: every transfer is a stream of 8-byte
+// words (4 payload bytes | epoch << 32) stored into the receiver's LL area; the
+// receiver polls the words themselves.  No release fence, no separate flag and
+// no store-completion wait per hop, and no CTA-wide synchronisation: thread t
+// of slice s owns the same words of a chunk in every op, so each thread runs
+// its own words through the rounds (the dependency order is the schedule's
+// round order, as in complete_body).  Same arithmetic per word, same bits.
+constexpr int kLLBatch = 8;
+
+__device__ __forceinline__ uint32_t ld_word(const char* buf, uint64_t o, uint64_t end) {
+  if (o + 4 <= end) return *reinterpret_cast<const uint32_t*>(buf + o);
+  return (uint32_t)(*reinterpret_cast<const uint16_t*>(buf + o));   // bf16 tail: 2 valid bytes
+}
+__device__ __forceinline__ void st_word(char* buf, uint64_t o, uint64_t end, uint32_t v) {
+  if (o + 4 <= end)
+    *reinterpret_cast<uint32_t*>(buf + o) = v;
+  else
+    *reinterpret_cast<uint16_t*>(buf + o) = (uint16_t)v;
+}
+
+// Poll kLLBatch words (w = base + j*nthr < wend) of `ll` until they carry epoch ep.
+__device__ __forceinline__ bool ll_poll_batch(const uint64_t* ll, uint64_t base, uint64_t wend, uint32_t ep,
+                                              uint32_t (&val)[kLLBatch], const LaunchPlan& P, uint32_t where) {
+  const bool sys = P.sys_scope;
+  const uint32_t nthr = blockDim.x;
+  uint64_t v[kLLBatch];
+#pragma unroll
+  for (int j = 0; j < kLLBatch; ++j) {
+    const uint64_t w = base + (uint64_t)j * nthr;
+    v[j] = (w < wend) ? ld_ll(ll + w, sys) : ((uint64_t)ep << 32);
+  }
+  uint64_t t0 = 0;
+  for (uint32_t it = 0;; ++it) {
+    bool all = true;
+#pragma unroll
+    for (int j = 0; j < kLLBatch; ++j) {
+      if ((uint32_t)(v[j] >> 32) != ep) {
+        all = false;
+        v[j] = ld_ll(ll + base + (uint64_t)j * nthr, sys);
+      }
+    }
+    if (all) break;
+    if (it == 0) t0 = globaltimer();
+    if ((it & 255) == 255) {
+      if (*(volatile uint32_t*)&P.state->err) return false;
+      if (globaltimer() - t0 > P.timeout_ns) {
+        if (atomicCAS(&P.state->err, 0u, (uint32_t)ERR_TIMEOUT) == 0u) atomicExch(&P.state->err_info, where);
+        return false;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kLLBatch; ++j) val[j] = (uint32_t)v[j];
+  return true;
+}
+
+// word-stream modes
+enum LLMode : int { LL_PUSH = 0, LL_EXCH = 1, LL_FWD = 2, LL_FWD_UNPACK = 3, LL_UNPACK = 4 };
+
+// Words [wa, wb) of one chunk slice.  ub: user buffer, cb0: the chunk's first
+// byte in it, end: buffer byte end; mll: my LL area of the chunk, pll: the
+// peer's LL area of the chunk (unused for LL_UNPACK).
+template <int DT, int MODE>
+__device__ bool ll_words(char* ub, uint64_t cb0, uint64_t end, const uint64_t* mll, uint64_t* pll, uint64_t wa,
+                         uint64_t wb, uint32_t ep, const LaunchPlan& P, uint32_t where) {
+  const bool sys = P.sys_scope;
+  const uint32_t nthr = blockDim.x;
+  for (uint64_t base = wa + threadIdx.x; base < wb; base += (uint64_t)kLLBatch * nthr) {
+    uint32_t val[kLLBatch];
+    if constexpr (MODE != LL_PUSH) {
+      if (!ll_poll_batch(mll, base, wb, ep, val, P, where)) return false;
+    }
+#pragma unroll
+    for (int j = 0; j < kLLBatch; ++j) {
+      const uint64_t w = base + (uint64_t)j * nthr;
+      if (w >= wb) break;
+      const uint64_t o = cb0 + 4 * w;
+      if constexpr (MODE == LL_PUSH) {
+        st_ll(pll + w, ld_word(ub, o, end), ep, sys);
+      } else if constexpr (MODE == LL_EXCH) {
+        const uint32_t z = add_word<DT>(ld_word(ub, o, end), val[j]);
+        st_word(ub, o, end, z);
+        st_ll(pll + w, z, ep, sys);
+      } else if constexpr (MODE == LL_FWD) {
+        st_ll(pll + w, val[j], ep, sys);
+      } else if constexpr (MODE == LL_FWD_UNPACK) {
+        st_word(ub, o, end, val[j]);
+        st_ll(pll + w, val[j], ep, sys);
+      } else {
+        st_word(ub, o, end, val[j]);
+      }
+    }
+  }
+  return true;
+}
+
+template <int DT>
+__device__ void ll_phase_b(const LaunchPlan& P, int s, int me, uint32_t ep) {
+  const int G = P.G, V = 16 / P.esize, es = P.esize;
+  const uint64_t end = P.count * es;
+  char* ub = P.buf[me];
+  const int own = (me == P.sigma) ? -1 : P.logical_of_phys[me];
+  uint32_t unpacked = 0;   // chunks whose LL words were already written to the user buffer
+  // which half of chunk c this rank computed itself in the exchange: 1 low, 2 high, 0 none
+  auto local_half = [&](int c) { return c == own ? 1 : (me == P.sigma ? 2 : 0); };
+  struct Words {
+    uint64_t cb0, wa, wm, wb;
+  };
+  auto words_of = [&](int c) {
+    const Range cr = chunk_range(P, c);
+    const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
+    const uint64_t nvec = (sl.hi - sl.lo + V - 1) / V;
+    const uint64_t mid = sl.lo + (nvec / 2) * V < sl.hi ? sl.lo + (nvec / 2) * V : sl.hi;
+    Words w;
+    w.cb0 = cr.lo * es;
+    w.wa = (sl.lo * es - w.cb0) / 4;
+    w.wm = (mid * es - w.cb0) / 4;
+    w.wb = (sl.hi * es - w.cb0 + 3) / 4;
+    return w;
+  };
+  bool ok = true;
+  for (int k = 0; k < P.nops[me] && ok; ++k) {
+    const Op op = P.ops[me][k];
+    const int c = op.chunk, peer = op.peer;
+    const Words w = words_of(c);
+    const uint64_t* mll = P.ll[me] + (size_t)c * kLLChunkWords;
+    uint64_t* pll = P.ll[peer] + (size_t)c * kLLChunkWords;
+    const uint32_t where = 0xB00 | k;
+    if (op.kind == OP_EXCH_LOW) {
+      // my partial for the straggler's half, then my half: x_sigma arrives, add, keep, return
+      ll_words<DT, LL_PUSH>(ub, w.cb0, end, mll, pll, w.wm, w.wb, ep, P, where);
+      ok = ll_words<DT, LL_EXCH>(ub, w.cb0, end, mll, pll, w.wa, w.wm, ep, P, where);
+    } else if (op.kind == OP_EXCH_HIGH) {
+      ll_words<DT, LL_PUSH>(ub, w.cb0, end, mll, pll, w.wa, w.wm, ep, P, where);
+      ok = ll_words<DT, LL_EXCH>(ub, w.cb0, end, mll, pll, w.wm, w.wb, ep, P, where);
+    } else {
+      const int lh = local_half(c);
+      const bool first = !((unpacked >> c) & 1u);
+      const uint64_t l0 = lh == 1 ? w.wa : w.wm, l1 = lh == 1 ? w.wm : w.wb;   // local half (if any)
+      const uint64_t r0 = lh == 1 ? w.wm : w.wa, r1 = lh == 1 ? w.wb : w.wm;   // LL half
+      if (lh) ll_words<DT, LL_PUSH>(ub, w.cb0, end, mll, pll, l0, l1, ep, P, where);
+      const uint64_t f0 = lh ? r0 : w.wa, f1 = lh ? r1 : w.wb;
+      ok = first ? ll_words<DT, LL_FWD_UNPACK>(ub, w.cb0, end, mll, pll, f0, f1, ep, P, where)
+                 : ll_words<DT, LL_FWD>(ub, w.cb0, end, mll, pll, f0, f1, ep, P, where);
+      unpacked |= 1u << c;
+    }
+  }
+  // postcondition: the LL words of every chunk not yet forwarded land in the buffer
+  for (int c = 0; c < P.nchunks && ok; ++c) {
+    if ((unpacked >> c) & 1u) continue;
+    const Words w = words_of(c);
+    const uint64_t* mll = P.ll[me] + (size_t)c * kLLChunkWords;
+    const int lh = local_half(c);
+    const uint64_t f0 = lh == 1 ? w.wm : w.wa, f1 = lh == 2 ? w.wm : w.wb;
+    ok = ll_words<DT, LL_UNPACK>(ub, w.cb0, end, mll, nullptr, f0, f1, ep, P, 0xD00 | c);
+  }
+}
+
 // Phase B body (Algorithm 1 round executor) for rank `me`, slice s.
 template <int DT, int W, int MV>
 __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
   const int G = P.G;
   const int V = 16 / P.esize;
   constexpr bool tma = MV == MOVER_TMA;
+  if (P.use_ll) {
+    ll_phase_b<DT>(P, s, me, ep);
+    return;
+  }
   // the straggler reaches barrier (2): announce per slice to the others
   if (me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
     st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep, P.sys_scope);

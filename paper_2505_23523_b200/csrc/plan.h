@@ -27,6 +27,11 @@ enum Slot : int {
 #endif
 constexpr int kThreads = STRAGGLAR_THREADS;   // CTA size of the data kernels
 constexpr int kMaxSlices = 1024;
+// Low-latency (LL) Phase B for small chunks: every 8-byte word carries 4
+// payload bytes and the call epoch; per rank one LL area of kLLChunkBytes of
+// payload per chunk follows the flag array in the same allocation.
+constexpr uint32_t kLLChunkBytes = 256u * 1024u;
+constexpr uint32_t kLLChunkWords = kLLChunkBytes / 4;
 
 // Device-resident per-communicator state (in the launching process's memory).
 struct DevState {
@@ -63,6 +68,9 @@ struct LaunchPlan {
   int sys_scope;             // 1: flags/fences at system scope (peers on other GPUs); 0: gpu scope (team)
   uint64_t timeout_ns;
   DevState* state;
+  uint64_t* ll[kMaxWorld];   // LL area of each physical rank: [chunk][word] (payload | epoch << 32)
+  int use_ll;                // Phase B through the LL areas (small chunks)
+  int pad2;
   int logical_of_phys[kMaxWorld];
   int nops[kMaxWorld];       // by physical rank
   Op ops[kMaxWorld][kMaxOps];// by physical rank

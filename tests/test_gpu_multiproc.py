@@ -30,6 +30,8 @@ def _port():
     (4, 0, 99999, "float32", "lsu"),
     (6, 4, 123457, "bfloat16", "tma"),   # Appendix-B schedule (even non-power-of-2 n)
     (8, 3, 500001, "float32", "tma"),    # the full n = 8 schedule across 8 processes
+    (4, 1, 30001, "float32", "tma"),     # small chunks: LL protocol, system scope
+    (8, 5, 70001, "bfloat16", "lsu"),    # small chunks: LL protocol, 8 processes
 ])
 def test_multiprocess_ipc(world, sigma, count, dtype, mover):
     if not torch.cuda.is_available():

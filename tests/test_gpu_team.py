@@ -334,3 +334,34 @@ def test_randomized_cases(S):
         xs, outs = run_team(S, n, sigma, dtype, count, pattern=pattern, config=60 + case, algo=algo)
         want = N.ring_allreduce(xs, dtype) if algo == "ring" else N.stragglar_allreduce(xs, sigma, dtype)
         check_equal(outs, want, xs, dtype, f"case {case}: n={n} s={sigma} {dtype} {count} {pattern} {algo}")
+
+
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+@pytest.mark.parametrize("n", [2, 4, 6, 8])
+def test_ll_protocol_vs_regular(S, dtype, n):
+    """Small chunks use the low-latency (LL) Phase B (8-byte words = 4 payload
+    bytes + epoch); force it on and off on the same inputs: both must equal
+    the oracle bit for bit (tails, odd bf16 counts, every straggler)."""
+    old = os.environ.get("STRAGGLAR_LL_MAX_CHUNK")
+    try:
+        for sigma in range(n):
+            for count in [1, 3, 8 * (n - 1) + 5, 20001]:
+                xs = make_inputs(n, count, dtype, config=70 + sigma)
+                want = N.stragglar_allreduce(xs, sigma, dtype)
+                for ll in ("262144", "0"):
+                    os.environ["STRAGGLAR_LL_MAX_CHUNK"] = ll
+                    bufs = [to_dev(x, dtype) for x in xs]
+                    S.stragglar_team_init(n, sigma)
+                    if count % 2:
+                        S.stragglar_team_allreduce(bufs)
+                    else:
+                        S.stragglar_team_reduce_scatter(bufs)
+                        S.stragglar_team_complete(bufs)
+                    torch.cuda.synchronize()
+                    assert S.stragglar_team_check_error() == 0
+                    check_equal([to_host(b, dtype) for b in bufs], want, xs, dtype, f"ll={ll} s={sigma} c={count}")
+    finally:
+        if old is None:
+            os.environ.pop("STRAGGLAR_LL_MAX_CHUNK", None)
+        else:
+            os.environ["STRAGGLAR_LL_MAX_CHUNK"] = old
