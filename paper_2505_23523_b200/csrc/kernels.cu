@@ -537,6 +537,9 @@ __device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t
 // of slice s owns the same words of a chunk in every op, so each thread runs
 // its own words through the rounds (the dependency order is the schedule's
 // round order, as in complete_body).  Same arithmetic per word, same bits.
+#ifndef STRAGGLAR_LL_GENTLE
+#define STRAGGLAR_LL_GENTLE 0
+#endif
 constexpr int kLLBatch = 8;
 
 __device__ __forceinline__ uint32_t ld_word(const char* buf, uint64_t o, uint64_t end) {
@@ -564,6 +567,17 @@ __device__ __forceinline__ bool ll_poll_batch(const uint64_t* ll, uint64_t base,
   uint64_t t0 = 0;
   for (uint32_t it = 0;; ++it) {
     bool all = true;
+#if STRAGGLAR_LL_GENTLE
+    // poll one outstanding word at a time (words of a batch arrive together)
+#pragma unroll
+    for (int j = 0; j < kLLBatch; ++j) {
+      if (all && (uint32_t)(v[j] >> 32) != ep) {
+        all = false;
+        v[j] = ld_ll(ll + base + (uint64_t)j * nthr, sys);
+      }
+    }
+    if (!all) __nanosleep(STRAGGLAR_LL_GENTLE);
+#else
 #pragma unroll
     for (int j = 0; j < kLLBatch; ++j) {
       if ((uint32_t)(v[j] >> 32) != ep) {
@@ -571,6 +585,7 @@ __device__ __forceinline__ bool ll_poll_batch(const uint64_t* ll, uint64_t base,
         v[j] = ld_ll(ll + base + (uint64_t)j * nthr, sys);
       }
     }
+#endif
     if (all) break;
     if (it == 0) t0 = globaltimer();
     if ((it & 255) == 255) {
@@ -626,7 +641,7 @@ __device__ bool ll_words(char* ub, uint64_t cb0, uint64_t end, const uint64_t* m
   return true;
 }
 
-template <int DT>
+template <int DT, int W>
 __device__ void ll_phase_b(const LaunchPlan& P, int s, int me, uint32_t ep) {
   const int G = P.G, V = 16 / P.esize, es = P.esize;
   const uint64_t end = P.count * es;
@@ -651,6 +666,25 @@ __device__ void ll_phase_b(const LaunchPlan& P, int s, int me, uint32_t ep) {
     return w;
   };
   bool ok = true;
+  // Exchange operands go out first, so every exchange only waits for its
+  // partner's operand (as the flag protocol's exchange only waits for Phase A),
+  // not for the partner to reach that round: non-stragglers send the
+  // straggler their partial of its half of their chunk; the straggler sends
+  // every owner x_sigma for the owner's half.
+  if (me == P.sigma) {
+    for (int c = 0; c < P.nchunks; ++c) {
+      int owner = 0;
+#pragma unroll
+      for (int q = 0; q < W; ++q)
+        if (P.logical_of_phys[q] == c) owner = q;
+      const Words w = words_of(c);
+      ll_words<DT, LL_PUSH>(ub, w.cb0, end, nullptr, P.ll[owner] + (size_t)c * kLLChunkWords, w.wa, w.wm, ep, P, 0);
+    }
+  } else {
+    const Words w = words_of(own);
+    ll_words<DT, LL_PUSH>(ub, w.cb0, end, nullptr, P.ll[P.sigma] + (size_t)own * kLLChunkWords, w.wm, w.wb, ep, P,
+                          0);
+  }
   for (int k = 0; k < P.nops[me] && ok; ++k) {
     const Op op = P.ops[me][k];
     const int c = op.chunk, peer = op.peer;
@@ -659,11 +693,9 @@ __device__ void ll_phase_b(const LaunchPlan& P, int s, int me, uint32_t ep) {
     uint64_t* pll = P.ll[peer] + (size_t)c * kLLChunkWords;
     const uint32_t where = 0xB00 | k;
     if (op.kind == OP_EXCH_LOW) {
-      // my partial for the straggler's half, then my half: x_sigma arrives, add, keep, return
-      ll_words<DT, LL_PUSH>(ub, w.cb0, end, mll, pll, w.wm, w.wb, ep, P, where);
+      // my half: x_sigma arrived (pushed up front), add, keep, send the result
       ok = ll_words<DT, LL_EXCH>(ub, w.cb0, end, mll, pll, w.wa, w.wm, ep, P, where);
     } else if (op.kind == OP_EXCH_HIGH) {
-      ll_words<DT, LL_PUSH>(ub, w.cb0, end, mll, pll, w.wa, w.wm, ep, P, where);
       ok = ll_words<DT, LL_EXCH>(ub, w.cb0, end, mll, pll, w.wm, w.wb, ep, P, where);
     } else {
       const int lh = local_half(c);
@@ -695,7 +727,7 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
   const int V = 16 / P.esize;
   constexpr bool tma = MV == MOVER_TMA;
   if (P.use_ll) {
-    ll_phase_b<DT>(P, s, me, ep);
+    ll_phase_b<DT, W>(P, s, me, ep);
     return;
   }
   // the straggler reaches barrier (2): announce per slice to the others

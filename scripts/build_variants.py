@@ -7,7 +7,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2505_23523_b200 import build as B  # noqa: E402
 
-VARIANTS = {
+VARIANTS_ALL = {
     "s3_16k": ["STRAGGLAR_STAGES=3", "STRAGGLAR_STAGE_BYTES=16384"],
     "s4_12k": ["STRAGGLAR_STAGES=4", "STRAGGLAR_STAGE_BYTES=12288"],
     "s6_8k": ["STRAGGLAR_STAGES=6", "STRAGGLAR_STAGE_BYTES=8192"],
@@ -17,6 +17,11 @@ VARIANTS = {
     "s3_16k_t512": ["STRAGGLAR_STAGES=3", "STRAGGLAR_STAGE_BYTES=16384", "STRAGGLAR_THREADS=512", "STRAGGLAR_MIN_BLOCKS=2"],
     "s3_8k_t128": ["STRAGGLAR_STAGES=3", "STRAGGLAR_STAGE_BYTES=8192", "STRAGGLAR_THREADS=128", "STRAGGLAR_MIN_BLOCKS=8"],
 }
+VARIANTS_LL = {
+    "ll_gentle32": ["STRAGGLAR_LL_GENTLE=32"],
+    "ll_gentle200": ["STRAGGLAR_LL_GENTLE=200"],
+}
+VARIANTS = VARIANTS_LL if "--ll" in sys.argv else VARIANTS_ALL
 os.makedirs(os.path.join(ROOT, "build", "variants"), exist_ok=True)
 with ThreadPoolExecutor(4) as ex:
     futs = {k: ex.submit(B.build, True, False, v, os.path.join(ROOT, "build", "variants", f"lib_{k}.so")) for k, v in VARIANTS.items()}
