@@ -223,7 +223,7 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
   {
     // LL Phase B for small chunks (latency-bound): STRAGGLAR_LL_MAX_CHUNK bytes, 0 disables
     const uint64_t chunk_bytes = P.ce * P.esize;
-    uint64_t lim = env_u64("STRAGGLAR_LL_MAX_CHUNK", 64 * 1024);
+    uint64_t lim = env_u64("STRAGGLAR_LL_MAX_CHUNK", 0);   // off by default: slower on one GPU
     if (lim > kLLChunkBytes) lim = kLLChunkBytes;
     P.use_ll = (chunk_bytes > 0 && chunk_bytes <= lim) ? 1 : 0;
   }

@@ -30,8 +30,8 @@ def _port():
     (4, 0, 99999, "float32", "lsu"),
     (6, 4, 123457, "bfloat16", "tma"),   # Appendix-B schedule (even non-power-of-2 n)
     (8, 3, 500001, "float32", "tma"),    # the full n = 8 schedule across 8 processes
-    (4, 1, 30001, "float32", "tma"),     # small chunks: LL protocol, system scope
-    (8, 5, 70001, "bfloat16", "lsu"),    # small chunks: LL protocol, 8 processes
+    (4, 1, 30001, "float32", "tma+ll"),  # LL protocol forced on, system scope
+    (8, 5, 70001, "bfloat16", "lsu+ll"), # LL protocol forced on, 8 processes
 ])
 def test_multiprocess_ipc(world, sigma, count, dtype, mover):
     if not torch.cuda.is_available():
@@ -39,7 +39,9 @@ def test_multiprocess_ipc(world, sigma, count, dtype, mover):
     import __graft_entry__
 
     __graft_entry__.build()
-    env = dict(os.environ, STRAGGLAR_MOVER=mover)
+    env = dict(os.environ, STRAGGLAR_MOVER=mover.split("+")[0])
+    if mover.endswith("+ll"):
+        env["STRAGGLAR_LL_MAX_CHUNK"] = "262144"
     r = subprocess.run([sys.executable, os.path.join(HERE, "mp_worker.py"), str(world), str(sigma), str(count), dtype,
                         str(_port())], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
