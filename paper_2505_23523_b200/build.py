@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libstragglar.so")
-SOURCES = ["api.cu", "kernels.cu", "schedule.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "kernels_i32.cu", "kernels_f32.cu", "kernels_bf16.cu", "schedule.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -48,11 +48,36 @@ def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB
     if not force and not defines and out == LIB and not needs_build():
         return LIB
     tmp = f"{out}.{os.getpid()}.tmp"        # concurrent builders (torchrun ranks) never share a temp file
-    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = tempfile.mkdtemp(prefix="stragglar_build_")
+    compile_flags = [f for f in FLAGS if f not in ("-shared",)]
+    defs = [f"-D{d}" for d in defines]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        r = subprocess.run([NVCC, *compile_flags, *defs, "-c", os.path.join(CSRC, src), "-o", obj],
+                           capture_output=True, text=True)
+        return src, obj, r
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    errs = [r for _, _, r in results if r.returncode != 0]
+    if errs:
+        for r in errs:
+            sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libstragglar.so")
+    link = subprocess.run([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+                           *[o for _, o, _ in results], "-o", tmp], capture_output=True, text=True)
+    if link.returncode != 0:
+        sys.stderr.write(link.stdout + link.stderr)
+        raise RuntimeError("nvcc failed linking libstragglar.so")
+
+    class _Res:
+        stderr = "".join(r.stderr for _, _, r in results)
+
+    res = _Res()
     if out == LIB:
         with open(os.path.join(HERE, "ptxas_report.txt"), "w") as f:
             f.write(res.stderr)

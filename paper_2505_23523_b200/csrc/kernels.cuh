@@ -1,0 +1,931 @@
+// StragglAR kernels for sm_100a.
+//
+//   k_phase<..., KIND> one persistent kernel template for the method:
+//     KIND 0  Phase A: owner g pulls its chunk from the
+//             n-2 other non-stragglers, sums in canonical order (ascending
+//             physical rank, fp32 accumulation), stores in place.  Replaces
+//             ncclReduceScatter.                      [rs_body]
+//     KIND 1  Phase B (Algorithm 1): round executor; each CTA owns
+//             one slice of every chunk and walks its rank's op list in round
+//             order; the straggler exchange is fused with its
+//             reduction (P:347's separate reduction kernels become one pass).
+//                                                              [complete_body]
+//     KIND 3  Phase B as a one-round direct completion (NEXT N1(ii)). [direct_body]
+//     KIND 4  Phase A then Phase B (schedule) in one launch (single-call API).
+//     KIND 5  Phase A then direct completion in one launch.
+//   k_ring            hand-written Ring baseline, pull-based.
+//   k_delay           the paper's idle kernel on %globaltimer.
+//   k_barrier         device barrier among ranks (bench start line).
+//
+// One launch serves `nlocal` ranks: 1 in the per-process (NVLink) mode, all
+// of them in the single-device team mode (block b works for local rank b/G,
+// slice b%G).  All CTAs of a launch must be co-resident (cooperative launch),
+// because they spin on flags produced by CTAs of other ranks.
+#pragma once
+#include "device.cuh"
+#include "plan.h"
+
+namespace stragglar {
+
+// ---------------------------------------------------------------- flags
+__device__ __forceinline__ bool flag_ok(uint32_t v, uint32_t epoch) { return int32_t(v - epoch) >= 0; }
+
+// Spin (one thread) until *f >= epoch.  Bounded by the watchdog; gives up
+// early if another CTA of this process already reported an error.
+static __device__ bool spin_wait(const uint32_t* f, uint32_t epoch, const LaunchPlan& P, uint32_t where) {
+  const bool sys = P.sys_scope;
+  if (flag_ok(ld_acquire(f, sys), epoch)) return true;
+  const uint64_t t0 = globaltimer();
+  for (uint32_t it = 1;; ++it) {
+    if (flag_ok(ld_acquire(f, sys), epoch)) return true;
+    if (it > 2048) __nanosleep(32);
+    if ((it & 127) == 0) {
+      if (*(volatile uint32_t*)&P.state->err) return false;
+      if (globaltimer() - t0 > P.timeout_ns) {
+        if (atomicCAS(&P.state->err, 0u, (uint32_t)ERR_TIMEOUT) == 0u) atomicExch(&P.state->err_info, where);
+        return false;
+      }
+    }
+  }
+}
+
+// Whole-CTA wait: thread 0 spins, the barrier publishes the acquired state.
+__device__ __forceinline__ bool cta_wait(const uint32_t* f, uint32_t epoch, const LaunchPlan& P, uint32_t where) {
+  int ok = 1;
+  if (threadIdx.x == 0) ok = spin_wait(f, epoch, P, where);
+  return __syncthreads_and(ok);
+}
+
+// Whole-CTA signal: all prior stores of the CTA happen-before the flag store.
+__device__ __forceinline__ void cta_signal(uint32_t* f, uint32_t epoch, bool sys) {
+  __syncthreads();
+  if (threadIdx.x == 0) st_release(f, epoch, sys);
+}
+
+// The call's epoch lives in device memory (state->epoch + 1), so a captured
+// CUDA graph replays correctly: the last CTA to leave the call's final kernel
+// increments it, after every CTA of every kernel of the call has read it.
+__device__ __forceinline__ uint32_t call_epoch(const LaunchPlan& P) {
+  return *(volatile const uint32_t*)&P.state->epoch + 1u;
+}
+__device__ __forceinline__ void finish_call(const LaunchPlan& P) {
+  if (!P.last_kernel) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const uint32_t prev = atomicAdd(&P.state->exit_count, 1u);
+    if (prev == gridDim.x - 1) {
+      P.state->exit_count = 0;
+      __threadfence();
+      atomicAdd(&P.state->epoch, 1u);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t* flag_at(uint32_t* base, int slot, int G, int s) {
+  return base + (size_t)slot * G + s;
+}
+
+// ---------------------------------------------------------------- ranges
+struct Range {
+  uint64_t lo, hi;  // elements
+};
+
+// Slice s of [clo, chi): an even split of the 16-byte vectors; identical on
+// every rank (it depends only on count, world and G).
+__device__ __forceinline__ Range slice_of(uint64_t clo, uint64_t chi, int s, int G, int V) {
+  const uint64_t nv = (chi - clo + V - 1) / V;
+  const uint64_t a = nv * (uint64_t)s / G, b = nv * (uint64_t)(s + 1) / G;
+  Range r;
+  r.lo = clo + a * V;
+  r.hi = clo + b * V < chi ? clo + b * V : chi;
+  if (r.lo > r.hi) r.lo = r.hi;
+  return r;
+}
+
+__device__ __forceinline__ Range chunk_range(const LaunchPlan& P, int c) {
+  uint64_t lo = (uint64_t)c * P.ce, hi = lo + P.ce;
+  if (lo > P.count) lo = P.count;
+  if (hi > P.count) hi = P.count;
+  return {lo, hi};
+}
+
+// ---------------------------------------------------------------- data movers
+constexpr int kUnroll = 8;
+#ifndef STRAGGLAR_MIN_BLOCKS
+#define STRAGGLAR_MIN_BLOCKS 4
+#endif
+constexpr int kMinBlocks = STRAGGLAR_MIN_BLOCKS;  // 4 x 256 threads: <= 64 registers
+
+// dst <- src for 16-byte vectors [0, nv)
+__device__ __forceinline__ void copy_vecs(char* __restrict__ dst, const char* __restrict__ src, uint64_t nv) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  uint64_t i = threadIdx.x;
+  const uint64_t step = (uint64_t)kUnroll * blockDim.x;
+  for (; i + (kUnroll - 1) * blockDim.x < nv; i += step) {
+    uint4 v[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) v[u] = ld_vec(s + i + u * blockDim.x);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) st_vec(d + i + u * blockDim.x, v[u]);
+  }
+  for (; i < nv; i += blockDim.x) st_vec(d + i, ld_vec(s + i));
+}
+
+// d0 = d1 = a (+) b for 16-byte vectors [0, nv)  (fused exchange-reduce)
+template <int DT>
+__device__ __forceinline__ void add2_vecs(char* d0, char* d1, const char* a, const char* b, uint64_t nv) {
+  const uint4* pa = reinterpret_cast<const uint4*>(a);
+  const uint4* pb = reinterpret_cast<const uint4*>(b);
+  uint4* q0 = reinterpret_cast<uint4*>(d0);
+  uint4* q1 = reinterpret_cast<uint4*>(d1);
+  uint64_t i = threadIdx.x;
+  constexpr int U = 4;
+  const uint64_t step = (uint64_t)U * blockDim.x;
+  for (; i + (U - 1) * blockDim.x < nv; i += step) {
+    uint4 va[U], vb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      va[u] = ld_vec(pa + i + u * blockDim.x);
+      vb[u] = ld_vec(pb + i + u * blockDim.x);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint4 z = add_vec<DT>(va[u], vb[u]);
+      st_vec(q0 + i + u * blockDim.x, z);
+      if (q1) st_vec(q1 + i + u * blockDim.x, z);
+    }
+  }
+  for (; i < nv; i += blockDim.x) {
+    uint4 z = add_vec<DT>(ld_vec(pa + i), ld_vec(pb + i));
+    st_vec(q0 + i, z);
+    if (q1) st_vec(q1 + i, z);
+  }
+}
+
+// elementwise tail (< 16 bytes) of an add2
+template <int DT>
+__device__ __forceinline__ void add2_tail(char* d0, char* d1, const char* a, const char* b, int nelem, int esz) {
+  if ((int)threadIdx.x < nelem) {
+    const int o = threadIdx.x * esz;
+    scalar_add_store<DT>(d0 + o, d1 ? d1 + o : nullptr, a + o, b + o);
+  }
+}
+
+__device__ __forceinline__ void copy_tail(char* dst, const char* src, int nbytes) {
+  if ((int)threadIdx.x < nbytes) dst[threadIdx.x] = *(const volatile char*)(src + threadIdx.x);
+}
+
+// ---------------------------------------------------------------- TMA movers (cp.async.bulk)
+// A ring of kStages shared-memory stages per CTA.  Thread 0 issues bulk loads
+// (mbarrier complete_tx) kStages pieces ahead and bulk stores (bulk groups);
+// for the fused exchange every thread adds the two staged operands in shared
+// memory before the stores.  All threads track the per-stage mbarrier parity
+// identically, so the ring persists across the ops of a kernel.
+#ifndef STRAGGLAR_STAGES
+#define STRAGGLAR_STAGES 3
+#endif
+#ifndef STRAGGLAR_STAGE_BYTES
+#define STRAGGLAR_STAGE_BYTES 16384
+#endif
+constexpr int kStages = STRAGGLAR_STAGES;
+constexpr uint32_t kStageBytes = STRAGGLAR_STAGE_BYTES;
+constexpr int kTmaSmem = 128 + kStages * kStageBytes;
+
+struct Pipe {
+  uint64_t* bar;
+  char* stage;
+  uint32_t phase;  // bit s = parity to wait for on stage s
+  __device__ __forceinline__ char* buf(int s) const { return stage + (size_t)s * kStageBytes; }
+};
+
+// Shared-memory stage ring of the CTA (dynamic smem); mbarriers initialised once per launch.
+__device__ __forceinline__ Pipe make_pipe(bool active) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  Pipe p{reinterpret_cast<uint64_t*>(dsm), reinterpret_cast<char*>(dsm) + 128, 0u};
+  if (active) {
+    if (threadIdx.x == 0) {
+      for (int st = 0; st < kStages; ++st) mbar_init(&p.bar[st], 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+  }
+  return p;
+}
+
+__device__ __forceinline__ uint32_t advance_phase(uint32_t ph, uint32_t np) {
+#pragma unroll
+  for (int s = 0; s < kStages; ++s) {
+    const uint32_t uses = np / kStages + ((uint32_t)s < np % kStages ? 1u : 0u);
+    if (uses & 1u) ph ^= 1u << s;
+  }
+  return ph;
+}
+
+// dst <- src, nbytes a multiple of 16
+static __device__ void tma_copy(Pipe& p, char* dst, const char* src, uint64_t nbytes) {
+  const uint32_t np = (uint32_t)((nbytes + kStageBytes - 1) / kStageBytes);
+  if (threadIdx.x == 0 && np) {
+    fence_proxy_async_global();
+    auto issue = [&](uint32_t i) {
+      const int s = i % kStages;
+      const uint64_t off = (uint64_t)i * kStageBytes;
+      const uint32_t len = (uint32_t)((nbytes - off) < kStageBytes ? (nbytes - off) : kStageBytes);
+      mbar_expect_tx(&p.bar[s], len);
+      bulk_load(p.buf(s), src + off, len, &p.bar[s]);
+    };
+    for (uint32_t i = 0; i < np && i < (uint32_t)kStages; ++i) issue(i);
+    uint32_t ph = p.phase;
+    for (uint32_t i = 0; i < np; ++i) {
+      const int s = i % kStages;
+      mbar_wait(&p.bar[s], (ph >> s) & 1u);
+      ph ^= 1u << s;
+      const uint64_t off = (uint64_t)i * kStageBytes;
+      const uint32_t len = (uint32_t)((nbytes - off) < kStageBytes ? (nbytes - off) : kStageBytes);
+      bulk_store(dst + off, p.buf(s), len);
+      bulk_commit();
+      if (i + kStages < np) {
+        bulk_wait_read_all();
+        issue(i + kStages);
+      }
+    }
+    bulk_wait_all();
+    fence_proxy_async_global();
+  }
+  p.phase = advance_phase(p.phase, np);
+}
+
+// d0 = d1 = a (+) b through shared memory, nbytes a multiple of 16
+template <int DT>
+__device__ void tma_add2(Pipe& p, char* d0, char* d1, const char* a, const char* b, uint64_t nbytes) {
+  constexpr uint32_t kPiece = kStageBytes / 2;
+  const uint32_t np = (uint32_t)((nbytes + kPiece - 1) / kPiece);
+  auto piece_len = [&](uint32_t i) -> uint32_t {
+    const uint64_t off = (uint64_t)i * kPiece;
+    return (uint32_t)((nbytes - off) < kPiece ? (nbytes - off) : kPiece);
+  };
+  auto issue = [&](uint32_t i) {
+    const int s = i % kStages;
+    const uint64_t off = (uint64_t)i * kPiece;
+    const uint32_t len = piece_len(i);
+    mbar_expect_tx(&p.bar[s], 2 * len);
+    bulk_load(p.buf(s), a + off, len, &p.bar[s]);
+    bulk_load(p.buf(s) + kPiece, b + off, len, &p.bar[s]);
+  };
+  if (threadIdx.x == 0 && np) {
+    fence_proxy_async_global();
+    for (uint32_t i = 0; i < np && i < (uint32_t)kStages; ++i) issue(i);
+  }
+  uint32_t ph = p.phase;
+  for (uint32_t i = 0; i < np; ++i) {
+    const int s = i % kStages;
+    const uint32_t len = piece_len(i);
+    mbar_wait(&p.bar[s], (ph >> s) & 1u);
+    ph ^= 1u << s;
+    uint4* A = reinterpret_cast<uint4*>(p.buf(s));
+    const uint4* B = reinterpret_cast<const uint4*>(p.buf(s) + kPiece);
+    for (uint32_t v = threadIdx.x; v < len / 16; v += blockDim.x) A[v] = add_vec<DT>(A[v], B[v]);
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint64_t off = (uint64_t)i * kPiece;
+      bulk_store(d0 + off, A, len);
+      if (d1) bulk_store(d1 + off, A, len);
+      bulk_commit();
+      if (i + kStages < np) {
+        bulk_wait_read_all();
+        issue(i + kStages);
+      }
+    }
+  }
+  if (threadIdx.x == 0 && np) {
+    bulk_wait_all();
+    fence_proxy_async_global();
+  }
+  p.phase = ph;
+}
+
+// Phase A through shared memory: per stage, the W-1 non-straggler operands of
+// one piece (ascending physical order) are bulk-loaded, summed by the CTA in
+// canonical order into operand slot 0, and bulk-stored to the owner.
+template <int DT, int W>
+__device__ void tma_reduce(Pipe& p, char* dst, const char* const (&src)[W - 1], uint64_t lo_b, uint64_t nbytes) {
+  constexpr uint32_t kPiece = (kStageBytes / (W - 1)) / 16 * 16;
+  const uint32_t np = (uint32_t)((nbytes + kPiece - 1) / kPiece);
+  auto piece_len = [&](uint32_t i) -> uint32_t {
+    const uint64_t off = (uint64_t)i * kPiece;
+    return (uint32_t)((nbytes - off) < kPiece ? (nbytes - off) : kPiece);
+  };
+  auto issue = [&](uint32_t i) {
+    const int s = i % kStages;
+    const uint64_t off = lo_b + (uint64_t)i * kPiece;
+    const uint32_t len = piece_len(i);
+    mbar_expect_tx(&p.bar[s], (W - 1) * len);
+#pragma unroll
+    for (int j = 0; j < W - 1; ++j) bulk_load(p.buf(s) + j * kPiece, src[j] + off, len, &p.bar[s]);
+  };
+  if (threadIdx.x == 0 && np) {
+    fence_proxy_async_global();
+    for (uint32_t i = 0; i < np && i < (uint32_t)kStages; ++i) issue(i);
+  }
+  uint32_t ph = p.phase;
+  for (uint32_t i = 0; i < np; ++i) {
+    const int s = i % kStages;
+    const uint32_t len = piece_len(i);
+    mbar_wait(&p.bar[s], (ph >> s) & 1u);
+    ph ^= 1u << s;
+    char* base = p.buf(s);
+    for (uint32_t v = threadIdx.x; v < len / 16; v += blockDim.x) {
+      Acc<DT> acc;
+      acc.init(reinterpret_cast<const uint4*>(base)[v]);
+#pragma unroll
+      for (int j = 1; j < W - 1; ++j) acc.add(reinterpret_cast<const uint4*>(base + j * kPiece)[v]);
+      reinterpret_cast<uint4*>(base)[v] = acc.get();
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bulk_store(dst + lo_b + (uint64_t)i * kPiece, base, len);
+      bulk_commit();
+      if (i + kStages < np) {
+        bulk_wait_read_all();
+        issue(i + kStages);
+      }
+    }
+  }
+  if (threadIdx.x == 0 && np) {
+    bulk_wait_all();
+    fence_proxy_async_global();
+  }
+  p.phase = ph;
+}
+
+// a (+) b through shared memory, stored at offset lo_b of all W buffers
+template <int DT, int W>
+__device__ void tma_add_bcast(Pipe& p, char* const* dst, const char* a, const char* b, uint64_t lo_b,
+                              uint64_t nbytes) {
+  constexpr uint32_t kPiece = kStageBytes / 2;
+  const uint32_t np = (uint32_t)((nbytes + kPiece - 1) / kPiece);
+  auto piece_len = [&](uint32_t i) -> uint32_t {
+    const uint64_t off = (uint64_t)i * kPiece;
+    return (uint32_t)((nbytes - off) < kPiece ? (nbytes - off) : kPiece);
+  };
+  auto issue = [&](uint32_t i) {
+    const int s = i % kStages;
+    const uint64_t off = lo_b + (uint64_t)i * kPiece;
+    const uint32_t len = piece_len(i);
+    mbar_expect_tx(&p.bar[s], 2 * len);
+    bulk_load(p.buf(s), a + off, len, &p.bar[s]);
+    bulk_load(p.buf(s) + kPiece, b + off, len, &p.bar[s]);
+  };
+  if (threadIdx.x == 0 && np) {
+    fence_proxy_async_global();
+    for (uint32_t i = 0; i < np && i < (uint32_t)kStages; ++i) issue(i);
+  }
+  uint32_t ph = p.phase;
+  for (uint32_t i = 0; i < np; ++i) {
+    const int s = i % kStages;
+    const uint32_t len = piece_len(i);
+    mbar_wait(&p.bar[s], (ph >> s) & 1u);
+    ph ^= 1u << s;
+    uint4* A = reinterpret_cast<uint4*>(p.buf(s));
+    const uint4* B = reinterpret_cast<const uint4*>(p.buf(s) + kPiece);
+    for (uint32_t v = threadIdx.x; v < len / 16; v += blockDim.x) A[v] = add_vec<DT>(A[v], B[v]);
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const uint64_t off = lo_b + (uint64_t)i * kPiece;
+#pragma unroll
+      for (int d = 0; d < W; ++d) bulk_store(dst[d] + off, A, len);
+      bulk_commit();
+      if (i + kStages < np) {
+        bulk_wait_read_all();
+        issue(i + kStages);
+      }
+    }
+  }
+  if (threadIdx.x == 0 && np) {
+    bulk_wait_all();
+    fence_proxy_async_global();
+  }
+  p.phase = ph;
+}
+
+// LSU version of the same
+template <int DT, int W>
+__device__ void lsu_add_bcast(char* const* dst, const char* a, const char* b, uint64_t lo_b, uint64_t nbytes) {
+  const uint64_t nv = nbytes / 16;
+  constexpr int U = 4;
+  uint64_t i = threadIdx.x;
+  for (; i + (U - 1) * blockDim.x < nv; i += (uint64_t)U * blockDim.x) {
+    uint4 va[U], vb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      va[u] = ld_vec(a + lo_b + (i + u * blockDim.x) * 16);
+      vb[u] = ld_vec(b + lo_b + (i + u * blockDim.x) * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint4 z = add_vec<DT>(va[u], vb[u]);
+#pragma unroll
+      for (int d = 0; d < W; ++d) st_vec(dst[d] + lo_b + (i + u * blockDim.x) * 16, z);
+    }
+  }
+  for (; i < nv; i += blockDim.x) {
+    const uint4 z = add_vec<DT>(ld_vec(a + lo_b + i * 16), ld_vec(b + lo_b + i * 16));
+#pragma unroll
+    for (int d = 0; d < W; ++d) st_vec(dst[d] + lo_b + i * 16, z);
+  }
+}
+
+// ---------------------------------------------------------------- Phase A
+// Canonical sum of the slice over the non-stragglers in ascending physical order.
+template <int DT, int W>
+__device__ void rs_slice(const LaunchPlan& P, const char* const (&src)[W - 1], char* dst, uint64_t lo_b, uint64_t hi_b) {
+  const uint64_t nv = (hi_b - lo_b) / 16;
+  constexpr int U = (W <= 4) ? 4 : 2;
+  uint64_t i = threadIdx.x;
+  const uint64_t step = (uint64_t)U * blockDim.x;
+  for (; i + (U - 1) * blockDim.x < nv; i += step) {
+    uint4 v[U][W - 1];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int j = 0; j < W - 1; ++j) v[u][j] = ld_vec(src[j] + lo_b + (i + u * blockDim.x) * 16);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      Acc<DT> acc;
+      acc.init(v[u][0]);
+#pragma unroll
+      for (int j = 1; j < W - 1; ++j) acc.add(v[u][j]);
+      st_vec(dst + lo_b + (i + u * blockDim.x) * 16, acc.get());
+    }
+  }
+  for (; i < nv; i += blockDim.x) {
+    Acc<DT> acc;
+    acc.init(ld_vec(src[0] + lo_b + i * 16));
+#pragma unroll
+    for (int j = 1; j < W - 1; ++j) acc.add(ld_vec(src[j] + lo_b + i * 16));
+    st_vec(dst + lo_b + i * 16, acc.get());
+  }
+  // tail: fewer than 16 bytes at the very end of the buffer
+  const int tail = (int)((hi_b - lo_b) % 16) / P.esize;
+  if ((int)threadIdx.x < tail) {
+    const uint64_t o = lo_b + nv * 16 + threadIdx.x * P.esize;
+    if constexpr (DT == DT_BF16) {
+      float a = 0.f;
+#pragma unroll
+      for (int j = 0; j < W - 1; ++j) {
+        float x = __uint_as_float(uint32_t(*(const volatile uint16_t*)(src[j] + o)) << 16);
+        a = (j == 0) ? x : __fadd_rn(a, x);
+      }
+      __nv_bfloat16 h = __float2bfloat16_rn(a);
+      *(volatile uint16_t*)(dst + o) = *reinterpret_cast<uint16_t*>(&h);
+    } else {
+      uint32_t a = *(const volatile uint32_t*)(src[0] + o);
+#pragma unroll
+      for (int j = 1; j < W - 1; ++j) a = add_word<DT>(a, *(const volatile uint32_t*)(src[j] + o));
+      *(volatile uint32_t*)(dst + o) = a;
+    }
+  }
+}
+
+// Phase A body for non-straggler `me`, slice s.
+template <int DT, int W, int MV>
+__device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
+  const int G = P.G;
+  if (blockIdx.x == 0 && threadIdx.x == 0) P.state->t_rs_start = globaltimer();
+  // barrier (1) among the non-stragglers, per slice
+  if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep, P.sys_scope);
+  if (threadIdx.x == 0) {
+    bool ok = true;
+    for (int p = 0; p < W && ok; ++p)
+      if (p != me && p != P.sigma)
+        ok = spin_wait(flag_at(P.flags[me], SLOT_ARRIVE + p, G, s), ep, P, 0x100 | p);
+    (void)ok;
+  }
+  if (!__syncthreads_and(*(volatile uint32_t*)&P.state->err == 0)) return;
+
+  const int g = P.logical_of_phys[me];  // owned chunk
+  const Range c = chunk_range(P, g);
+  const Range r = slice_of(c.lo, c.hi, s, G, 16 / P.esize);
+  // non-stragglers in ascending physical order (compile-time indices, no local memory)
+  const char* src[W - 1];
+#pragma unroll
+  for (int j = 0; j < W - 1; ++j) src[j] = P.buf[j < P.sigma ? j : j + 1];
+  // with two ranks the owner's chunk already is the non-straggler "sum"
+  if constexpr (W > 2) {
+    if constexpr (MV == MOVER_TMA) {
+      const uint64_t lo_b = r.lo * P.esize, hi_b = r.hi * P.esize;
+      const uint64_t body = (hi_b - lo_b) / 16 * 16;
+      tma_reduce<DT, W>(pipe, P.buf[me], src, lo_b, body);
+      rs_slice<DT, W>(P, src, P.buf[me], lo_b + body, hi_b);   // < 16-byte tail only
+    } else {
+      rs_slice<DT, W>(P, src, P.buf[me], r.lo * P.esize, r.hi * P.esize);
+    }
+  }
+  // "partial ready" for the straggler's half of the exchange
+  cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, G, s), ep, P.sys_scope);
+}
+
+// ---------------------------------------------------------------- LL Phase B (small chunks)
+// Low-latency variant of complete_body: every transfer is a stream of 8-byte
+// words (4 payload bytes | epoch << 32) stored into the receiver's LL area; the
+// receiver polls the words themselves.  No release fence, no separate flag and
+// no store-completion wait per hop, and no CTA-wide synchronisation: thread t
+// of slice s owns the same words of a chunk in every op, so each thread runs
+// its own words through the rounds (the dependency order is the schedule's
+// round order, as in complete_body).  Same arithmetic per word, same bits.
+#ifndef STRAGGLAR_LL_GENTLE
+#define STRAGGLAR_LL_GENTLE 0
+#endif
+constexpr int kLLBatch = 8;
+
+__device__ __forceinline__ uint32_t ld_word(const char* buf, uint64_t o, uint64_t end) {
+  if (o + 4 <= end) return *reinterpret_cast<const uint32_t*>(buf + o);
+  return (uint32_t)(*reinterpret_cast<const uint16_t*>(buf + o));   // bf16 tail: 2 valid bytes
+}
+__device__ __forceinline__ void st_word(char* buf, uint64_t o, uint64_t end, uint32_t v) {
+  if (o + 4 <= end)
+    *reinterpret_cast<uint32_t*>(buf + o) = v;
+  else
+    *reinterpret_cast<uint16_t*>(buf + o) = (uint16_t)v;
+}
+
+// Poll kLLBatch words (w = base + j*nthr < wend) of `ll` until they carry epoch ep.
+__device__ __forceinline__ bool ll_poll_batch(const uint64_t* ll, uint64_t base, uint64_t wend, uint32_t ep,
+                                              uint32_t (&val)[kLLBatch], const LaunchPlan& P, uint32_t where) {
+  const bool sys = P.sys_scope;
+  const uint32_t nthr = blockDim.x;
+  uint64_t v[kLLBatch];
+#pragma unroll
+  for (int j = 0; j < kLLBatch; ++j) {
+    const uint64_t w = base + (uint64_t)j * nthr;
+    v[j] = (w < wend) ? ld_ll(ll + w, sys) : ((uint64_t)ep << 32);
+  }
+  uint64_t t0 = 0;
+  for (uint32_t it = 0;; ++it) {
+    bool all = true;
+#if STRAGGLAR_LL_GENTLE
+    // poll one outstanding word at a time (words of a batch arrive together)
+#pragma unroll
+    for (int j = 0; j < kLLBatch; ++j) {
+      if (all && (uint32_t)(v[j] >> 32) != ep) {
+        all = false;
+        v[j] = ld_ll(ll + base + (uint64_t)j * nthr, sys);
+      }
+    }
+    if (!all) __nanosleep(STRAGGLAR_LL_GENTLE);
+#else
+#pragma unroll
+    for (int j = 0; j < kLLBatch; ++j) {
+      if ((uint32_t)(v[j] >> 32) != ep) {
+        all = false;
+        v[j] = ld_ll(ll + base + (uint64_t)j * nthr, sys);
+      }
+    }
+#endif
+    if (all) break;
+    if (it == 0) t0 = globaltimer();
+    if ((it & 255) == 255) {
+      if (*(volatile uint32_t*)&P.state->err) return false;
+      if (globaltimer() - t0 > P.timeout_ns) {
+        if (atomicCAS(&P.state->err, 0u, (uint32_t)ERR_TIMEOUT) == 0u) atomicExch(&P.state->err_info, where);
+        return false;
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kLLBatch; ++j) val[j] = (uint32_t)v[j];
+  return true;
+}
+
+// word-stream modes
+enum LLMode : int { LL_PUSH = 0, LL_EXCH = 1, LL_FWD = 2, LL_FWD_UNPACK = 3, LL_UNPACK = 4 };
+
+// Words [wa, wb) of one chunk slice.  ub: user buffer, cb0: the chunk's first
+// byte in it, end: buffer byte end; mll: my LL area of the chunk, pll: the
+// peer's LL area of the chunk (unused for LL_UNPACK).
+template <int DT, int MODE>
+__device__ bool ll_words(char* ub, uint64_t cb0, uint64_t end, const uint64_t* mll, uint64_t* pll, uint64_t wa,
+                         uint64_t wb, uint32_t ep, const LaunchPlan& P, uint32_t where) {
+  const bool sys = P.sys_scope;
+  const uint32_t nthr = blockDim.x;
+  for (uint64_t base = wa + threadIdx.x; base < wb; base += (uint64_t)kLLBatch * nthr) {
+    uint32_t val[kLLBatch];
+    if constexpr (MODE != LL_PUSH) {
+      if (!ll_poll_batch(mll, base, wb, ep, val, P, where)) return false;
+    }
+#pragma unroll
+    for (int j = 0; j < kLLBatch; ++j) {
+      const uint64_t w = base + (uint64_t)j * nthr;
+      if (w >= wb) break;
+      const uint64_t o = cb0 + 4 * w;
+      if constexpr (MODE == LL_PUSH) {
+        st_ll(pll + w, ld_word(ub, o, end), ep, sys);
+      } else if constexpr (MODE == LL_EXCH) {
+        const uint32_t z = add_word<DT>(ld_word(ub, o, end), val[j]);
+        st_word(ub, o, end, z);
+        st_ll(pll + w, z, ep, sys);
+      } else if constexpr (MODE == LL_FWD) {
+        st_ll(pll + w, val[j], ep, sys);
+      } else if constexpr (MODE == LL_FWD_UNPACK) {
+        st_word(ub, o, end, val[j]);
+        st_ll(pll + w, val[j], ep, sys);
+      } else {
+        st_word(ub, o, end, val[j]);
+      }
+    }
+  }
+  return true;
+}
+
+template <int DT, int W>
+__device__ void ll_phase_b(const LaunchPlan& P, int s, int me, uint32_t ep) {
+  const int G = P.G, V = 16 / P.esize, es = P.esize;
+  const uint64_t end = P.count * es;
+  char* ub = P.buf[me];
+  const int own = (me == P.sigma) ? -1 : P.logical_of_phys[me];
+  uint32_t unpacked = 0;   // chunks whose LL words were already written to the user buffer
+  // which half of chunk c this rank computed itself in the exchange: 1 low, 2 high, 0 none
+  auto local_half = [&](int c) { return c == own ? 1 : (me == P.sigma ? 2 : 0); };
+  struct Words {
+    uint64_t cb0, wa, wm, wb;
+  };
+  auto words_of = [&](int c) {
+    const Range cr = chunk_range(P, c);
+    const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
+    const uint64_t nvec = (sl.hi - sl.lo + V - 1) / V;
+    const uint64_t mid = sl.lo + (nvec / 2) * V < sl.hi ? sl.lo + (nvec / 2) * V : sl.hi;
+    Words w;
+    w.cb0 = cr.lo * es;
+    w.wa = (sl.lo * es - w.cb0) / 4;
+    w.wm = (mid * es - w.cb0) / 4;
+    w.wb = (sl.hi * es - w.cb0 + 3) / 4;
+    return w;
+  };
+  bool ok = true;
+  // Exchange operands go out first, so every exchange only waits for its
+  // partner's operand (as the flag protocol's exchange only waits for Phase A),
+  // not for the partner to reach that round: non-stragglers send the
+  // straggler their partial of its half of their chunk; the straggler sends
+  // every owner x_sigma for the owner's half.
+  if (me == P.sigma) {
+    for (int c = 0; c < P.nchunks; ++c) {
+      int owner = 0;
+#pragma unroll
+      for (int q = 0; q < W; ++q)
+        if (P.logical_of_phys[q] == c) owner = q;
+      const Words w = words_of(c);
+      ll_words<DT, LL_PUSH>(ub, w.cb0, end, nullptr, P.ll[owner] + (size_t)c * kLLChunkWords, w.wa, w.wm, ep, P, 0);
+    }
+  } else {
+    const Words w = words_of(own);
+    ll_words<DT, LL_PUSH>(ub, w.cb0, end, nullptr, P.ll[P.sigma] + (size_t)own * kLLChunkWords, w.wm, w.wb, ep, P,
+                          0);
+  }
+  for (int k = 0; k < P.nops[me] && ok; ++k) {
+    const Op op = P.ops[me][k];
+    const int c = op.chunk, peer = op.peer;
+    const Words w = words_of(c);
+    const uint64_t* mll = P.ll[me] + (size_t)c * kLLChunkWords;
+    uint64_t* pll = P.ll[peer] + (size_t)c * kLLChunkWords;
+    const uint32_t where = 0xB00 | k;
+    if (op.kind == OP_EXCH_LOW) {
+      // my half: x_sigma arrived (pushed up front), add, keep, send the result
+      ok = ll_words<DT, LL_EXCH>(ub, w.cb0, end, mll, pll, w.wa, w.wm, ep, P, where);
+    } else if (op.kind == OP_EXCH_HIGH) {
+      ok = ll_words<DT, LL_EXCH>(ub, w.cb0, end, mll, pll, w.wm, w.wb, ep, P, where);
+    } else {
+      const int lh = local_half(c);
+      const bool first = !((unpacked >> c) & 1u);
+      const uint64_t l0 = lh == 1 ? w.wa : w.wm, l1 = lh == 1 ? w.wm : w.wb;   // local half (if any)
+      const uint64_t r0 = lh == 1 ? w.wm : w.wa, r1 = lh == 1 ? w.wb : w.wm;   // LL half
+      if (lh) ll_words<DT, LL_PUSH>(ub, w.cb0, end, mll, pll, l0, l1, ep, P, where);
+      const uint64_t f0 = lh ? r0 : w.wa, f1 = lh ? r1 : w.wb;
+      ok = first ? ll_words<DT, LL_FWD_UNPACK>(ub, w.cb0, end, mll, pll, f0, f1, ep, P, where)
+                 : ll_words<DT, LL_FWD>(ub, w.cb0, end, mll, pll, f0, f1, ep, P, where);
+      unpacked |= 1u << c;
+    }
+  }
+  // postcondition: the LL words of every chunk not yet forwarded land in the buffer
+  for (int c = 0; c < P.nchunks && ok; ++c) {
+    if ((unpacked >> c) & 1u) continue;
+    const Words w = words_of(c);
+    const uint64_t* mll = P.ll[me] + (size_t)c * kLLChunkWords;
+    const int lh = local_half(c);
+    const uint64_t f0 = lh == 1 ? w.wm : w.wa, f1 = lh == 2 ? w.wm : w.wb;
+    ok = ll_words<DT, LL_UNPACK>(ub, w.cb0, end, mll, nullptr, f0, f1, ep, P, 0xD00 | c);
+  }
+}
+
+// Phase B body (Algorithm 1 round executor) for rank `me`, slice s.
+template <int DT, int W, int MV>
+__device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
+  const int G = P.G;
+  const int V = 16 / P.esize;
+  constexpr bool tma = MV == MOVER_TMA;
+  if (P.use_ll) {
+    ll_phase_b<DT, W>(P, s, me, ep);
+    return;
+  }
+  // the straggler reaches barrier (2): announce per slice to the others
+  if (me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep, P.sys_scope);
+  char* mine = P.buf[me];
+  const int nops = P.nops[me];
+  for (int k = 0; k < nops; ++k) {
+    const Op op = P.ops[me][k];
+    const int c = op.chunk, peer = op.peer;
+    const Range cr = chunk_range(P, c);
+    const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
+    const uint64_t nvec_total = (sl.hi - sl.lo + V - 1) / V;
+    const uint64_t mid = sl.lo + (nvec_total / 2) * V < sl.hi ? sl.lo + (nvec_total / 2) * V : sl.hi;
+    if (op.kind == OP_EXCH_LOW) {
+      // non-straggler r: [lo, mid) of c_r = partial_r (+) x_sigma, stored at both ends
+      if (!cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, G, s), ep, P, 0x200 | k)) break;
+      const uint64_t a = sl.lo * P.esize, b = mid * P.esize;
+      if constexpr (tma)
+        tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, (b - a) / 16 * 16);
+      else
+        add2_vecs<DT>(mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, (b - a) / 16);
+      add2_tail<DT>(mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
+                    mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
+                    (int)((b - a) % 16) / P.esize, P.esize);
+      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep, P.sys_scope);
+    } else if (op.kind == OP_EXCH_HIGH) {
+      // straggler: [mid, hi) of c_r; waits for rank r's Phase-A partial
+      if (!cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, G, s), ep, P, 0x300 | k)) break;
+      const uint64_t a = mid * P.esize, b = sl.hi * P.esize;
+      if constexpr (tma)
+        tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, (b - a) / 16 * 16);
+      else
+        add2_vecs<DT>(mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, (b - a) / 16);
+      add2_tail<DT>(mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
+                    P.buf[peer] + a + (b - a) / 16 * 16, mine + a + (b - a) / 16 * 16,
+                    (int)((b - a) % 16) / P.esize, P.esize);
+      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep, P.sys_scope);
+    } else {
+      // copy of a fully reduced chunk (push)
+      if (!cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x400 | k)) break;
+      const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
+      if constexpr (tma)
+        tma_copy(pipe, P.buf[peer] + a, mine + a, (b - a) / 16 * 16);
+      else
+        copy_vecs(P.buf[peer] + a, mine + a, (b - a) / 16);
+      copy_tail(P.buf[peer] + a + (b - a) / 16 * 16, mine + a + (b - a) / 16 * 16, (int)((b - a) % 16));
+      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep, P.sys_scope);
+    }
+  }
+  // postcondition: every chunk has landed here
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < P.nchunks; ++c)
+      if (!spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x500 | c)) break;
+  }
+}
+
+// Direct completion body (NEXT N1(ii)): one round instead of Algorithm 1's
+// n + log n - 2.  Owner g (non-straggler) fully reduces its chunk (partial +
+// x_sigma, the straggler exchange's single add) and stores the
+// result to every rank.  On NVSwitch every port then carries about S bytes
+// (vs R*C = 9/7 S for the pairwise schedule at n = 8): the fabric is not
+// single-port (the P:149-150 assumption).
+template <int DT, int W, int MV>
+__device__ void direct_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
+  const int G = P.G;
+  const int V = 16 / P.esize;
+  constexpr bool tma = MV == MOVER_TMA;
+  int own = -1;
+  if (me == P.sigma) {
+    // the straggler arrives: its buffer may now be read by every owner
+    if (threadIdx.x < W && (int)threadIdx.x != me)
+      st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep, P.sys_scope);
+  } else {
+    own = P.logical_of_phys[me];
+    if (cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + P.sigma, G, s), ep, P, 0x900)) {
+      const Range cr = chunk_range(P, own);
+      const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
+      const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
+      const uint64_t body = (b - a) / 16 * 16;
+      // every rank's buffer, own included, receives the fully reduced slice
+      if constexpr (tma)
+        tma_add_bcast<DT, W>(pipe, P.buf, P.buf[me], P.buf[P.sigma], a, body);
+      else
+        lsu_add_bcast<DT, W>(P.buf, P.buf[me], P.buf[P.sigma], a, body);
+      const int tail = (int)((b - a) % 16) / P.esize;
+      if ((int)threadIdx.x < tail) {
+        // read both operands before any store (the own buffer is a destination)
+        const uint64_t o = a + body + threadIdx.x * P.esize;
+        char tmp[4];
+        scalar_add_store<DT>(tmp, nullptr, P.buf[me] + o, P.buf[P.sigma] + o);
+#pragma unroll
+        for (int d = 0; d < W; ++d) {
+          if (P.esize == 2)
+            *(volatile uint16_t*)(P.buf[d] + o) = *reinterpret_cast<uint16_t*>(tmp);
+          else
+            *(volatile uint32_t*)(P.buf[d] + o) = *reinterpret_cast<uint32_t*>(tmp);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x < W && (int)threadIdx.x != me)
+        st_release(flag_at(P.flags[threadIdx.x], SLOT_HAVE + own, G, s), ep, P.sys_scope);
+    }
+  }
+  // postcondition: every other chunk has landed here
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < P.nchunks; ++c)
+      if (c != own && !spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0xA00 | c)) break;
+  }
+}
+
+// KIND: 0 Phase A only, 1 Phase B (schedule), 3 Phase B (direct),
+//       4 Phase A + schedule in one launch, 5 Phase A + direct in one launch.
+template <int DT, int W, int MV, int KIND>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_constant__ LaunchPlan P) {
+  const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
+  const int me = P.local_rank[li];
+  const uint32_t ep = call_epoch(P);
+  Pipe pipe = make_pipe(MV == MOVER_TMA);
+  if constexpr (KIND == 0 || KIND == 4 || KIND == 5)
+    if (me != P.sigma) rs_body<DT, W, MV>(P, pipe, s, me, ep);
+  if constexpr (KIND == 1 || KIND == 4) complete_body<DT, W, MV>(P, pipe, s, me, ep);
+  if constexpr (KIND == 3 || KIND == 5) direct_body<DT, W, MV>(P, pipe, s, me, ep);
+  finish_call(P);
+}
+
+// ---------------------------------------------------------------- Ring
+// Physical ring 0 -> 1 -> ... -> n-1 -> 0 with n chunks.  Step t < n-1: pull
+// the left neighbour's partial of chunk (j-1-t) and add the own data (RS);
+// step t >= n-1: copy the left neighbour's final chunk (j-t+n-1) (AllGather).
+template <int DT, int W, int MV>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_constant__ LaunchPlan P) {
+  const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
+  const int j = P.local_rank[li];
+  const int G = P.G;
+  const int V = 16 / P.esize;
+  const uint32_t ep = call_epoch(P);
+  const int left = (j + W - 1) % W, right = (j + 1) % W;
+  if (threadIdx.x == 0) st_release(flag_at(P.flags[right], SLOT_RING_ARRIVE, G, s), ep, P.sys_scope);
+  constexpr bool tma = MV == MOVER_TMA;
+  Pipe pipe = make_pipe(tma);
+  char* mine = P.buf[j];
+  const char* lbuf = P.buf[left];
+  for (int t = 0; t < 2 * (W - 1); ++t) {
+    const int wslot = (t == 0) ? SLOT_RING_ARRIVE : SLOT_RING_READY + t - 1;
+    if (!cta_wait(flag_at(P.flags[j], wslot, G, s), ep, P, 0x600 | t)) {
+      finish_call(P);
+      return;
+    }
+    const int k = (t < W - 1) ? ((j - 1 - t) % W + 2 * W) % W : ((j - t + W - 1) % W + 2 * W) % W;
+    const Range cr = chunk_range(P, k);
+    const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
+    const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
+    const uint64_t nv = (b - a) / 16;
+    if (t < W - 1) {
+      if constexpr (tma)
+        tma_add2<DT>(pipe, mine + a, nullptr, lbuf + a, mine + a, nv * 16);
+      else
+        add2_vecs<DT>(mine + a, nullptr, lbuf + a, mine + a, nv);
+      add2_tail<DT>(mine + a + nv * 16, nullptr, lbuf + a + nv * 16, mine + a + nv * 16, (int)((b - a) % 16) / P.esize,
+                    P.esize);
+    } else {
+      if constexpr (tma)
+        tma_copy(pipe, mine + a, lbuf + a, nv * 16);
+      else
+        copy_vecs(mine + a, lbuf + a, nv);
+      copy_tail(mine + a + nv * 16, lbuf + a + nv * 16, (int)((b - a) % 16));
+    }
+    if (t < 2 * (W - 1) - 1) cta_signal(flag_at(P.flags[right], SLOT_RING_READY + t, G, s), ep, P.sys_scope);
+  }
+  // I am done reading the left buffer; wait until the right neighbour is done with mine
+  cta_signal(flag_at(P.flags[left], SLOT_RING_DONE, G, s), ep, P.sys_scope);
+  cta_wait(flag_at(P.flags[j], SLOT_RING_DONE, G, s), ep, P, 0x700);
+  finish_call(P);
+}
+
+template <int DT, int W, int MV>
+inline void* kernel_ptr_mv(int which) {
+  switch (which) {
+    case 0: return (void*)k_phase<DT, W, MV, 0>;   // Phase A
+    case 1: return (void*)k_phase<DT, W, MV, 1>;   // Phase B, Algorithm 1 schedule
+    case 2: return (void*)k_ring<DT, W, MV>;
+    case 3: return (void*)k_phase<DT, W, MV, 3>;   // Phase B, direct completion
+    case 4: return (void*)k_phase<DT, W, MV, 4>;   // A + B (schedule), one launch
+    case 5: return (void*)k_phase<DT, W, MV, 5>;   // A + B (direct), one launch
+    default: return nullptr;
+  }
+}
+
+template <int DT, int W>
+inline void* kernel_ptr(int which, int mover) {
+  return mover == MOVER_TMA ? kernel_ptr_mv<DT, W, MOVER_TMA>(which) : kernel_ptr_mv<DT, W, MOVER_LSU>(which);
+}
+
+// Per-dtype instantiation units (kernels_i32.cu, kernels_f32.cu, kernels_bf16.cu)
+void* select_kernel_i32(int which, int world, int mover);
+void* select_kernel_f32(int which, int world, int mover);
+void* select_kernel_bf16(int which, int world, int mover);
+
+}  // namespace stragglar
