@@ -190,6 +190,22 @@ __device__ __forceinline__ void copy_tail(char* dst, const char* src, int nbytes
 #define STRAGGLAR_STAGE_BYTES 16384
 #endif
 constexpr int kStages = STRAGGLAR_STAGES;
+// Refill lag: 1 = a stage is refilled one iteration after its stores were
+// issued (wait_group.read 1: the newest piece's stores may still be reading
+// shared memory while the next piece is computed); 0 = refill right after
+// the stores (wait_group.read 0, serialises store reads with compute).
+#ifndef STRAGGLAR_TMA_LAG
+#define STRAGGLAR_TMA_LAG 1
+#endif
+constexpr int kAhead = kStages - STRAGGLAR_TMA_LAG;   // pieces loaded ahead
+
+__device__ __forceinline__ void ring_release_wait() {
+#if STRAGGLAR_TMA_LAG
+  bulk_wait_read_1();
+#else
+  bulk_wait_read_all();
+#endif
+}
 constexpr uint32_t kStageBytes = STRAGGLAR_STAGE_BYTES;
 constexpr int kTmaSmem = 128 + kStages * kStageBytes;
 
@@ -235,7 +251,7 @@ static __device__ void tma_copy(Pipe& p, char* dst, const char* src, uint64_t nb
       mbar_expect_tx(&p.bar[s], len);
       bulk_load(p.buf(s), src + off, len, &p.bar[s]);
     };
-    for (uint32_t i = 0; i < np && i < (uint32_t)kStages; ++i) issue(i);
+    for (uint32_t i = 0; i < np && i < (uint32_t)kAhead; ++i) issue(i);
     uint32_t ph = p.phase;
     for (uint32_t i = 0; i < np; ++i) {
       const int s = i % kStages;
@@ -245,9 +261,9 @@ static __device__ void tma_copy(Pipe& p, char* dst, const char* src, uint64_t nb
       const uint32_t len = (uint32_t)((nbytes - off) < kStageBytes ? (nbytes - off) : kStageBytes);
       bulk_store(dst + off, p.buf(s), len);
       bulk_commit();
-      if (i + kStages < np) {
-        bulk_wait_read_all();
-        issue(i + kStages);
+      if (i + kAhead < np) {
+        ring_release_wait();
+        issue(i + kAhead);
       }
     }
     bulk_wait_all();
@@ -275,7 +291,7 @@ __device__ void tma_add2(Pipe& p, char* d0, char* d1, const char* a, const char*
   };
   if (threadIdx.x == 0 && np) {
     fence_proxy_async_global();
-    for (uint32_t i = 0; i < np && i < (uint32_t)kStages; ++i) issue(i);
+    for (uint32_t i = 0; i < np && i < (uint32_t)kAhead; ++i) issue(i);
   }
   uint32_t ph = p.phase;
   for (uint32_t i = 0; i < np; ++i) {
@@ -293,9 +309,9 @@ __device__ void tma_add2(Pipe& p, char* d0, char* d1, const char* a, const char*
       bulk_store(d0 + off, A, len);
       if (d1) bulk_store(d1 + off, A, len);
       bulk_commit();
-      if (i + kStages < np) {
-        bulk_wait_read_all();
-        issue(i + kStages);
+      if (i + kAhead < np) {
+        ring_release_wait();
+        issue(i + kAhead);
       }
     }
   }
@@ -327,7 +343,7 @@ __device__ void tma_reduce(Pipe& p, char* dst, const char* const (&src)[W - 1], 
   };
   if (threadIdx.x == 0 && np) {
     fence_proxy_async_global();
-    for (uint32_t i = 0; i < np && i < (uint32_t)kStages; ++i) issue(i);
+    for (uint32_t i = 0; i < np && i < (uint32_t)kAhead; ++i) issue(i);
   }
   uint32_t ph = p.phase;
   for (uint32_t i = 0; i < np; ++i) {
@@ -348,9 +364,9 @@ __device__ void tma_reduce(Pipe& p, char* dst, const char* const (&src)[W - 1], 
     if (threadIdx.x == 0) {
       bulk_store(dst + lo_b + (uint64_t)i * kPiece, base, len);
       bulk_commit();
-      if (i + kStages < np) {
-        bulk_wait_read_all();
-        issue(i + kStages);
+      if (i + kAhead < np) {
+        ring_release_wait();
+        issue(i + kAhead);
       }
     }
   }
@@ -381,7 +397,7 @@ __device__ void tma_add_bcast(Pipe& p, char* const* dst, const char* a, const ch
   };
   if (threadIdx.x == 0 && np) {
     fence_proxy_async_global();
-    for (uint32_t i = 0; i < np && i < (uint32_t)kStages; ++i) issue(i);
+    for (uint32_t i = 0; i < np && i < (uint32_t)kAhead; ++i) issue(i);
   }
   uint32_t ph = p.phase;
   for (uint32_t i = 0; i < np; ++i) {
@@ -399,9 +415,9 @@ __device__ void tma_add_bcast(Pipe& p, char* const* dst, const char* a, const ch
 #pragma unroll
       for (int d = 0; d < W; ++d) bulk_store(dst[d] + off, A, len);
       bulk_commit();
-      if (i + kStages < np) {
-        bulk_wait_read_all();
-        issue(i + kStages);
+      if (i + kAhead < np) {
+        ring_release_wait();
+        issue(i + kAhead);
       }
     }
   }

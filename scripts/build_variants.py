@@ -17,11 +17,18 @@ VARIANTS_ALL = {
     "s3_16k_t512": ["STRAGGLAR_STAGES=3", "STRAGGLAR_STAGE_BYTES=16384", "STRAGGLAR_THREADS=512", "STRAGGLAR_MIN_BLOCKS=2"],
     "s3_8k_t128": ["STRAGGLAR_STAGES=3", "STRAGGLAR_STAGE_BYTES=8192", "STRAGGLAR_THREADS=128", "STRAGGLAR_MIN_BLOCKS=8"],
 }
+VARIANTS_LAG = {
+    "lag0_s3": ["STRAGGLAR_TMA_LAG=0"],
+    "lag1_s3": ["STRAGGLAR_TMA_LAG=1"],
+    "lag1_s4_12k": ["STRAGGLAR_TMA_LAG=1", "STRAGGLAR_STAGES=4", "STRAGGLAR_STAGE_BYTES=12288"],
+    "lag1_s4_16k": ["STRAGGLAR_TMA_LAG=1", "STRAGGLAR_STAGES=4", "STRAGGLAR_STAGE_BYTES=16384"],
+    "lag1_s6_8k": ["STRAGGLAR_TMA_LAG=1", "STRAGGLAR_STAGES=6", "STRAGGLAR_STAGE_BYTES=8192"],
+}
 VARIANTS_LL = {
     "ll_gentle32": ["STRAGGLAR_LL_GENTLE=32"],
     "ll_gentle200": ["STRAGGLAR_LL_GENTLE=200"],
 }
-VARIANTS = VARIANTS_LL if "--ll" in sys.argv else VARIANTS_ALL
+VARIANTS = VARIANTS_LL if "--ll" in sys.argv else VARIANTS_LAG if "--lag" in sys.argv else VARIANTS_ALL
 os.makedirs(os.path.join(ROOT, "build", "variants"), exist_ok=True)
 with ThreadPoolExecutor(4) as ex:
     futs = {k: ex.submit(B.build, True, False, v, os.path.join(ROOT, "build", "variants", f"lib_{k}.so")) for k, v in VARIANTS.items()}
