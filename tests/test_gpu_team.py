@@ -365,3 +365,26 @@ def test_ll_protocol_vs_regular(S, dtype, n):
             os.environ.pop("STRAGGLAR_LL_MAX_CHUNK", None)
         else:
             os.environ["STRAGGLAR_LL_MAX_CHUNK"] = old
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_system_scope_flags(S, dtype):
+    """The per-process (NVLink) mode's memory-model scope — ld.acquire.sys /
+    fence.acq_rel.sys flags and relaxed.sys LL words — exercised in team mode
+    on every Phase-B path (schedule, direct completion, LL) and the Ring."""
+    old = {k: os.environ.get(k) for k in ("STRAGGLAR_SYS_SCOPE", "STRAGGLAR_LL_MAX_CHUNK")}
+    try:
+        os.environ["STRAGGLAR_SYS_SCOPE"] = "1"
+        for n, sigma in [(4, 2), (8, 0), (6, 5)]:
+            for count in [9999, 300001]:
+                for algo, ll in [("stragglar", "0"), ("stragglar", "262144"), ("direct", "0"), ("ring", "0")]:
+                    os.environ["STRAGGLAR_LL_MAX_CHUNK"] = ll
+                    xs, outs = run_team(S, n, sigma, dtype, count, config=80, algo=algo)
+                    want = N.ring_allreduce(xs, dtype) if algo == "ring" else N.stragglar_allreduce(xs, sigma, dtype)
+                    check_equal(outs, want, xs, dtype, f"sys n={n} {algo} ll={ll}")
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
