@@ -232,8 +232,12 @@ def bench_team(args):
     T_tot = t_start.elapsed_time(t_end) * 1e3 / args.steps
     T_A = statistics.mean(e[0].elapsed_time(e[1]) * 1e3 for e in steps)
     D_meas = statistics.mean(e[0].elapsed_time(e[2]) * 1e3 for e in steps)
-    T_post = statistics.mean(e[2].elapsed_time(e[3]) * 1e3 for e in steps)
-    T_post_sd = statistics.pstdev(e[2].elapsed_time(e[3]) * 1e3 for e in steps)
+    posts = [e[2].elapsed_time(e[3]) * 1e3 for e in steps]
+    T_post = statistics.mean(posts)
+    T_post_sd = statistics.pstdev(posts)
+    T_post_stats = {"mean": round(T_post, 2), "median": round(statistics.median(posts), 2), "min": round(min(posts), 2),
+                    "sem": round(statistics.stdev(posts) / len(posts) ** 0.5, 2) if len(posts) > 1 else None,
+                    "n": len(posts)}
 
     # NEXT row N1(ii): direct completion after the same Phase A and delay
     def direct_step(evs):
@@ -315,7 +319,7 @@ def bench_team(args):
             "l2": "inputs (8 x 256 MiB) exceed the 126 MB L2; buffers reduced in place step after step",
             "parallelism": "team8-on-1gpu",
         },
-        "T_post_us": round(T_post, 2), "T_post_sd_us": round(T_post_sd, 2),
+        "T_post_us": round(T_post, 2), "T_post_sd_us": round(T_post_sd, 2), "T_post_stats_us": T_post_stats,
         "T_total_us": round(T_tot, 2), "T_phaseA_us": round(T_A, 2), "D_meas_us": round(D_meas, 2),
         "algbw_GBps": round(S_bytes / (T_post * 1e-6) / 1e9, 1),
         "busbw_GBps": round(S_bytes / (T_post * 1e-6) / 1e9 * 2 * (world - 1) / world, 1),
