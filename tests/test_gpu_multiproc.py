@@ -59,3 +59,17 @@ def test_watchdog_reports_missing_peer():
     r = subprocess.run([sys.executable, os.path.join(HERE, "mp_timeout.py"), str(_port())],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("world,sigma,mode", [(2, 1, "schedule"), (4, 2, "schedule"), (4, 0, "direct")])
+def test_ddp_comm_hook(world, sigma, mode):
+    """data-parallel training with StragglAR as the
+    gradient AllReduce — DDP comm hook vs DDP's default hook, 3 steps."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    r = subprocess.run([sys.executable, os.path.join(HERE, "mp_ddp.py"), str(world), str(sigma), str(_port()), mode],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
