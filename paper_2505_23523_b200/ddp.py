@@ -14,7 +14,6 @@ allreduce hook the gradients are divided by the world size (before the sum,
 as DDP does).  The division is the only torch op in the hook; the reduction
 runs in the library's kernels.
 """
-from __future__ import annotations
 
 import torch
 import torch.distributed as dist
@@ -24,7 +23,7 @@ class StragglarHookState:
     def __init__(self, comm, use_direct: bool = False):
         self.comm = comm
         self.use_direct = use_direct
-        self._registered = []  # (data_ptr, nbytes) of peer-mapped bucket buffers
+        self._registered: list = []  # (data_ptr, nbytes) of peer-mapped bucket buffers
 
     def _ensure_registered(self, buf: torch.Tensor) -> None:
         p, nb = buf.data_ptr(), buf.numel() * buf.element_size()
