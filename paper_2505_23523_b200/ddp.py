@@ -34,7 +34,7 @@ class StragglarHookState:
         self._registered.append((p, nb))
 
 
-def stragglar_hook(state: StragglarHookState, bucket: dist.GradBucket) -> torch.futures.Future:
+def stragglar_hook(state: StragglarHookState, bucket: dist.GradBucket) -> torch.futures.Future[torch.Tensor]:
     buf = bucket.buffer()
     state._ensure_registered(buf)
     buf.div_(state.comm.world)
@@ -42,6 +42,6 @@ def stragglar_hook(state: StragglarHookState, bucket: dist.GradBucket) -> torch.
         state.comm.lib.stragglar_allreduce_direct(buf)
     else:
         state.comm.allreduce(buf)
-    fut: torch.futures.Future = torch.futures.Future()
+    fut: torch.futures.Future[torch.Tensor] = torch.futures.Future()
     fut.set_result(buf)
     return fut
