@@ -156,11 +156,17 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   c.flags_bytes = ((size_t)kSlots * G * sizeof(uint32_t) + 255) / 256 * 256;
   c.rank_bytes = c.flags_bytes + (size_t)(kMaxWorld - 1) * kLLChunkWords * sizeof(uint64_t);
   const size_t nbytes = team ? c.rank_bytes * world : c.rank_bytes;
-  CK(cudaMalloc(&c.flags, nbytes));
-  CK(cudaMemset(c.flags, 0, nbytes));
-  CK(cudaMalloc(&c.state, sizeof(DevState)));
-  CK(cudaMemset(c.state, 0, sizeof(DevState)));
-  CK(cudaDeviceSynchronize());
+  auto fail_free = [&]() {
+    if (c.flags) cudaFree(c.flags);
+    if (c.state) cudaFree(c.state);
+    c.flags = nullptr;
+    c.state = nullptr;
+    return STRAGGLAR_ERR_CUDA;
+  };
+  if (cudaMalloc(&c.flags, nbytes) != cudaSuccess || cudaMemset(c.flags, 0, nbytes) != cudaSuccess ||
+      cudaMalloc(&c.state, sizeof(DevState)) != cudaSuccess ||
+      cudaMemset(c.state, 0, sizeof(DevState)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    return fail_free();
   for (int p = 0; p < kMaxWorld; ++p) {
     c.peer_flags[p] = nullptr;
     c.peer_ll[p] = nullptr;
@@ -705,10 +711,21 @@ int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_
   piece = piece / v * v;
   if (piece == 0) piece = v;
   const uint64_t npieces = (count + piece - 1) / piece;
-  cudaStream_t h2d = nullptr, d2h = nullptr;
-  CK(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
-  std::vector<cudaEvent_t> ev(3 * npieces + 1, nullptr);
+  struct Res {                                      // released on every return path
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    std::vector<cudaEvent_t> ev;
+    ~Res() {
+      for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
+      if (h2d) cudaStreamDestroy(h2d);
+      if (d2h) cudaStreamDestroy(d2h);
+    }
+  } res;
+  CK(cudaStreamCreateWithFlags(&res.h2d, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&res.d2h, cudaStreamNonBlocking));
+  cudaStream_t h2d = res.h2d, d2h = res.d2h;
+  res.ev.assign(3 * npieces + 1, nullptr);
+  std::vector<cudaEvent_t>& ev = res.ev;
   for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaEventRecord(ev.back(), s));               // everything earlier on `stream` first
   CK(cudaStreamWaitEvent(h2d, ev.back(), 0));
@@ -732,9 +749,6 @@ int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_
   if (npieces) CK(cudaStreamWaitEvent(s, ev[3 * (npieces - 1) + 2], 0));
   CK(cudaStreamSynchronize(s));
   CK(cudaStreamSynchronize(d2h));
-  for (auto& e : ev) cudaEventDestroy(e);
-  cudaStreamDestroy(h2d);
-  cudaStreamDestroy(d2h);
   return st;
 }
 

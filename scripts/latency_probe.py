@@ -39,24 +39,20 @@ out["delay0_us"] = dev_time(lambda: S.stragglar_team_inject_delay(0))
 VARIANTS = [("tma", "0", "16384"), ("lsu", "0", "16384")]
 for mover, sysscope, slicebytes in VARIANTS:
     for n in [2, 4, 8]:
-        if True:
-            os.environ["STRAGGLAR_MOVER"] = mover
-            os.environ["STRAGGLAR_SYS_SCOPE"] = sysscope
-            os.environ["STRAGGLAR_SLICE_BYTES"] = slicebytes
-            S.stragglar_team_init(n, 0)
-            g = f"sys{sysscope}_sb{slicebytes}"
-            for count in [1024, 1 << 19, 1 << 22]:
-                bufs = [torch.randn(count, device="cuda").to(torch.bfloat16) for _ in range(n)]
-                ring = [b.clone() for b in bufs]
-                key = f"{mover}_n{n}_G{g}_c{count}"
-                out[key + "_A"] = dev_time(lambda: S.stragglar_team_reduce_scatter(bufs) or S.stragglar_team_complete(bufs)) \
-                    if False else None
-                out[key + "_AB"] = dev_time(lambda: (S.stragglar_team_reduce_scatter(bufs), S.stragglar_team_complete(bufs)))
-                out[key + "_fused"] = dev_time(lambda: S.stragglar_team_allreduce(bufs))
-                out[key + "_direct_fused"] = dev_time(lambda: S.stragglar_team_allreduce_direct(bufs))
-                out[key + "_ring"] = dev_time(lambda: S.stragglar_team_allreduce_ring(ring))
-                del out[key + "_A"]
-            assert S.stragglar_team_check_error() == 0
+        os.environ["STRAGGLAR_MOVER"] = mover
+        os.environ["STRAGGLAR_SYS_SCOPE"] = sysscope
+        os.environ["STRAGGLAR_SLICE_BYTES"] = slicebytes
+        S.stragglar_team_init(n, 0)
+        g = f"sys{sysscope}_sb{slicebytes}"
+        for count in [1024, 1 << 19, 1 << 22]:
+            bufs = [torch.randn(count, device="cuda").to(torch.bfloat16) for _ in range(n)]
+            ring = [b.clone() for b in bufs]
+            key = f"{mover}_n{n}_G{g}_c{count}"
+            out[key + "_AB"] = dev_time(lambda: (S.stragglar_team_reduce_scatter(bufs), S.stragglar_team_complete(bufs)))
+            out[key + "_fused"] = dev_time(lambda: S.stragglar_team_allreduce(bufs))
+            out[key + "_direct_fused"] = dev_time(lambda: S.stragglar_team_allreduce_direct(bufs))
+            out[key + "_ring"] = dev_time(lambda: S.stragglar_team_allreduce_ring(ring))
+        assert S.stragglar_team_check_error() == 0
 for k in ["STRAGGLAR_SYS_SCOPE", "STRAGGLAR_SLICE_BYTES", "STRAGGLAR_MOVER"]:
     os.environ.pop(k, None)
 print(json.dumps(out, indent=1))
