@@ -158,6 +158,13 @@ int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, in
  * and the whole direct-completion AllReduce. */
 int stragglar_team_complete_direct(void* const* bufs, size_t count, int dtype, int op, void* stream);
 int stragglar_team_allreduce_direct(void* const* bufs, size_t count, int dtype, int op, void* stream);
+/* Measurement only: the whole AllReduce in one launch (Phase A + B) with the
+ * straggler's CTAs arriving delay_ns after the launch, so the straggler's
+ * exchanges can overlap the non-stragglers' Phase A tail slice by slice, as
+ * across GPUs (the split reduce_scatter -> inject_delay -> complete sequence
+ * serialises them).  Used for the partial-overlap delay sweep. */
+int stragglar_team_allreduce_delayed(void* const* bufs, size_t count, int dtype, int op, uint64_t delay_ns,
+                                     void* stream);
 /* Bench only: spin until `ns` nanoseconds after the start of the most
  * recent team Phase A launch (the straggler's arrival time). */
 int stragglar_team_inject_delay(uint64_t ns, void* stream);

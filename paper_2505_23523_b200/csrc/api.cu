@@ -285,9 +285,10 @@ int team_rs(void* const* bufs, size_t count, int dtype, void* stream) {
   return launch(K_RS, dtype, P, k * P.G, stream);
 }
 
-int team_b(void* const* bufs, size_t count, int dtype, void* stream, int which = K_COMPLETE) {
+int team_b(void* const* bufs, size_t count, int dtype, void* stream, int which = K_COMPLETE, uint64_t delay_ns = 0) {
   Comm& c = g_team;
   LaunchPlan P = base_plan(c, count, dtype, true);
+  P.sigma_delay_ns = delay_ns;
   for (int p = 0; p < c.world; ++p) {
     P.buf[p] = (char*)bufs[p];
     P.local_rank[p] = p;
@@ -659,6 +660,15 @@ int stragglar_team_allreduce_direct(void* const* bufs, size_t count, int dtype, 
   if (st || count == 0) return st;
   if (g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;
   return team_b(bufs, count, dtype, stream, K_FUSED_DIRECT);
+}
+
+int stragglar_team_allreduce_delayed(void* const* bufs, size_t count, int dtype, int op, uint64_t delay_ns,
+                                     void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int st = team_check(bufs, count, dtype, op);
+  if (st || count == 0) return st;
+  if (g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;
+  return team_b(bufs, count, dtype, stream, K_FUSED, delay_ns);
 }
 
 int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, int op, void* stream) {

@@ -864,6 +864,16 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_con
   const int me = P.local_rank[li];
   const uint32_t ep = call_epoch(P);
   Pipe pipe = make_pipe(MV == MOVER_TMA);
+  if constexpr (KIND == 4 || KIND == 5) {
+    // measurement only (team mode): the straggler's CTAs arrive sigma_delay_ns
+    // after the launch (P:405-407 idle time, inside the kernel), so Phase B of
+    // each slice can overlap the non-stragglers' Phase A tail as on real GPUs
+    if (P.sigma_delay_ns && me == P.sigma && threadIdx.x == 0) {
+      const uint64_t until = globaltimer() + P.sigma_delay_ns;
+      while (globaltimer() < until) __nanosleep(500);
+    }
+    __syncthreads();
+  }
   if constexpr (KIND == 0 || KIND == 4 || KIND == 5)
     if (me != P.sigma) rs_body<DT, W, MV>(P, pipe, s, me, ep);
   if constexpr (KIND == 1 || KIND == 4) complete_body<DT, W, MV>(P, pipe, s, me, ep);

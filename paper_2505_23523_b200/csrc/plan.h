@@ -71,6 +71,7 @@ struct LaunchPlan {
   uint64_t* ll[kMaxWorld];   // LL area of each physical rank: [chunk][word] (payload | epoch << 32)
   int use_ll;                // Phase B through the LL areas (small chunks)
   int pad2;
+  uint64_t sigma_delay_ns;   // team measurement only: straggler CTAs start this late (KIND 4/5)
   int logical_of_phys[kMaxWorld];
   int nops[kMaxWorld];       // by physical rank
   Op ops[kMaxWorld][kMaxOps];// by physical rank

@@ -73,6 +73,7 @@ _SIGS = {
     "stragglar_team_complete_direct": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_team_allreduce_direct": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_team_inject_delay": ([_c_u64, _vp], _c_int),
+    "stragglar_team_allreduce_delayed": ([_PP, _c_size, _c_int, _c_int, _c_u64, _vp], _c_int),
     "stragglar_team_allreduce_host": ([_PP, _PP, _PP, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_team_slices": ([ctypes.POINTER(_c_int)], _c_int),
     "stragglar_team_check_error": ([ctypes.POINTER(_c_int)], _c_int),
@@ -292,6 +293,12 @@ def stragglar_team_complete_direct(bufs, stream=None) -> None:
 
 def stragglar_team_allreduce_direct(bufs, stream=None) -> None:
     _team_call("stragglar_team_allreduce_direct", bufs, stream)
+
+
+def stragglar_team_allreduce_delayed(bufs, delay_ns: int, stream=None) -> None:
+    arr, n, dt = _team_args(bufs)
+    _ck("stragglar_team_allreduce_delayed",
+        _lib.stragglar_team_allreduce_delayed(arr, n, dt, SUM, int(delay_ns), _stream_ptr(stream)))
 
 
 def stragglar_team_inject_delay(ns: int, stream=None) -> None:

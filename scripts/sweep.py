@@ -143,7 +143,17 @@ def delay_sweep(n, sigma, count, dtype, iters, warm):
             e[3].record()
         torch.cuda.synchronize()
         tot = statistics.median(e[0].elapsed_time(e[3]) * 1e3 for e in E)
+        # one launch, straggler CTAs delayed inside it: Phase B overlaps the Phase-A tail
+        F = [(ev(), ev()) for _ in range(iters)]
+        blocker()
+        for a, b in F:
+            a.record()
+            S.stragglar_team_allreduce_delayed(bufs, D)
+            b.record()
+        torch.cuda.synchronize()
+        fused = statistics.median(a.elapsed_time(b) * 1e3 for a, b in F)
         rows.append({"delay_frac_of_T_RS": f, "delay_us": round(D / 1e3, 2), "T_total_stragglar_us": round(tot, 2),
+                     "T_total_stragglar_overlapped_us": round(fused, 2),
                      "T_total_ring_us": round(D / 1e3 + T_ring, 2),
                      "stragglar_wins": tot < D / 1e3 + T_ring})
     crit_pred = max(T_RS - max(T_ring - T_SAR, 0.0), 0.0)

@@ -45,9 +45,11 @@ def main(path, out):
           f"critical delay by P:423-424 = {ds['critical_delay_predicted_us (P:423-424)']} us; "
           f"first measured winning delay = {ds['first_winning_delay_measured_us']} us.  In team mode every "
           "link is HBM, so StragglAR's total bytes (3n S) undercut the Ring's (5(n-1) S) even with no delay.", "",
-          "| delay / T_RS | delay us | StragglAR total us | Ring total us |", "|---|---|---|---|"]
+          "| delay / T_RS | delay us | StragglAR total us (A, delay, B serialised) | StragglAR total us (one launch, B overlaps A tail) | Ring total us |",
+          "|---|---|---|---|---|"]
     for r in ds["rows"]:
-        L.append(f"| {r['delay_frac_of_T_RS']} | {r['delay_us']} | {r['T_total_stragglar_us']} | {r['T_total_ring_us']} |")
+        L.append(f"| {r['delay_frac_of_T_RS']} | {r['delay_us']} | {r['T_total_stragglar_us']} | "
+                 f"{r.get('T_total_stragglar_overlapped_us', '')} | {r['T_total_ring_us']} |")
     if d.get("dp_buckets"):
         b = d["dp_buckets"]
         L += ["", "## Config 4: 16 back-to-back 25 MiB bf16 buckets, straggler delays bucket 0 only (n = 8)", "",

@@ -388,3 +388,17 @@ def test_system_scope_flags(S, dtype):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
+
+
+def test_delayed_single_launch(S):
+    """The measurement entry point with the straggler delayed inside the
+    kernel (Phase B overlapping the Phase-A tail) gives the same bits."""
+    n, sigma, dtype = 8, 4, "float32"
+    S.stragglar_team_init(n, sigma)
+    for count, d in [(123457, 0), (123457, 30_000), (2_000_003, 100_000)]:
+        xs = make_inputs(n, count, dtype, config=90)
+        bufs = [to_dev(x, dtype) for x in xs]
+        S.stragglar_team_allreduce_delayed(bufs, d)
+        torch.cuda.synchronize()
+        assert S.stragglar_team_check_error() == 0
+        check_equal([to_host(b, dtype) for b in bufs], N.stragglar_allreduce(xs, sigma, dtype), xs, dtype, f"d={d}")
