@@ -424,6 +424,12 @@ def bench_multi(args):
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
         dist.all_reduce(dly, op=dist.ReduceOp.MAX)
         results[name] = (tot.item(), dly.item(), launches, clk.summary())
+        if name == "stragglar":
+            # in-kernel stamps of the last call: Phase A on the non-stragglers, whole kernel per rank
+            ta, tk = S.stragglar_phase_times()
+            ph = torch.tensor([ta if rank != sigma else 0.0, tk], device="cpu" if shared else "cuda")
+            dist.all_reduce(ph, op=dist.ReduceOp.MAX)
+            phase_times = {"T_phaseA_us_max_NS": round(ph[0].item(), 2), "T_kernel_us_max": round(ph[1].item(), 2)}
     code, where = S.stragglar_check_error_where(False)
     if code:
         raise RuntimeError(f"device watchdog fired (where=0x{where:x})")
@@ -453,7 +459,7 @@ def bench_multi(args):
             "config": {"workload": f"{args.workload}: {desc}; one process per GPU, CUDA IPC over NVLink/NVSwitch",
                        "world": world, "straggler_rank": sigma, "count": count, "delay_us": D_ns / 1e3,
                        "parallelism": f"allreduce{world}"},
-            "T_total_us": round(T_tot, 2), "D_meas_us": round(D_meas, 2),
+            "T_total_us": round(T_tot, 2), "D_meas_us": round(D_meas, 2), "phase_times_in_kernel": phase_times,
             "algbw_GBps": round(S_bytes / (T_post * 1e-6) / 1e9, 1),
             "busbw_GBps": round(S_bytes / (T_post * 1e-6) / 1e9 * 2 * (world - 1) / world, 1),
             "ring_us": round(results["ring"][0] - results["ring"][1], 2),

@@ -140,6 +140,11 @@ int stragglar_check_error(int* code);
  * (straggler side), 0x4 copy, 0x5 completion, 0x6/0x7 ring, 0x8 barrier,
  * 0x9/0xA direct completion. */
 int stragglar_check_error_where(int team, int* code, uint32_t* where);
+/* Phase breakdown of this rank's last stragglar_allreduce(_direct) call, from
+ * %globaltimer stamps inside the kernel (this GPU's clock): *t_a_us = kernel
+ * start to the end of the rank's Phase A (the straggler has none: ~0),
+ * *t_total_us = kernel start to the end of its Phase B.  Synchronizes. */
+int stragglar_phase_times(double* t_a_us, double* t_total_us);
 int stragglar_finalize(void);
 
 /* ---- single-device team (all ranks on the current device) ---------------

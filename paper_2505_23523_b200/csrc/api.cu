@@ -297,6 +297,14 @@ int team_b(void* const* bufs, size_t count, int dtype, void* stream, int which =
   return launch(which, dtype, P, c.world * P.G, stream);
 }
 
+// Phase stamps of the next fused call: t_start = max (atomicMin target), the
+// two ends = 0 (atomicMax targets).  Stream-ordered, graph-capturable.
+int reset_stamps(Comm& c, void* stream) {
+  CK(cudaMemsetAsync(&c.state->t_start, 0xff, sizeof(uint64_t), (cudaStream_t)stream));
+  CK(cudaMemsetAsync(&c.state->t_a_done, 0, 2 * sizeof(uint64_t), (cudaStream_t)stream));
+  return STRAGGLAR_OK;
+}
+
 int read_error(Comm& c, int* code, uint32_t* where = nullptr) {
   if (!code) return STRAGGLAR_ERR_INVALID_ARG;
   if (!c.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
@@ -488,6 +496,7 @@ int stragglar_allreduce(void* buf, size_t count, int dtype, int op, void* stream
   if (st || count == 0) return st;
   LaunchPlan P;
   if ((st = proc_plan(buf, count, dtype, &P))) return st;
+  if ((st = reset_stamps(c, stream))) return st;
   // one persistent launch: non-stragglers run Phase A then Phase B, the
   // straggler Phase B only (its delay is whatever precedes it on its stream)
   return launch(K_FUSED, dtype, P, P.G, stream);
@@ -501,6 +510,7 @@ int stragglar_allreduce_direct(void* buf, size_t count, int dtype, int op, void*
   if (st || count == 0) return st;
   LaunchPlan P;
   if ((st = proc_plan(buf, count, dtype, &P))) return st;
+  if ((st = reset_stamps(c, stream))) return st;
   return launch(K_FUSED_DIRECT, dtype, P, P.G, stream);
 }
 
@@ -592,6 +602,19 @@ int stragglar_inject_delay(uint64_t ns, void* stream) {
 int stragglar_check_error(int* code) {
   std::lock_guard<std::mutex> lk(g_mu);
   return read_error(g_proc, code);
+}
+
+int stragglar_phase_times(double* t_a_us, double* t_total_us) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!t_a_us || !t_total_us) return STRAGGLAR_ERR_INVALID_ARG;
+  if (!g_proc.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  CK(cudaDeviceSynchronize());
+  DevState h;
+  CK(cudaMemcpy(&h, g_proc.state, sizeof(h), cudaMemcpyDeviceToHost));
+  if (h.t_start == ~0ull || h.t_b_done < h.t_start) return STRAGGLAR_ERR_INVALID_ARG;   // no fused call yet
+  *t_a_us = (h.t_a_done - h.t_start) * 1e-3;
+  *t_total_us = (h.t_b_done - h.t_start) * 1e-3;
+  return STRAGGLAR_OK;
 }
 
 int stragglar_check_error_where(int team, int* code, uint32_t* where) {

@@ -864,6 +864,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_con
   const int me = P.local_rank[li];
   const uint32_t ep = call_epoch(P);
   Pipe pipe = make_pipe(MV == MOVER_TMA);
+  const bool stamps = (KIND == 4 || KIND == 5) && P.nlocal == 1;   // per-process fused call
+  if (stamps && threadIdx.x == 0)   // (reset by the host in stream order before the launch)
+    atomicMin(reinterpret_cast<unsigned long long*>(&P.state->t_start), (unsigned long long)globaltimer());
   if constexpr (KIND == 4 || KIND == 5) {
     // measurement only (team mode): the straggler's CTAs arrive sigma_delay_ns
     // after the launch (P:405-407 idle time, inside the kernel), so Phase B of
@@ -876,8 +879,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_con
   }
   if constexpr (KIND == 0 || KIND == 4 || KIND == 5)
     if (me != P.sigma) rs_body<DT, W, MV>(P, pipe, s, me, ep);
+  if (stamps && threadIdx.x == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(&P.state->t_a_done), (unsigned long long)globaltimer());
   if constexpr (KIND == 1 || KIND == 4) complete_body<DT, W, MV>(P, pipe, s, me, ep);
   if constexpr (KIND == 3 || KIND == 5) direct_body<DT, W, MV>(P, pipe, s, me, ep);
+  if (stamps && threadIdx.x == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(&P.state->t_b_done), (unsigned long long)globaltimer());
   finish_call(P);
 }
 

@@ -41,7 +41,10 @@ struct DevState {
   uint64_t t_release;    // when the last injected delay released
   uint32_t epoch;        // calls completed; the running call uses epoch + 1
   uint32_t exit_count;   // CTAs that finished the call's last kernel (reset by the last one)
-  uint64_t pad[4];
+  uint64_t t_start;      // phase stamps of the last fused call (%globaltimer, this GPU):
+  uint64_t t_a_done;     //   min CTA start, max end of Phase A, max end of Phase B
+  uint64_t t_b_done;
+  uint64_t pad;
 };
 
 enum ErrCode : uint32_t { ERR_TIMEOUT = 1, ERR_BAD_PLAN = 2 };

@@ -61,6 +61,7 @@ _SIGS = {
     "stragglar_check_error": ([ctypes.POINTER(_c_int)], _c_int),
     "stragglar_finalize": ([], _c_int),
     "stragglar_check_error_where": ([_c_int, ctypes.POINTER(_c_int), ctypes.POINTER(ctypes.c_uint32)], _c_int),
+    "stragglar_phase_times": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _c_int),
     "stragglar_select": ([_c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                           ctypes.POINTER(_c_int), ctypes.POINTER(ctypes.c_double)], _c_int),
     "stragglar_set_cost_model": ([ctypes.c_double, ctypes.c_double], _c_int),
@@ -249,6 +250,13 @@ def stragglar_check_error_where(team: bool = False):
     if st not in (0, 6):
         _ck("stragglar_check_error_where", st)
     return code.value, where.value
+
+
+def stragglar_phase_times():
+    """-> (t_a_us, t_total_us) of this rank's last fused call (in-kernel stamps)."""
+    a, t = ctypes.c_double(0), ctypes.c_double(0)
+    _ck("stragglar_phase_times", _lib.stragglar_phase_times(ctypes.byref(a), ctypes.byref(t)))
+    return a.value, t.value
 
 
 def stragglar_finalize() -> None:

@@ -50,6 +50,8 @@ def worker(rank, world, sigma, count, dtype, port, q):
         if rank == sigma:
             S.stragglar_inject_delay(200_000)
         comm.allreduce(t)
+        ta, tk = S.stragglar_phase_times()          # in-kernel stamps of that call
+        assert 0.0 <= ta <= tk < 60e6, (ta, tk)
         comm.allreduce_ring(ring)
         # NEXT row N2: selection for an expected delay (0 and 10 ms)
         used = [S.stragglar_allreduce_auto(autos[0], 0), S.stragglar_allreduce_auto(autos[1], 10_000_000)]
