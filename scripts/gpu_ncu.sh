@@ -4,7 +4,7 @@ set -u
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 TAG=${TAG:-r01}
-if [ -z "$SKIP_LISTS" ]; then
+if [ -z "${SKIP_LISTS:-}" ]; then
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv \
     python scripts/profile_step.py > gpurun_out/${TAG}_launches.log 2>&1; echo "launches rc=$?"
 # (demangled names read "k_phase<(int)1, (int)8, (int)1, (int)1>")
