@@ -182,6 +182,13 @@ int stragglar_team_inject_delay(uint64_t ns, void* stream);
  * equal host_in. */
 int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_out, void* const* bufs,
                                   size_t count, int dtype, int op, void* stream);
+/* Tracing (team mode): when enabled, thread 0 of every Phase-B CTA records
+ * three %globaltimer stamps per op — wait began, data movement began, op
+ * signalled — at out[((rank * G + slice) * 16 + op) * 3 + {0,1,2}], G = the
+ * slices of the last call (written to *slices).  read_trace synchronizes the
+ * device; with out == NULL it only reports the sizes. */
+int stragglar_team_set_trace(int enable);
+int stragglar_team_read_trace(uint64_t* out, size_t max_entries, size_t* n_entries, int* slices);
 /* Slices per rank (CTAs per rank per launch) chosen at team_init. */
 int stragglar_team_slices(int* slices);
 int stragglar_team_check_error(int* code);

@@ -62,6 +62,8 @@ struct Comm {
   RankPrograms progs;
   uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
   int mover = MOVER_LSU;
+  uint64_t* trace = nullptr;            // Phase-B op trace (optional)
+  int last_G = 0;                       // slices of the last call (trace layout)
   double alpha_s = 3e-6;               // P:450 per-message latency used in the paper's model
   double beta_s_per_byte = 1.0 / 770e9; // measured B200 peer copy per direction (B200_PROFILING.md)
   std::vector<Registration> regs;
@@ -195,6 +197,7 @@ void common_finalize(Comm& c) {
   c.regs.clear();
   if (c.flags) cudaFree(c.flags);
   if (c.state) cudaFree(c.state);
+  if (c.trace) cudaFree(c.trace);
   c = Comm();
 }
 
@@ -226,6 +229,7 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
   P.G = slices_for(c, P.ce * P.esize);
   P.timeout_ns = c.timeout_ns;
   P.mover = c.mover;
+  P.trace = c.trace;
   {
     // LL Phase B for small chunks (latency-bound): STRAGGLAR_LL_MAX_CHUNK bytes, 0 disables
     const uint64_t chunk_bytes = P.ce * P.esize;
@@ -267,6 +271,7 @@ int team_check(void* const* bufs, size_t count, int dtype, int op) {
 }
 
 int launch(int which, int dtype, const LaunchPlan& P, int nblocks, void* stream) {
+  if (which == 1 || which == 4) (g_team.active && P.state == g_team.state ? g_team : g_proc).last_G = P.G;
   cudaError_t e = launch_plan_kernel(which, dtype, P, nblocks, (cudaStream_t)stream);
   if (e != cudaSuccess) return STRAGGLAR_ERR_CUDA;
   g_launches.fetch_add(1);
@@ -783,6 +788,36 @@ int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_
   CK(cudaStreamSynchronize(s));
   CK(cudaStreamSynchronize(d2h));
   return st;
+}
+
+int stragglar_team_set_trace(int enable) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_team;
+  if (!c.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (c.trace) {
+    cudaDeviceSynchronize();
+    cudaFree(c.trace);
+    c.trace = nullptr;
+  }
+  if (!enable) return STRAGGLAR_OK;
+  const size_t n = (size_t)c.world * c.G * kMaxOps * 3;
+  CK(cudaMalloc(&c.trace, n * sizeof(uint64_t)));
+  CK(cudaMemset(c.trace, 0, n * sizeof(uint64_t)));
+  return STRAGGLAR_OK;
+}
+
+int stragglar_team_read_trace(uint64_t* out, size_t max_entries, size_t* n_entries, int* slices) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_team;
+  if (!c.active || !c.trace) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (!n_entries || !slices) return STRAGGLAR_ERR_INVALID_ARG;
+  const size_t n = (size_t)c.world * c.last_G * kMaxOps * 3;
+  *n_entries = n;
+  *slices = c.last_G;
+  if (!out || max_entries < n) return STRAGGLAR_ERR_INVALID_ARG;
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(out, c.trace, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return STRAGGLAR_OK;
 }
 
 int stragglar_team_check_error(int* code) {

@@ -752,16 +752,20 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
     st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep, P.sys_scope);
   char* mine = P.buf[me];
   const int nops = P.nops[me];
+  // optional trace: per op, when the wait began, when data movement began, when it was signalled
+  uint64_t* tr = (P.trace && threadIdx.x == 0) ? P.trace + ((size_t)me * G + s) * kMaxOps * 3 : nullptr;
   for (int k = 0; k < nops; ++k) {
     const Op op = P.ops[me][k];
     const int c = op.chunk, peer = op.peer;
     const Range cr = chunk_range(P, c);
     const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
+    if (tr) tr[3 * k] = globaltimer();
     const uint64_t nvec_total = (sl.hi - sl.lo + V - 1) / V;
     const uint64_t mid = sl.lo + (nvec_total / 2) * V < sl.hi ? sl.lo + (nvec_total / 2) * V : sl.hi;
     if (op.kind == OP_EXCH_LOW) {
       // non-straggler r: [lo, mid) of c_r = partial_r (+) x_sigma, stored at both ends
       if (!cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, G, s), ep, P, 0x200 | k)) break;
+      if (tr) tr[3 * k + 1] = globaltimer();
       const uint64_t a = sl.lo * P.esize, b = mid * P.esize;
       if constexpr (tma)
         tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, (b - a) / 16 * 16);
@@ -774,6 +778,7 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
     } else if (op.kind == OP_EXCH_HIGH) {
       // straggler: [mid, hi) of c_r; waits for rank r's Phase-A partial
       if (!cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, G, s), ep, P, 0x300 | k)) break;
+      if (tr) tr[3 * k + 1] = globaltimer();
       const uint64_t a = mid * P.esize, b = sl.hi * P.esize;
       if constexpr (tma)
         tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, (b - a) / 16 * 16);
@@ -786,6 +791,7 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
     } else {
       // copy of a fully reduced chunk (push)
       if (!cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x400 | k)) break;
+      if (tr) tr[3 * k + 1] = globaltimer();
       const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
       if constexpr (tma)
         tma_copy(pipe, P.buf[peer] + a, mine + a, (b - a) / 16 * 16);
@@ -794,6 +800,7 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
       copy_tail(P.buf[peer] + a + (b - a) / 16 * 16, mine + a + (b - a) / 16 * 16, (int)((b - a) % 16));
       cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep, P.sys_scope);
     }
+    if (tr) tr[3 * k + 2] = globaltimer();
   }
   // postcondition: every chunk has landed here
   if (threadIdx.x == 0) {

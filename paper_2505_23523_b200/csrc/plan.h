@@ -75,6 +75,7 @@ struct LaunchPlan {
   int use_ll;                // Phase B through the LL areas (small chunks)
   int pad2;
   uint64_t sigma_delay_ns;   // team measurement only: straggler CTAs start this late (KIND 4/5)
+  uint64_t* trace;           // optional: [rank][slice][op][3] %globaltimer stamps (wait, data, done) of Phase B
   int logical_of_phys[kMaxWorld];
   int nops[kMaxWorld];       // by physical rank
   Op ops[kMaxWorld][kMaxOps];// by physical rank

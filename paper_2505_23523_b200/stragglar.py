@@ -77,6 +77,8 @@ _SIGS = {
     "stragglar_team_allreduce_delayed": ([_PP, _c_size, _c_int, _c_int, _c_u64, _vp], _c_int),
     "stragglar_team_allreduce_host": ([_PP, _PP, _PP, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_team_slices": ([ctypes.POINTER(_c_int)], _c_int),
+    "stragglar_team_set_trace": ([_c_int], _c_int),
+    "stragglar_team_read_trace": ([ctypes.POINTER(_c_u64), _c_size, ctypes.POINTER(_c_size), ctypes.POINTER(_c_int)], _c_int),
     "stragglar_team_check_error": ([ctypes.POINTER(_c_int)], _c_int),
     "stragglar_team_finalize": ([], _c_int),
 }
@@ -322,6 +324,21 @@ def stragglar_team_allreduce_host(host_in, host_out, bufs, stream=None) -> None:
     _ck("stragglar_team_allreduce_host",
         _lib.stragglar_team_allreduce_host(_ptr_array(host_in), _ptr_array(host_out), arr, n, dt, SUM,
                                            _stream_ptr(stream)))
+
+
+def stragglar_team_set_trace(enable: bool) -> None:
+    _ck("stragglar_team_set_trace", _lib.stragglar_team_set_trace(1 if enable else 0))
+
+
+def stragglar_team_read_trace():
+    """-> (list of uint64 stamps [rank][slice][op][wait, data, done], slices G)."""
+    n, g = _c_size(0), _c_int(0)
+    st = _lib.stragglar_team_read_trace(None, 0, ctypes.byref(n), ctypes.byref(g))
+    if st not in (0, 1):
+        _ck("stragglar_team_read_trace", st)
+    buf = (_c_u64 * n.value)()
+    _ck("stragglar_team_read_trace", _lib.stragglar_team_read_trace(buf, n.value, ctypes.byref(n), ctypes.byref(g)))
+    return list(buf), g.value
 
 
 def stragglar_team_check_error() -> int:

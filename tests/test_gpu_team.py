@@ -402,3 +402,28 @@ def test_delayed_single_launch(S):
         torch.cuda.synchronize()
         assert S.stragglar_team_check_error() == 0
         check_equal([to_host(b, dtype) for b in bufs], N.stragglar_allreduce(xs, sigma, dtype), xs, dtype, f"d={d}")
+
+
+def test_trace_stamps(S):
+    """Tracing: every Phase-B op of every rank and slice gets ordered stamps
+    (wait <= data <= done), and the result is still exact."""
+    n, sigma, dtype, count = 4, 1, "float32", 200003
+    xs = make_inputs(n, count, dtype, config=95)
+    bufs = [to_dev(x, dtype) for x in xs]
+    S.stragglar_team_init(n, sigma)
+    S.stragglar_team_set_trace(True)
+    S.stragglar_team_allreduce(bufs)
+    torch.cuda.synchronize()
+    tr, G = S.stragglar_team_read_trace()
+    S.stragglar_team_set_trace(False)
+    check_equal([to_host(b, dtype) for b in bufs], N.stragglar_allreduce(xs, sigma, dtype), xs, dtype, "trace")
+    nops = [4, 2, 2, 4]          # sends per logical rank at n = 4 (Appendix A of SURVEY, S:147/S:165-166)
+    seen = 0
+    for p in range(n):
+        logical = {1: 3, 3: 1}.get(p, p)     # straggler 1 <-> logical 3
+        for s in range(G):
+            for k in range(nops[logical]):
+                w, d, e = tr[((p * G + s) * 16 + k) * 3:((p * G + s) * 16 + k) * 3 + 3]
+                assert 0 < w <= d <= e, (p, s, k, w, d, e)
+                seen += 1
+    assert seen == G * sum(nops)
