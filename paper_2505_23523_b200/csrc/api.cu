@@ -749,44 +749,60 @@ int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_
   piece = piece / v * v;
   if (piece == 0) piece = v;
   const uint64_t npieces = (count + piece - 1) / piece;
+  // copy streams per direction (several copy engines; ranks alternate between them)
+  int ncs = (int)env_u64("STRAGGLAR_E2E_STREAMS", 2);
+  if (ncs < 1) ncs = 1;
+  if (ncs > world) ncs = world;
   struct Res {                                      // released on every return path
-    cudaStream_t h2d = nullptr, d2h = nullptr;
+    std::vector<cudaStream_t> h2d, d2h;
     std::vector<cudaEvent_t> ev;
     ~Res() {
       for (auto& e : ev)
         if (e) cudaEventDestroy(e);
-      if (h2d) cudaStreamDestroy(h2d);
-      if (d2h) cudaStreamDestroy(d2h);
+      for (auto x : h2d)
+        if (x) cudaStreamDestroy(x);
+      for (auto x : d2h)
+        if (x) cudaStreamDestroy(x);
     }
   } res;
-  CK(cudaStreamCreateWithFlags(&res.h2d, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&res.d2h, cudaStreamNonBlocking));
-  cudaStream_t h2d = res.h2d, d2h = res.d2h;
-  res.ev.assign(3 * npieces + 1, nullptr);
+  res.h2d.assign(ncs, nullptr);
+  res.d2h.assign(ncs, nullptr);
+  for (int i = 0; i < ncs; ++i) {
+    CK(cudaStreamCreateWithFlags(&res.h2d[i], cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&res.d2h[i], cudaStreamNonBlocking));
+  }
+  // events: per piece, one after each H2D stream, one after the AllReduce, one after each D2H stream
+  const size_t per = 2 * ncs + 1;
+  res.ev.assign(per * npieces + 1, nullptr);
   std::vector<cudaEvent_t>& ev = res.ev;
   for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   CK(cudaEventRecord(ev.back(), s));               // everything earlier on `stream` first
-  CK(cudaStreamWaitEvent(h2d, ev.back(), 0));
+  for (int i = 0; i < ncs; ++i) CK(cudaStreamWaitEvent(res.h2d[i], ev.back(), 0));
   std::vector<void*> sub(world);
   st = STRAGGLAR_OK;
   for (uint64_t k = 0; k < npieces && st == STRAGGLAR_OK; ++k) {
     const uint64_t off = k * piece, n = (count - off) < piece ? (count - off) : piece;
     const size_t boff = off * es, bytes = n * es;
+    cudaEvent_t* e = &ev[per * k];
     for (int p = 0; p < world; ++p)
-      CK(cudaMemcpyAsync((char*)bufs[p] + boff, (const char*)host_in[p] + boff, bytes, cudaMemcpyHostToDevice, h2d));
-    CK(cudaEventRecord(ev[3 * k], h2d));
-    CK(cudaStreamWaitEvent(s, ev[3 * k], 0));
+      CK(cudaMemcpyAsync((char*)bufs[p] + boff, (const char*)host_in[p] + boff, bytes, cudaMemcpyHostToDevice,
+                         res.h2d[p % ncs]));
+    for (int i = 0; i < ncs; ++i) {
+      CK(cudaEventRecord(e[i], res.h2d[i]));
+      CK(cudaStreamWaitEvent(s, e[i], 0));
+    }
     for (int p = 0; p < world; ++p) sub[p] = (char*)bufs[p] + boff;
     st = stragglar_team_allreduce(sub.data(), n, dtype, op, stream);
-    CK(cudaEventRecord(ev[3 * k + 1], s));
-    CK(cudaStreamWaitEvent(d2h, ev[3 * k + 1], 0));
+    CK(cudaEventRecord(e[ncs], s));
+    for (int i = 0; i < ncs; ++i) CK(cudaStreamWaitEvent(res.d2h[i], e[ncs], 0));
     for (int p = 0; p < world; ++p)
-      CK(cudaMemcpyAsync((char*)host_out[p] + boff, (char*)bufs[p] + boff, bytes, cudaMemcpyDeviceToHost, d2h));
-    CK(cudaEventRecord(ev[3 * k + 2], d2h));
+      CK(cudaMemcpyAsync((char*)host_out[p] + boff, (char*)bufs[p] + boff, bytes, cudaMemcpyDeviceToHost,
+                         res.d2h[p % ncs]));
+    for (int i = 0; i < ncs; ++i) CK(cudaEventRecord(e[ncs + 1 + i], res.d2h[i]));
   }
-  if (npieces) CK(cudaStreamWaitEvent(s, ev[3 * (npieces - 1) + 2], 0));
+  if (npieces)
+    for (int i = 0; i < ncs; ++i) CK(cudaStreamWaitEvent(s, ev[per * (npieces - 1) + ncs + 1 + i], 0));
   CK(cudaStreamSynchronize(s));
-  CK(cudaStreamSynchronize(d2h));
   return st;
 }
 
