@@ -750,7 +750,7 @@ int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_
   if (piece == 0) piece = v;
   const uint64_t npieces = (count + piece - 1) / piece;
   // copy streams per direction (several copy engines; ranks alternate between them)
-  int ncs = (int)env_u64("STRAGGLAR_E2E_STREAMS", 2);
+  int ncs = (int)env_u64("STRAGGLAR_E2E_STREAMS", 1);   // 1 measured best: 48 ms vs 63-72 ms with 2-8
   if (ncs < 1) ncs = 1;
   if (ncs > world) ncs = world;
   struct Res {                                      // released on every return path
