@@ -216,12 +216,14 @@ int stragglar_set_cost_model(double alpha_s, double beta_s_per_byte);
 int stragglar_allreduce_auto(void* buf, size_t count, int dtype, int op, void* stream, uint64_t expected_delay_ns,
                              int* used_stragglar);
 
-/* Environment knobs (read per call unless noted): STRAGGLAR_MOVER=tma|lsu
- * (at init; data mover), STRAGGLAR_SLICE_BYTES (target bytes per slice, 16384),
- * STRAGGLAR_SLICES (per-process slice cap, at init), STRAGGLAR_TIMEOUT_MS
- * (watchdog, at init), STRAGGLAR_LL_MAX_CHUNK (chunks up to this many bytes
- * use the low-latency word protocol in Phase B; 0 = off, the default —
- * measured slower than the flag protocol on one B200), STRAGGLAR_E2E_PIECE_BYTES. */
+/* Environment knobs, read once by stragglar_init / stragglar_team_init:
+ * STRAGGLAR_MOVER=tma|lsu (data mover), STRAGGLAR_SLICE_BYTES (target bytes
+ * per slice, 16384), STRAGGLAR_SLICES (per-process slice cap, 2 x SMs),
+ * STRAGGLAR_TIMEOUT_MS (watchdog, 10000), STRAGGLAR_LL_MAX_CHUNK (chunks up
+ * to this many bytes use the low-latency word protocol in Phase B; 0 = off,
+ * the default — measured slower than the flag protocol on one B200),
+ * STRAGGLAR_SYS_SCOPE (team mode: system-scope flags, 0), and for the host
+ * entry point STRAGGLAR_E2E_PIECE_BYTES (8 MiB) / STRAGGLAR_E2E_STREAMS (1). */
 
 /* Number of kernel launches the library enqueued since load (bench evidence). */
 int stragglar_launch_count(uint64_t* launches);

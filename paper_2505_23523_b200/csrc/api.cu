@@ -63,6 +63,12 @@ struct Comm {
   uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
   int mover = MOVER_LSU;
   uint64_t* trace = nullptr;            // Phase-B op trace (optional)
+  // tuning knobs, read from the environment once at init (include/stragglar.h)
+  uint64_t slice_bytes = 16384;         // STRAGGLAR_SLICE_BYTES
+  uint64_t ll_max_chunk = 0;            // STRAGGLAR_LL_MAX_CHUNK (0: LL off)
+  int sys_scope = 1;                    // STRAGGLAR_SYS_SCOPE (team mode only; default 0 there)
+  uint64_t e2e_piece_bytes = 8ull << 20;// STRAGGLAR_E2E_PIECE_BYTES (8 MiB measured best)
+  int e2e_streams = 1;                  // STRAGGLAR_E2E_STREAMS (1 measured best)
   int last_G = 0;                       // slices of the last call (trace layout)
   double alpha_s = 3e-6;               // P:450 per-message latency used in the paper's model
   double beta_s_per_byte = 1.0 / 770e9; // measured B200 peer copy per direction (B200_PROFILING.md)
@@ -155,6 +161,12 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   c.team = team;
   c.rs_pending = false;
   c.timeout_ns = env_u64("STRAGGLAR_TIMEOUT_MS", 10000) * 1000000ull;
+  c.slice_bytes = env_u64("STRAGGLAR_SLICE_BYTES", 16384);
+  c.ll_max_chunk = env_u64("STRAGGLAR_LL_MAX_CHUNK", 0);       // off by default: slower on one GPU
+  if (c.ll_max_chunk > kLLChunkBytes) c.ll_max_chunk = kLLChunkBytes;
+  c.sys_scope = team ? (int)env_u64("STRAGGLAR_SYS_SCOPE", 0) : 1;
+  c.e2e_piece_bytes = env_u64("STRAGGLAR_E2E_PIECE_BYTES", 8ull << 20);
+  c.e2e_streams = (int)env_u64("STRAGGLAR_E2E_STREAMS", 1);
   c.flags_bytes = ((size_t)kSlots * G * sizeof(uint32_t) + 255) / 256 * 256;
   c.rank_bytes = c.flags_bytes + (size_t)(kMaxWorld - 1) * kLLChunkWords * sizeof(uint64_t);
   const size_t nbytes = team ? c.rank_bytes * world : c.rank_bytes;
@@ -206,7 +218,7 @@ void common_finalize(Comm& c) {
 // large ones all of them.  Any G is safe call to call: flags hold monotone
 // epochs, so values left at other positions by earlier calls are stale (< epoch).
 int slices_for(const Comm& c, uint64_t chunk_bytes) {
-  const uint64_t per = env_u64("STRAGGLAR_SLICE_BYTES", 16384);
+  const uint64_t per = c.slice_bytes;
   uint64_t g = per ? (chunk_bytes + per - 1) / per : (uint64_t)c.G;
   if (g < 1) g = 1;
   if (g > (uint64_t)c.G) g = c.G;
@@ -233,11 +245,9 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
   {
     // LL Phase B for small chunks (latency-bound): STRAGGLAR_LL_MAX_CHUNK bytes, 0 disables
     const uint64_t chunk_bytes = P.ce * P.esize;
-    uint64_t lim = env_u64("STRAGGLAR_LL_MAX_CHUNK", 0);   // off by default: slower on one GPU
-    if (lim > kLLChunkBytes) lim = kLLChunkBytes;
-    P.use_ll = (chunk_bytes > 0 && chunk_bytes <= lim) ? 1 : 0;
+    P.use_ll = (chunk_bytes > 0 && chunk_bytes <= c.ll_max_chunk) ? 1 : 0;
   }
-  P.sys_scope = c.team ? (int)env_u64("STRAGGLAR_SYS_SCOPE", 0) : 1;
+  P.sys_scope = c.sys_scope;
   P.state = c.state;
   for (int p = 0; p < c.world; ++p) {
     P.flags[p] = c.peer_flags[p];
@@ -745,12 +755,12 @@ int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_
   // AllReduce of piece k (SMs) and D2H of piece k-1 (copy engine, the other
   // direction) overlap.  Pieces keep 16-byte alignment.
   const uint64_t v = 16 / es;
-  uint64_t piece = env_u64("STRAGGLAR_E2E_PIECE_BYTES", 8ull << 20) / es;   // 8 MiB: measured best (profiles/r01)
+  uint64_t piece = g_team.e2e_piece_bytes / es;
   piece = piece / v * v;
   if (piece == 0) piece = v;
   const uint64_t npieces = (count + piece - 1) / piece;
   // copy streams per direction (several copy engines; ranks alternate between them)
-  int ncs = (int)env_u64("STRAGGLAR_E2E_STREAMS", 1);   // 1 measured best: 48 ms vs 63-72 ms with 2-8
+  int ncs = g_team.e2e_streams;
   if (ncs < 1) ncs = 1;
   if (ncs > world) ncs = world;
   struct Res {                                      // released on every return path

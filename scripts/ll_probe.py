@@ -28,11 +28,11 @@ def dev_time(fn, iters=20):
 
 out = {}
 for n in (2, 8):
-    S.stragglar_team_init(n, 0)
     for count in (1024, 16384, 131072, 458752):
         bufs = [torch.randn(count, device="cuda").to(torch.bfloat16) for _ in range(n)]
         for ll in ("0", "262144"):
             os.environ["STRAGGLAR_LL_MAX_CHUNK"] = ll
+            S.stragglar_team_init(n, 0)                # knobs are read at init
             out[f"n{n}_c{count}_ll{ll}_fused"] = dev_time(lambda: S.stragglar_team_allreduce(bufs))
             out[f"n{n}_c{count}_ll{ll}_B"] = dev_time(lambda: (S.stragglar_team_reduce_scatter(bufs),
                                                                S.stragglar_team_complete(bufs)))

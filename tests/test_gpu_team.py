@@ -188,11 +188,11 @@ def test_host_entry_point(S, piece_bytes):
     host = [torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory() for x in xs]
     out = [torch.empty_like(h).pin_memory() for h in host]
     dev = [torch.empty(count, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
-    S.stragglar_team_init(n, sigma)
     old = os.environ.pop("STRAGGLAR_E2E_PIECE_BYTES", None)
     if piece_bytes:
         os.environ["STRAGGLAR_E2E_PIECE_BYTES"] = piece_bytes
     try:
+        S.stragglar_team_init(n, sigma)          # knobs are read at init
         S.stragglar_team_allreduce_host(host, out, dev)
     finally:
         os.environ.pop("STRAGGLAR_E2E_PIECE_BYTES", None)
