@@ -95,7 +95,7 @@ int esize_of(int dtype) {
   }
 }
 
-bool pow2_world(int w) { return w == 2 || w == 4 || w == 6 || w == 8; }  // 6: Appendix B schedule
+bool supported_world(int w) { return w == 2 || w == 4 || w == 6 || w == 8; }  // 6: Appendix B schedule
 
 uint64_t chunk_elems(uint64_t count, int parts, int esize) {
   const uint64_t v = 16 / esize;
@@ -127,7 +127,7 @@ int resident_ctas(int world, int mover, int* sm_count) {
 }
 
 int common_init(Comm& c, int world, int rank, int sigma, bool team) {
-  if (!pow2_world(world)) return STRAGGLAR_ERR_UNSUPPORTED;
+  if (!supported_world(world)) return STRAGGLAR_ERR_UNSUPPORTED;
   if (sigma < 0 || sigma >= world) return STRAGGLAR_ERR_INVALID_ARG;
   if (!team && (rank < 0 || rank >= world)) return STRAGGLAR_ERR_INVALID_ARG;
   try {
