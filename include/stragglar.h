@@ -183,13 +183,15 @@ int stragglar_team_inject_delay(uint64_t ns, void* stream);
 int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_out, void* const* bufs,
                                   size_t count, int dtype, int op, void* stream);
 /* Tracing (team mode): when enabled, thread 0 of every Phase-B CTA records
- * three %globaltimer stamps per op — wait began, data movement began, op
- * signalled — at out[((rank * G + slice) * 16 + op) * 3 + {0,1,2}], G = the
- * slices of the last call (written to *slices).  read_trace synchronizes the
+ * three %globaltimer stamps per op and slice — wait began, data movement
+ * began, op signalled — at out[((rank * NS + slice) * 16 + op) * 3 + {0,1,2}],
+ * NS = slices per chunk of the last call (CTAs per rank x slices per CTA,
+ * written to *slices).  read_trace synchronizes the
  * device; with out == NULL it only reports the sizes. */
 int stragglar_team_set_trace(int enable);
 int stragglar_team_read_trace(uint64_t* out, size_t max_entries, size_t* n_entries, int* slices);
-/* Slices per rank (CTAs per rank per launch) chosen at team_init. */
+/* CTAs per rank per launch chosen at team_init (each covers 1..16 slices of
+ * every chunk, by message size: STRAGGLAR_SUBSLICE_BYTES). */
 int stragglar_team_slices(int* slices);
 int stragglar_team_check_error(int* code);
 int stragglar_team_finalize(void);
@@ -218,7 +220,11 @@ int stragglar_allreduce_auto(void* buf, size_t count, int dtype, int op, void* s
 
 /* Environment knobs, read once by stragglar_init / stragglar_team_init:
  * STRAGGLAR_MOVER=tma|lsu (data mover), STRAGGLAR_SLICE_BYTES (target bytes
- * per slice, 16384), STRAGGLAR_SLICES (per-process slice cap, 2 x SMs),
+ * per slice, 16384), STRAGGLAR_SLICES (per-process CTA cap, 2 x SMs),
+ * STRAGGLAR_SUBSLICES (slices per CTA at most, 1..16) and
+ * STRAGGLAR_SUBSLICE_BYTES (their target size on large messages, 131072: each
+ * hop hands over ~128 KB pieces, so a forwarded slice is still in L2 when
+ * the next hop reads it),
  * STRAGGLAR_TIMEOUT_MS (watchdog, 10000), STRAGGLAR_LL_MAX_CHUNK (chunks up
  * to this many bytes use the low-latency word protocol in Phase B; 0 = off,
  * the default — measured slower than the flag protocol on one B200),

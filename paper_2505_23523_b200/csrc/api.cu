@@ -50,7 +50,9 @@ struct Comm {
   bool active = false;
   bool team = false;
   int world = 0, rank = -1, sigma = -1, device = -1;
-  int G = 0;
+  int G = 0;                   // CTAs per rank (the launch's co-residency budget)
+  int sub = 1;                 // slices per CTA at most (STRAGGLAR_SUBSLICES)
+  uint64_t sub_bytes = 0;      // target slice size on large messages (STRAGGLAR_SUBSLICE_BYTES)
   bool rs_pending = false;     // team: a Phase A awaits its Phase B (same call epoch)
   uint32_t* flags = nullptr;   // own flag array(s) + LL area(s); team: world of them back to back
   uint32_t* peer_flags[kMaxWorld] = {nullptr};
@@ -69,7 +71,7 @@ struct Comm {
   int sys_scope = 1;                    // STRAGGLAR_SYS_SCOPE (team mode only; default 0 there)
   uint64_t e2e_piece_bytes = 8ull << 20;// STRAGGLAR_E2E_PIECE_BYTES (8 MiB measured best)
   int e2e_streams = 1;                  // STRAGGLAR_E2E_STREAMS (1 measured best)
-  int last_G = 0;                       // slices of the last call (trace layout)
+  int last_slices = 0;                  // slices per chunk of the last Phase-B call (trace layout)
   double alpha_s = 3e-6;               // P:450 per-message latency used in the paper's model
   double beta_s_per_byte = 1.0 / 770e9; // measured B200 peer copy per direction (B200_PROFILING.md)
   std::vector<Registration> regs;
@@ -162,12 +164,16 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   c.rs_pending = false;
   c.timeout_ns = env_u64("STRAGGLAR_TIMEOUT_MS", 10000) * 1000000ull;
   c.slice_bytes = env_u64("STRAGGLAR_SLICE_BYTES", 16384);
+  c.sub = (int)env_u64("STRAGGLAR_SUBSLICES", kMaxSub);
+  c.sub_bytes = env_u64("STRAGGLAR_SUBSLICE_BYTES", 128 * 1024);
+  if (c.sub < 1) c.sub = 1;
+  if (c.sub > kMaxSub) c.sub = kMaxSub;
   c.ll_max_chunk = env_u64("STRAGGLAR_LL_MAX_CHUNK", 0);       // off by default: slower on one GPU
   if (c.ll_max_chunk > kLLChunkBytes) c.ll_max_chunk = kLLChunkBytes;
   c.sys_scope = team ? (int)env_u64("STRAGGLAR_SYS_SCOPE", 0) : 1;
   c.e2e_piece_bytes = env_u64("STRAGGLAR_E2E_PIECE_BYTES", 8ull << 20);
   c.e2e_streams = (int)env_u64("STRAGGLAR_E2E_STREAMS", 1);
-  c.flags_bytes = ((size_t)kSlots * G * sizeof(uint32_t) + 255) / 256 * 256;
+  c.flags_bytes = ((size_t)kSlots * G * kMaxSub * sizeof(uint32_t) + 255) / 256 * 256;
   c.rank_bytes = c.flags_bytes + (size_t)(kMaxWorld - 1) * kLLChunkWords * sizeof(uint64_t);
   const size_t nbytes = team ? c.rank_bytes * world : c.rank_bytes;
   auto fail_free = [&]() {
@@ -213,16 +219,28 @@ void common_finalize(Comm& c) {
   c = Comm();
 }
 
-// Slices per call: about one slice per kSliceBytes of a chunk, at most the
-// communicator's G.  Small messages use few CTAs (less flag traffic per round),
-// large ones all of them.  Any G is safe call to call: flags hold monotone
-// epochs, so values left at other positions by earlier calls are stale (< epoch).
-int slices_for(const Comm& c, uint64_t chunk_bytes) {
+// Slices per call: about one slice per slice_bytes of a chunk.  Small messages
+// use few CTAs (less flag traffic per round); large ones all G CTAs, each
+// covering up to `sub` slices.  Any (G, sub) is safe call to call: flags hold
+// monotone epochs, so values left at other positions by earlier calls are
+// stale (< epoch); within a call every kernel uses the same layout.
+void slices_for(const Comm& c, uint64_t chunk_bytes, int* G, int* sub) {
   const uint64_t per = c.slice_bytes;
-  uint64_t g = per ? (chunk_bytes + per - 1) / per : (uint64_t)c.G;
+  uint64_t g = per ? (chunk_bytes + per - 1) / per : (uint64_t)c.G * c.sub;
   if (g < 1) g = 1;
-  if (g > (uint64_t)c.G) g = c.G;
-  return (int)g;
+  if (g <= (uint64_t)c.G) {
+    *G = (int)g;
+    *sub = 1;
+    return;
+  }
+  // large messages: each CTA covers ~chunk/(G*sub_bytes) slices of about
+  // sub_bytes (rounded; 1 if sub_bytes is 0)
+  const uint64_t unit = (uint64_t)c.G * c.sub_bytes;
+  uint64_t m = unit ? (chunk_bytes + unit / 2) / unit : 1;
+  if (m < 1) m = 1;
+  if (m > (uint64_t)c.sub) m = c.sub;
+  *G = c.G;
+  *sub = (int)m;
 }
 
 // The call's epoch is not a launch parameter: kernels read state->epoch + 1 and
@@ -238,7 +256,7 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
   P.esize = esize_of(dtype);
   P.ce = chunk_elems(count, c.world - 1, P.esize);
   P.nchunks = c.world - 1;
-  P.G = slices_for(c, P.ce * P.esize);
+  slices_for(c, P.ce * P.esize, &P.G, &P.sub);
   P.timeout_ns = c.timeout_ns;
   P.mover = c.mover;
   P.trace = c.trace;
@@ -246,6 +264,7 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
     // LL Phase B for small chunks (latency-bound): STRAGGLAR_LL_MAX_CHUNK bytes, 0 disables
     const uint64_t chunk_bytes = P.ce * P.esize;
     P.use_ll = (chunk_bytes > 0 && chunk_bytes <= c.ll_max_chunk) ? 1 : 0;
+    if (P.use_ll) P.sub = 1;   // the LL area is laid out per CTA slice
   }
   P.sys_scope = c.sys_scope;
   P.state = c.state;
@@ -281,7 +300,7 @@ int team_check(void* const* bufs, size_t count, int dtype, int op) {
 }
 
 int launch(int which, int dtype, const LaunchPlan& P, int nblocks, void* stream) {
-  if (which == 1 || which == 4) (g_team.active && P.state == g_team.state ? g_team : g_proc).last_G = P.G;
+  if (which == 1 || which == 4) (g_team.active && P.state == g_team.state ? g_team : g_proc).last_slices = P.G * P.sub;
   cudaError_t e = launch_plan_kernel(which, dtype, P, nblocks, (cudaStream_t)stream);
   if (e != cudaSuccess) return STRAGGLAR_ERR_CUDA;
   g_launches.fetch_add(1);
@@ -539,7 +558,8 @@ int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* s
   if ((st = proc_plan(buf, count, dtype, &P))) return st;
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
-  P.G = slices_for(c, P.ce * P.esize);
+  slices_for(c, P.ce * P.esize, &P.G, &P.sub);
+  P.sub = 1;   // the ring kernel runs one slice per CTA
   return launch(K_RING, dtype, P, P.G, stream);
 }
 
@@ -718,7 +738,8 @@ int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, in
   LaunchPlan P = base_plan(c, count, dtype, true);
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
-  P.G = slices_for(c, P.ce * P.esize);
+  slices_for(c, P.ce * P.esize, &P.G, &P.sub);
+  P.sub = 1;   // the ring kernel runs one slice per CTA
   for (int p = 0; p < c.world; ++p) {
     P.buf[p] = (char*)bufs[p];
     P.local_rank[p] = p;
@@ -826,7 +847,7 @@ int stragglar_team_set_trace(int enable) {
     c.trace = nullptr;
   }
   if (!enable) return STRAGGLAR_OK;
-  const size_t n = (size_t)c.world * c.G * kMaxOps * 3;
+  const size_t n = (size_t)c.world * c.G * kMaxSub * kMaxOps * 3;
   CK(cudaMalloc(&c.trace, n * sizeof(uint64_t)));
   CK(cudaMemset(c.trace, 0, n * sizeof(uint64_t)));
   return STRAGGLAR_OK;
@@ -837,9 +858,9 @@ int stragglar_team_read_trace(uint64_t* out, size_t max_entries, size_t* n_entri
   Comm& c = g_team;
   if (!c.active || !c.trace) return STRAGGLAR_ERR_NOT_INITIALIZED;
   if (!n_entries || !slices) return STRAGGLAR_ERR_INVALID_ARG;
-  const size_t n = (size_t)c.world * c.last_G * kMaxOps * 3;
+  const size_t n = (size_t)c.world * c.last_slices * kMaxOps * 3;
   *n_entries = n;
-  *slices = c.last_G;
+  *slices = c.last_slices;
   if (!out || max_entries < n) return STRAGGLAR_ERR_INVALID_ARG;
   CK(cudaDeviceSynchronize());
   CK(cudaMemcpy(out, c.trace, n * sizeof(uint64_t), cudaMemcpyDeviceToHost));

@@ -507,43 +507,43 @@ __device__ void rs_slice(const LaunchPlan& P, const char* const (&src)[W - 1], c
   }
 }
 
-// Phase A body for non-straggler `me`, slice s.
+// Phase A body for non-straggler `me`, CTA slot s (slices s*sub .. s*sub+sub-1).
 template <int DT, int W, int MV>
 __device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
-  const int G = P.G;
+  const int NV = P.G * P.sub;   // slices per chunk (flag stride)
   if (blockIdx.x == 0 && threadIdx.x == 0) P.state->t_rs_start = globaltimer();
-  // barrier (1) among the non-stragglers, per slice
+  // barrier (1) among the non-stragglers, per CTA slot
   if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
-    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep, P.sys_scope);
-  if (threadIdx.x == 0) {
-    bool ok = true;
-    for (int p = 0; p < W && ok; ++p)
-      if (p != me && p != P.sigma)
-        ok = spin_wait(flag_at(P.flags[me], SLOT_ARRIVE + p, G, s), ep, P, 0x100 | p);
-    (void)ok;
-  }
-  if (!__syncthreads_and(*(volatile uint32_t*)&P.state->err == 0)) return;
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, NV, s), ep, P.sys_scope);
+  // one waiting thread per peer: the acquire loads overlap instead of queueing
+  int ok = 1;
+  if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
+    ok = spin_wait(flag_at(P.flags[me], SLOT_ARRIVE + threadIdx.x, NV, s), ep, P, 0x100 | threadIdx.x);
+  if (!__syncthreads_and(ok)) return;
 
   const int g = P.logical_of_phys[me];  // owned chunk
   const Range c = chunk_range(P, g);
-  const Range r = slice_of(c.lo, c.hi, s, G, 16 / P.esize);
   // non-stragglers in ascending physical order (compile-time indices, no local memory)
   const char* src[W - 1];
 #pragma unroll
   for (int j = 0; j < W - 1; ++j) src[j] = P.buf[j < P.sigma ? j : j + 1];
-  // with two ranks the owner's chunk already is the non-straggler "sum"
-  if constexpr (W > 2) {
-    if constexpr (MV == MOVER_TMA) {
-      const uint64_t lo_b = r.lo * P.esize, hi_b = r.hi * P.esize;
-      const uint64_t body = (hi_b - lo_b) / 16 * 16;
-      tma_reduce<DT, W>(pipe, P.buf[me], src, lo_b, body);
-      rs_slice<DT, W>(P, src, P.buf[me], lo_b + body, hi_b);   // < 16-byte tail only
-    } else {
-      rs_slice<DT, W>(P, src, P.buf[me], r.lo * P.esize, r.hi * P.esize);
+  for (int j = 0; j < P.sub; ++j) {
+    const int v = s * P.sub + j;
+    const Range r = slice_of(c.lo, c.hi, v, NV, 16 / P.esize);
+    // with two ranks the owner's chunk already is the non-straggler "sum"
+    if constexpr (W > 2) {
+      if constexpr (MV == MOVER_TMA) {
+        const uint64_t lo_b = r.lo * P.esize, hi_b = r.hi * P.esize;
+        const uint64_t body = (hi_b - lo_b) / 16 * 16;
+        tma_reduce<DT, W>(pipe, P.buf[me], src, lo_b, body);
+        rs_slice<DT, W>(P, src, P.buf[me], lo_b + body, hi_b);   // < 16-byte tail only
+      } else {
+        rs_slice<DT, W>(P, src, P.buf[me], r.lo * P.esize, r.hi * P.esize);
+      }
     }
+    // "partial ready" for the straggler's half of the exchange
+    cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, NV, v), ep, P.sys_scope);
   }
-  // "partial ready" for the straggler's half of the exchange
-  cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, G, s), ep, P.sys_scope);
 }
 
 // ---------------------------------------------------------------- LL Phase B (small chunks)
@@ -737,76 +737,80 @@ __device__ void ll_phase_b(const LaunchPlan& P, int s, int me, uint32_t ep) {
   }
 }
 
-// Phase B body (Algorithm 1 round executor) for rank `me`, slice s.
+// Phase B body (Algorithm 1 round executor) for rank `me`, CTA slot s: walks
+// the rank's op list in round order; every op runs over the CTA's `sub`
+// slices one after the other, each handed to the partner with its own flag.
 template <int DT, int W, int MV>
 __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
-  const int G = P.G;
+  const int NV = P.G * P.sub;   // slices per chunk (flag stride)
   const int V = 16 / P.esize;
   constexpr bool tma = MV == MOVER_TMA;
   if (P.use_ll) {
     ll_phase_b<DT, W>(P, s, me, ep);
     return;
   }
-  // the straggler reaches barrier (2): announce per slice to the others
+  // the straggler reaches barrier (2): announce per CTA slot to the others
   if (me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
-    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep, P.sys_scope);
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, NV, s), ep, P.sys_scope);
   char* mine = P.buf[me];
   const int nops = P.nops[me];
-  // optional trace: per op, when the wait began, when data movement began, when it was signalled
-  uint64_t* tr = (P.trace && threadIdx.x == 0) ? P.trace + ((size_t)me * G + s) * kMaxOps * 3 : nullptr;
-  for (int k = 0; k < nops; ++k) {
+  bool ok = true;
+  for (int k = 0; k < nops && ok; ++k) {
     const Op op = P.ops[me][k];
     const int c = op.chunk, peer = op.peer;
     const Range cr = chunk_range(P, c);
-    const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
-    if (tr) tr[3 * k] = globaltimer();
-    const uint64_t nvec_total = (sl.hi - sl.lo + V - 1) / V;
-    const uint64_t mid = sl.lo + (nvec_total / 2) * V < sl.hi ? sl.lo + (nvec_total / 2) * V : sl.hi;
-    if (op.kind == OP_EXCH_LOW) {
-      // non-straggler r: [lo, mid) of c_r = partial_r (+) x_sigma, stored at both ends
-      if (!cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, G, s), ep, P, 0x200 | k)) break;
-      if (tr) tr[3 * k + 1] = globaltimer();
-      const uint64_t a = sl.lo * P.esize, b = mid * P.esize;
-      if constexpr (tma)
-        tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, (b - a) / 16 * 16);
-      else
-        add2_vecs<DT>(mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, (b - a) / 16);
-      add2_tail<DT>(mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
-                    mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
-                    (int)((b - a) % 16) / P.esize, P.esize);
-      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep, P.sys_scope);
-    } else if (op.kind == OP_EXCH_HIGH) {
-      // straggler: [mid, hi) of c_r; waits for rank r's Phase-A partial
-      if (!cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, G, s), ep, P, 0x300 | k)) break;
-      if (tr) tr[3 * k + 1] = globaltimer();
-      const uint64_t a = mid * P.esize, b = sl.hi * P.esize;
-      if constexpr (tma)
-        tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, (b - a) / 16 * 16);
-      else
-        add2_vecs<DT>(mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, (b - a) / 16);
-      add2_tail<DT>(mine + a + (b - a) / 16 * 16, P.buf[peer] + a + (b - a) / 16 * 16,
-                    P.buf[peer] + a + (b - a) / 16 * 16, mine + a + (b - a) / 16 * 16,
-                    (int)((b - a) % 16) / P.esize, P.esize);
-      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep, P.sys_scope);
-    } else {
-      // copy of a fully reduced chunk (push)
-      if (!cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x400 | k)) break;
-      if (tr) tr[3 * k + 1] = globaltimer();
-      const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
-      if constexpr (tma)
-        tma_copy(pipe, P.buf[peer] + a, mine + a, (b - a) / 16 * 16);
-      else
-        copy_vecs(P.buf[peer] + a, mine + a, (b - a) / 16);
-      copy_tail(P.buf[peer] + a + (b - a) / 16 * 16, mine + a + (b - a) / 16 * 16, (int)((b - a) % 16));
-      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, G, s), ep, P.sys_scope);
+    for (int j = 0; j < P.sub && ok; ++j) {
+      const int v = s * P.sub + j;
+      const Range sl = slice_of(cr.lo, cr.hi, v, NV, V);
+      // optional trace: per op and slice, when the wait began, data movement began, it was signalled
+      uint64_t* tr = (P.trace && threadIdx.x == 0) ? P.trace + (((size_t)me * NV + v) * kMaxOps + k) * 3 : nullptr;
+      if (tr) tr[0] = globaltimer();
+      const uint64_t nvec_total = (sl.hi - sl.lo + V - 1) / V;
+      const uint64_t mid = sl.lo + (nvec_total / 2) * V < sl.hi ? sl.lo + (nvec_total / 2) * V : sl.hi;
+      if (op.kind == OP_EXCH_LOW) {
+        // non-straggler r: [lo, mid) of c_r = partial_r (+) x_sigma, stored at both ends
+        if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, NV, s), ep, P, 0x200 | k))) break;
+        if (tr) tr[1] = globaltimer();
+        const uint64_t a = sl.lo * P.esize, b = mid * P.esize, body = (b - a) / 16 * 16;
+        if constexpr (tma)
+          tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, body);
+        else
+          add2_vecs<DT>(mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, body / 16);
+        add2_tail<DT>(mine + a + body, P.buf[peer] + a + body, mine + a + body, P.buf[peer] + a + body,
+                      (int)((b - a) % 16) / P.esize, P.esize);
+      } else if (op.kind == OP_EXCH_HIGH) {
+        // straggler: [mid, hi) of c_r; waits for rank r's Phase-A partial
+        if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, NV, v), ep, P, 0x300 | k))) break;
+        if (tr) tr[1] = globaltimer();
+        const uint64_t a = mid * P.esize, b = sl.hi * P.esize, body = (b - a) / 16 * 16;
+        if constexpr (tma)
+          tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, body);
+        else
+          add2_vecs<DT>(mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, body / 16);
+        add2_tail<DT>(mine + a + body, P.buf[peer] + a + body, P.buf[peer] + a + body, mine + a + body,
+                      (int)((b - a) % 16) / P.esize, P.esize);
+      } else {
+        // copy of a fully reduced chunk (push)
+        if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, NV, v), ep, P, 0x400 | k))) break;
+        if (tr) tr[1] = globaltimer();
+        const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize, body = (b - a) / 16 * 16;
+        if constexpr (tma)
+          tma_copy(pipe, P.buf[peer] + a, mine + a, body);
+        else
+          copy_vecs(P.buf[peer] + a, mine + a, body / 16);
+        copy_tail(P.buf[peer] + a + body, mine + a + body, (int)((b - a) % 16));
+      }
+      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, NV, v), ep, P.sys_scope);
+      if (tr) tr[2] = globaltimer();
     }
-    if (tr) tr[3 * k + 2] = globaltimer();
   }
-  // postcondition: every chunk has landed here
-  if (threadIdx.x == 0) {
-    for (int c = 0; c < P.nchunks; ++c)
-      if (!spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0x500 | c)) break;
+  // postcondition: every chunk has landed here (one waiting thread per
+  // (chunk, slice) flag, so the acquire loads overlap)
+  if (ok && (int)threadIdx.x < P.nchunks * P.sub) {
+    const int c = threadIdx.x / P.sub, j = threadIdx.x % P.sub;
+    spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, NV, s * P.sub + j), ep, P, 0x500 | c);
   }
+  __syncthreads();
 }
 
 // Direct completion body (NEXT N1(ii)): one round instead of Algorithm 1's
@@ -817,22 +821,26 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
 // single-port (the P:149-150 assumption).
 template <int DT, int W, int MV>
 __device__ void direct_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
-  const int G = P.G;
+  const int NV = P.G * P.sub;   // slices per chunk (flag stride)
   const int V = 16 / P.esize;
   constexpr bool tma = MV == MOVER_TMA;
   int own = -1;
+  bool ok = true;
   if (me == P.sigma) {
     // the straggler arrives: its buffer may now be read by every owner
     if (threadIdx.x < W && (int)threadIdx.x != me)
-      st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, G, s), ep, P.sys_scope);
+      st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, NV, s), ep, P.sys_scope);
   } else {
     own = P.logical_of_phys[me];
-    if (cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + P.sigma, G, s), ep, P, 0x900)) {
+    ok = cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + P.sigma, NV, s), ep, P, 0x900);
+    if (ok) {
+      // the CTA's sub slices are adjacent: one pass over their union (no
+      // pipeline drain between them), then one flag per slice
       const Range cr = chunk_range(P, own);
-      const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
-      const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
+      const uint64_t a = slice_of(cr.lo, cr.hi, s * P.sub, NV, V).lo * P.esize;
+      const uint64_t b = slice_of(cr.lo, cr.hi, s * P.sub + P.sub - 1, NV, V).hi * P.esize;
       const uint64_t body = (b - a) / 16 * 16;
-      // every rank's buffer, own included, receives the fully reduced slice
+      // every rank's buffer, own included, receives the fully reduced slices
       if constexpr (tma)
         tma_add_bcast<DT, W>(pipe, P.buf, P.buf[me], P.buf[P.sigma], a, body);
       else
@@ -852,15 +860,17 @@ __device__ void direct_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint
         }
       }
       __syncthreads();
-      if (threadIdx.x < W && (int)threadIdx.x != me)
-        st_release(flag_at(P.flags[threadIdx.x], SLOT_HAVE + own, G, s), ep, P.sys_scope);
+      for (int j = 0; j < P.sub; ++j)
+        if (threadIdx.x < W && (int)threadIdx.x != me)
+          st_release(flag_at(P.flags[threadIdx.x], SLOT_HAVE + own, NV, s * P.sub + j), ep, P.sys_scope);
     }
   }
-  // postcondition: every other chunk has landed here
-  if (threadIdx.x == 0) {
-    for (int c = 0; c < P.nchunks; ++c)
-      if (c != own && !spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, G, s), ep, P, 0xA00 | c)) break;
+  // postcondition: every other chunk has landed here (one waiting thread per flag)
+  if (ok && (int)threadIdx.x < P.nchunks * P.sub) {
+    const int c = threadIdx.x / P.sub, j = threadIdx.x % P.sub;
+    if (c != own) spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, NV, s * P.sub + j), ep, P, 0xA00 | c);
   }
+  __syncthreads();
 }
 
 // KIND: 0 Phase A only, 1 Phase B (schedule), 3 Phase B (direct),
@@ -903,7 +913,7 @@ template <int DT, int W, int MV>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_constant__ LaunchPlan P) {
   const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
   const int j = P.local_rank[li];
-  const int G = P.G;
+  const int G = P.G * P.sub;   // the host launches the ring with sub = 1
   const int V = 16 / P.esize;
   const uint32_t ep = call_epoch(P);
   const int left = (j + W - 1) % W, right = (j + 1) % W;

@@ -6,8 +6,9 @@
 
 namespace stragglar {
 
-// Flag slots.  Every rank owns kSlots * G uint32 flags; slot k, slice s lives
-// at flags[k * G + s].  Flags hold the call's epoch (monotonic, never reset):
+// Flag slots.  Every rank owns kSlots * G * sub uint32 flags; slot k, slice v
+// lives at flags[k * G * sub + v] (G CTAs per rank, each covering `sub`
+// consecutive slices of every chunk; see LaunchPlan::sub).  Flags hold the call's epoch (monotonic, never reset):
 // a waiter proceeds when (int32)(flag - epoch) >= 0.  Producers write peers'
 // flags (remote store, release at system scope); consumers spin on their own
 // (local load, acquire at system scope).
@@ -27,6 +28,7 @@ enum Slot : int {
 #endif
 constexpr int kThreads = STRAGGLAR_THREADS;   // CTA size of the data kernels
 constexpr int kMaxSlices = 1024;
+constexpr int kMaxSub = 16;                   // slices per CTA (LaunchPlan::sub) at most
 // Low-latency (LL) Phase B for small chunks: every 8-byte word carries 4
 // payload bytes and the call epoch; per rank one LL area of kLLChunkBytes of
 // payload per chunk follows the flag array in the same allocation.
@@ -56,7 +58,10 @@ enum Mover : int { MOVER_LSU = 0, MOVER_TMA = 1 };
 struct LaunchPlan {
   int world;
   int sigma;                 // physical straggler
-  int G;                     // slices per chunk == CTAs per rank
+  int G;                     // CTAs per rank
+  int sub;                   // slices per CTA: every chunk is cut into G * sub slices and CTA s
+                             // handles slices s*sub .. s*sub+sub-1, one flag each (finer-grained
+                             // hand-offs between ranks with the same CTAs); 1 = one slice per CTA
   int nlocal;                // ranks served by this launch (1, or world in team mode)
   int local_rank[kMaxWorld]; // physical rank of local index i (blockIdx.x / G)
   char* buf[kMaxWorld];      // data buffer of each physical rank (local or peer mapping)

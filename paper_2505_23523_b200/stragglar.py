@@ -331,7 +331,7 @@ def stragglar_team_set_trace(enable: bool) -> None:
 
 
 def stragglar_team_read_trace():
-    """-> (list of uint64 stamps [rank][slice][op][wait, data, done], slices G)."""
+    """-> (list of uint64 stamps [rank][slice][op][wait, data, done], slices per chunk)."""
     n, g = _c_size(0), _c_int(0)
     st = _lib.stragglar_team_read_trace(None, 0, ctypes.byref(n), ctypes.byref(g))
     if st not in (0, 1):

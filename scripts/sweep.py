@@ -222,12 +222,17 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--max-log2-bytes", type=int, default=30)
+    ap.add_argument("--worlds", default="2,4,8")
+    ap.add_argument("--sizes-only", action="store_true", help="size sweep only (A/B runs)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     out = {"sizes": [], "configs": {}, "delay_sweep": None}
-    for n in (2, 4, 8):
+    for n in [int(x) for x in args.worlds.split(",")]:
         for k in range(20, args.max_log2_bytes + 1):
             out["sizes"].append(measure(n, 0, (1 << k) // 2, torch.bfloat16, args.iters, args.warmup))
+    if args.sizes_only:
+        print(json.dumps(out))
+        return
     out["configs"]["config4_dp_bucket_25MiB_bf16"] = measure(8, 0, 13_107_200, torch.bfloat16, args.iters, args.warmup)
     out["configs"]["config5_tp_64x8192_bf16_straggler3"] = measure(8, 3, 524_288, torch.bfloat16, args.iters, args.warmup)
     out["configs"]["config1_n4_1M_fp32"] = measure(4, 0, 1 << 20, torch.float32, args.iters, args.warmup)

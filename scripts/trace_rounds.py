@@ -66,5 +66,21 @@ for r in sorted(rounds):
                  "op_time_median_us": round(statistics.median(x[2] - x[1] for x in v) / 1e3, 1),
                  "span_GBps": round(nbytes / (span * 1e-6) / 1e9, 1) if span > 0 else None})
 total = max(r["done_last_us"] for r in rows)
-out = {"G": G, "chunk_bytes": C, "phase_b_trace_span_us": total, "rounds": rows}
+# per rank: for every op, median over slices of (wait began, data began, signalled)
+per_rank = {}
+for p in range(n):
+    lst = []
+    for k, (r, c, kind) in enumerate(ops[p]):
+        w_, d_, e_ = [], [], []
+        for s in range(G):
+            base = ((p * G + s) * 16 + k) * 3
+            w, d, e = tr[base:base + 3]
+            if w and d and e:
+                w_.append(w - t_min); d_.append(d - t_min); e_.append(e - t_min)
+        if w_:
+            lst.append({"op": k, "round": r, "chunk": c, "kind": "exch" if kind == 0 else "copy",
+                        "wait_us": round(statistics.median(w_) / 1e3, 1), "data_us": round(statistics.median(d_) / 1e3, 1),
+                        "done_us": round(statistics.median(e_) / 1e3, 1), "done_max_us": round(max(e_) / 1e3, 1)})
+    per_rank[f"phys{p}"] = lst
+out = {"G": G, "chunk_bytes": C, "phase_b_trace_span_us": total, "rounds": rows, "per_rank": per_rank}
 print(json.dumps(out, indent=1))

@@ -427,3 +427,44 @@ def test_trace_stamps(S):
                 assert 0 < w <= d <= e, (p, s, k, w, d, e)
                 seen += 1
     assert seen == G * sum(nops)
+
+
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+def test_subslices(S, dtype):
+    """Several slices per CTA (LaunchPlan::sub, each handed over with its own
+    flag): forced at moderate sizes with small slice targets, on the fused
+    call, the split phases, direct completion and the Ring (sub = 1 there),
+    with the Phase-B trace laid out per slice."""
+    keys = ("STRAGGLAR_SLICE_BYTES", "STRAGGLAR_SUBSLICE_BYTES")
+    old = {k: os.environ.get(k) for k in keys}
+    try:
+        os.environ["STRAGGLAR_SLICE_BYTES"] = "1024"
+        os.environ["STRAGGLAR_SUBSLICE_BYTES"] = "2048"
+        for n, sigma, count in [(8, 0, 2_000_003), (4, 2, 300_001), (6, 1, 777_777), (2, 1, 500_001)]:
+            for algo in ("stragglar", "direct", "ring"):
+                xs, outs = run_team(S, n, sigma, dtype, count, config=97, algo=algo)
+                want = N.ring_allreduce(xs, dtype) if algo == "ring" else N.stragglar_allreduce(xs, sigma, dtype)
+                check_equal(outs, want, xs, dtype, f"sub n={n} {algo}")
+            # split phases with tracing: G * sub slices per chunk in the trace
+            xs = make_inputs(n, count, dtype, config=98)
+            bufs = [to_dev(x, dtype) for x in xs]
+            S.stragglar_team_init(n, sigma)
+            S.stragglar_team_set_trace(True)
+            S.stragglar_team_reduce_scatter(bufs)
+            S.stragglar_team_inject_delay(20_000)
+            S.stragglar_team_complete(bufs)
+            torch.cuda.synchronize()
+            assert S.stragglar_team_check_error() == 0
+            tr, nslices = S.stragglar_team_read_trace()
+            S.stragglar_team_set_trace(False)
+            assert nslices > S.stragglar_team_slices(), (nslices, S.stragglar_team_slices())
+            check_equal([to_host(b, dtype) for b in bufs], N.stragglar_allreduce(xs, sigma, dtype), xs, dtype,
+                        f"sub split n={n}")
+            stamps = np.asarray(tr).reshape(n, nslices, 16, 3)
+            assert (stamps[:, :, 0, 2] > 0).all()       # every rank's first op ran on every slice
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
