@@ -439,8 +439,8 @@ def test_subslices(S, dtype):
     old = {k: os.environ.get(k) for k in keys}
     try:
         os.environ["STRAGGLAR_SLICE_BYTES"] = "1024"
-        os.environ["STRAGGLAR_SUBSLICE_BYTES"] = "2048"
-        for n, sigma, count in [(8, 0, 2_000_003), (4, 2, 300_001), (6, 1, 777_777), (2, 1, 500_001)]:
+        os.environ["STRAGGLAR_SUBSLICE_BYTES"] = "1024"     # 3-16 slices per CTA below
+        for n, sigma, count in [(8, 0, 2_000_003), (4, 2, 900_001), (6, 1, 777_777), (2, 1, 500_001)]:
             for algo in ("stragglar", "direct", "ring"):
                 xs, outs = run_team(S, n, sigma, dtype, count, config=97, algo=algo)
                 want = N.ring_allreduce(xs, dtype) if algo == "ring" else N.stragglar_allreduce(xs, sigma, dtype)
