@@ -559,7 +559,6 @@ int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* s
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
   slices_for(c, P.ce * P.esize, &P.G, &P.sub);
-  P.sub = 1;   // the ring kernel runs one slice per CTA
   return launch(K_RING, dtype, P, P.G, stream);
 }
 
@@ -739,7 +738,6 @@ int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, in
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
   slices_for(c, P.ce * P.esize, &P.G, &P.sub);
-  P.sub = 1;   // the ring kernel runs one slice per CTA
   for (int p = 0; p < c.world; ++p) {
     P.buf[p] = (char*)bufs[p];
     P.local_rank[p] = p;

@@ -913,45 +913,50 @@ template <int DT, int W, int MV>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_constant__ LaunchPlan P) {
   const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
   const int j = P.local_rank[li];
-  const int G = P.G * P.sub;   // the host launches the ring with sub = 1
+  const int NV = P.G * P.sub;   // slices per chunk (flag stride); CTA s covers s*sub .. s*sub+sub-1
   const int V = 16 / P.esize;
   const uint32_t ep = call_epoch(P);
   const int left = (j + W - 1) % W, right = (j + 1) % W;
-  if (threadIdx.x == 0) st_release(flag_at(P.flags[right], SLOT_RING_ARRIVE, G, s), ep, P.sys_scope);
+  if (threadIdx.x == 0) st_release(flag_at(P.flags[right], SLOT_RING_ARRIVE, NV, s), ep, P.sys_scope);
   constexpr bool tma = MV == MOVER_TMA;
   Pipe pipe = make_pipe(tma);
   char* mine = P.buf[j];
   const char* lbuf = P.buf[left];
   for (int t = 0; t < 2 * (W - 1); ++t) {
-    const int wslot = (t == 0) ? SLOT_RING_ARRIVE : SLOT_RING_READY + t - 1;
-    if (!cta_wait(flag_at(P.flags[j], wslot, G, s), ep, P, 0x600 | t)) {
-      finish_call(P);
-      return;
-    }
     const int k = (t < W - 1) ? ((j - 1 - t) % W + 2 * W) % W : ((j - t + W - 1) % W + 2 * W) % W;
     const Range cr = chunk_range(P, k);
-    const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
-    const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
-    const uint64_t nv = (b - a) / 16;
-    if (t < W - 1) {
-      if constexpr (tma)
-        tma_add2<DT>(pipe, mine + a, nullptr, lbuf + a, mine + a, nv * 16);
-      else
-        add2_vecs<DT>(mine + a, nullptr, lbuf + a, mine + a, nv);
-      add2_tail<DT>(mine + a + nv * 16, nullptr, lbuf + a + nv * 16, mine + a + nv * 16, (int)((b - a) % 16) / P.esize,
-                    P.esize);
-    } else {
-      if constexpr (tma)
-        tma_copy(pipe, mine + a, lbuf + a, nv * 16);
-      else
-        copy_vecs(mine + a, lbuf + a, nv);
-      copy_tail(mine + a + nv * 16, lbuf + a + nv * 16, (int)((b - a) % 16));
+    for (int q = 0; q < P.sub; ++q) {
+      const int v = s * P.sub + q;
+      // step 0 waits for the left neighbour's arrival (per CTA), step t for its step t-1 on slice v
+      const uint32_t* wf = (t == 0) ? flag_at(P.flags[j], SLOT_RING_ARRIVE, NV, s)
+                                    : flag_at(P.flags[j], SLOT_RING_READY + t - 1, NV, v);
+      if (!cta_wait(wf, ep, P, 0x600 | t)) {
+        finish_call(P);
+        return;
+      }
+      const Range sl = slice_of(cr.lo, cr.hi, v, NV, V);
+      const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
+      const uint64_t nv = (b - a) / 16;
+      if (t < W - 1) {
+        if constexpr (tma)
+          tma_add2<DT>(pipe, mine + a, nullptr, lbuf + a, mine + a, nv * 16);
+        else
+          add2_vecs<DT>(mine + a, nullptr, lbuf + a, mine + a, nv);
+        add2_tail<DT>(mine + a + nv * 16, nullptr, lbuf + a + nv * 16, mine + a + nv * 16,
+                      (int)((b - a) % 16) / P.esize, P.esize);
+      } else {
+        if constexpr (tma)
+          tma_copy(pipe, mine + a, lbuf + a, nv * 16);
+        else
+          copy_vecs(mine + a, lbuf + a, nv);
+        copy_tail(mine + a + nv * 16, lbuf + a + nv * 16, (int)((b - a) % 16));
+      }
+      if (t < 2 * (W - 1) - 1) cta_signal(flag_at(P.flags[right], SLOT_RING_READY + t, NV, v), ep, P.sys_scope);
     }
-    if (t < 2 * (W - 1) - 1) cta_signal(flag_at(P.flags[right], SLOT_RING_READY + t, G, s), ep, P.sys_scope);
   }
   // I am done reading the left buffer; wait until the right neighbour is done with mine
-  cta_signal(flag_at(P.flags[left], SLOT_RING_DONE, G, s), ep, P.sys_scope);
-  cta_wait(flag_at(P.flags[j], SLOT_RING_DONE, G, s), ep, P, 0x700);
+  cta_signal(flag_at(P.flags[left], SLOT_RING_DONE, NV, s), ep, P.sys_scope);
+  cta_wait(flag_at(P.flags[j], SLOT_RING_DONE, NV, s), ep, P, 0x700);
   finish_call(P);
 }
 
