@@ -391,7 +391,7 @@ def bench_multi(args):
         dist.init_process_group("gloo")
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    _, _, dtype, count, desc = WORKLOADS[args.workload]
+    _, _, dtype, count, _ = WORKLOADS[args.workload]
     sigma = 0
     esize = ESIZE[dtype]
     S_bytes = count * esize
@@ -445,6 +445,19 @@ def bench_multi(args):
             ph = torch.tensor([ta if rank != sigma else 0.0, tk], device="cpu" if shared else "cuda")
             dist.all_reduce(ph, op=dist.ReduceOp.MAX)
             phase_times = {"T_phaseA_us_max_NS": round(ph[0].item(), 2), "T_kernel_us_max": round(ph[1].item(), 2)}
+    # end to end through the public host-buffer entry point: every step copies this rank's
+    # input from pinned host memory, runs StragglAR and copies the result back (pipelined pieces)
+    hin = buf.cpu().pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+    comm.allreduce_host(hin, hout, buf)
+    dist.barrier()
+    e2e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        comm.allreduce_host(hin, hout, buf)        # synchronous per rank
+    e2e_rank = (time.perf_counter() - t0) * 1e6 / e2e_steps
+    e2e_t = torch.tensor([e2e_rank], device="cpu" if shared else "cuda")
+    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     code, where = S.stragglar_check_error_where(False)
     if code:
         raise RuntimeError(f"device watchdog fired (where=0x{where:x})")
@@ -471,7 +484,8 @@ def bench_multi(args):
             "scaling": "weak", "vs_baseline": None,
             "dtype": {"float32": "f32", "bfloat16": "bf16", "int32": "i32"}[dtype],
             "data": "synthetic (seeded N(0,1))",
-            "config": {"workload": f"{args.workload}: {desc}; one process per GPU, CUDA IPC over NVLink/NVSwitch",
+            "config": {"workload": f"{args.workload} per-rank buffer ({count} {dtype}, SUM), {world} ranks, straggler "
+                                   "rank 0; one process per GPU, CUDA IPC over NVLink/NVSwitch",
                        "world": world, "straggler_rank": sigma, "count": count, "delay_us": D_ns / 1e3,
                        "parallelism": f"allreduce{world}"},
             "T_total_us": round(T_tot, 2), "D_meas_us": round(D_meas, 2), "phase_times_in_kernel": phase_times,
@@ -484,7 +498,10 @@ def bench_multi(args):
             "shared_device_test": shared,
             "roofline": roof,
             "cpu_baseline": None,
-            "e2e": None,
+            "e2e": {"value": round(e2e_t.item(), 1), "unit": "us", "h2d_bytes_per_step": world * S_bytes,
+                    "d2h_bytes_per_step": world * S_bytes,
+                    "what": "stragglar_allreduce_host per rank: pinned host -> HBM, StragglAR (no injected delay), "
+                            "HBM -> host, pipelined over 8 MiB pieces; max over ranks, mean of the steps"},
             "gpu_launches": launches,
             "clocks": clocks,
         }
@@ -499,6 +516,10 @@ def bench_reference(args):
     if int(os.environ.get("RANK", "0")) != 0:
         return
     world, sigma, dtype, count, desc = WORKLOADS[args.workload]
+    if world_env > 1:
+        # our arm at N GPUs runs N ranks (one per GPU, straggler 0) on the same per-rank buffer
+        world, sigma = world_env, 0
+        desc = f"{world} ranks, straggler rank 0, {count} {dtype} per rank SUM"
     sample = min(count, 1 << 22)
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import numerics as N

@@ -126,6 +126,17 @@ int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* s
  * (n+log2 n-2)/(n-1)*S, one round instead of n+log2 n-2.  Result identical
  * to stragglar_allreduce, bit for bit. */
 int stragglar_allreduce_direct(void* buf, size_t count, int dtype, int op, void* stream);
+/* End to end from host memory (collective): host_in (count elements) is
+ * copied into the registered device buffer `buf`, AllReduced with
+ * stragglar_allreduce, and the result copied to host_out (may equal
+ * host_in), through a pipeline of pieces (STRAGGLAR_E2E_PIECE_BYTES, 8 MiB):
+ * H2D of piece k+1, the AllReduce of piece k and D2H of piece k-1 overlap.
+ * Every rank cuts the same pieces, so each piece is one collective call.
+ * Synchronous: returns when host_out holds the result.  host buffers should
+ * be pinned for full PCIe bandwidth.  Same errors as stragglar_allreduce,
+ * INVALID_ARG for NULL host pointers. */
+int stragglar_allreduce_host(const void* host_in, void* host_out, void* buf, size_t count, int dtype, int op,
+                             void* stream);
 /* Device-side barrier among all ranks of the communicator (bench start line). */
 int stragglar_barrier(void* stream);
 /* Bench only: a one-thread kernel that spins on %globaltimer for `ns`

@@ -354,6 +354,74 @@ int read_error(Comm& c, int* code, uint32_t* where = nullptr) {
   return h.err == ERR_TIMEOUT ? STRAGGLAR_ERR_TIMEOUT : STRAGGLAR_OK;
 }
 
+// Host-buffer entry points: because the SUM is elementwise, the buffers go
+// through a three-stage pipeline of pieces: H2D of piece k+1 (copy engine, one
+// direction), the AllReduce of piece k (SMs) and D2H of piece k-1 (copy
+// engine, the other direction) overlap.  Pieces keep 16-byte alignment; every
+// rank cuts the same pieces, so each piece's AllReduce is one collective call.
+// Synchronous: returns after the last D2H landed.
+template <class F>
+int e2e_pipeline(int nbufs, const void* const* host_in, void* const* host_out, void* const* bufs, size_t count, int es,
+                 cudaStream_t s, uint64_t piece_bytes, int ncs, F&& allreduce_piece) {
+  const uint64_t v = 16 / es;
+  uint64_t piece = piece_bytes / es;
+  piece = piece / v * v;
+  if (piece == 0) piece = v;
+  const uint64_t npieces = (count + piece - 1) / piece;
+  // copy streams per direction (several copy engines; buffers alternate between them)
+  if (ncs < 1) ncs = 1;
+  if (ncs > nbufs) ncs = nbufs;
+  struct Res {                                      // released on every return path
+    std::vector<cudaStream_t> h2d, d2h;
+    std::vector<cudaEvent_t> ev;
+    ~Res() {
+      for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
+      for (auto x : h2d)
+        if (x) cudaStreamDestroy(x);
+      for (auto x : d2h)
+        if (x) cudaStreamDestroy(x);
+    }
+  } res;
+  res.h2d.assign(ncs, nullptr);
+  res.d2h.assign(ncs, nullptr);
+  for (int i = 0; i < ncs; ++i) {
+    CK(cudaStreamCreateWithFlags(&res.h2d[i], cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&res.d2h[i], cudaStreamNonBlocking));
+  }
+  // events: per piece, one after each H2D stream, one after the AllReduce, one after each D2H stream
+  const size_t per = 2 * ncs + 1;
+  res.ev.assign(per * npieces + 1, nullptr);
+  std::vector<cudaEvent_t>& ev = res.ev;
+  for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(cudaEventRecord(ev.back(), s));               // everything earlier on `stream` first
+  for (int i = 0; i < ncs; ++i) CK(cudaStreamWaitEvent(res.h2d[i], ev.back(), 0));
+  int st = STRAGGLAR_OK;
+  for (uint64_t k = 0; k < npieces && st == STRAGGLAR_OK; ++k) {
+    const uint64_t off = k * piece, n = (count - off) < piece ? (count - off) : piece;
+    const size_t boff = off * es, bytes = n * es;
+    cudaEvent_t* e = &ev[per * k];
+    for (int p = 0; p < nbufs; ++p)
+      CK(cudaMemcpyAsync((char*)bufs[p] + boff, (const char*)host_in[p] + boff, bytes, cudaMemcpyHostToDevice,
+                         res.h2d[p % ncs]));
+    for (int i = 0; i < ncs; ++i) {
+      CK(cudaEventRecord(e[i], res.h2d[i]));
+      CK(cudaStreamWaitEvent(s, e[i], 0));
+    }
+    st = allreduce_piece(off, n);
+    CK(cudaEventRecord(e[ncs], s));
+    for (int i = 0; i < ncs; ++i) CK(cudaStreamWaitEvent(res.d2h[i], e[ncs], 0));
+    for (int p = 0; p < nbufs; ++p)
+      CK(cudaMemcpyAsync((char*)host_out[p] + boff, (char*)bufs[p] + boff, bytes, cudaMemcpyDeviceToHost,
+                         res.d2h[p % ncs]));
+    for (int i = 0; i < ncs; ++i) CK(cudaEventRecord(e[ncs + 1 + i], res.d2h[i]));
+  }
+  if (npieces)
+    for (int i = 0; i < ncs; ++i) CK(cudaStreamWaitEvent(s, ev[per * (npieces - 1) + ncs + 1 + i], 0));
+  CK(cudaStreamSynchronize(s));
+  return st;
+}
+
 }  // namespace
 
 extern "C" {
@@ -768,71 +836,38 @@ int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_
   for (int p = 0; p < world; ++p)
     if (!host_in[p] || !host_out[p]) return STRAGGLAR_ERR_INVALID_ARG;
   const int es = esize_of(dtype);
-  cudaStream_t s = (cudaStream_t)stream;
-  // The SUM is elementwise, so the buffer is processed in pieces through a
-  // three-stage pipeline: H2D of piece k+1 (copy engine, one direction), the
-  // AllReduce of piece k (SMs) and D2H of piece k-1 (copy engine, the other
-  // direction) overlap.  Pieces keep 16-byte alignment.
-  const uint64_t v = 16 / es;
-  uint64_t piece = g_team.e2e_piece_bytes / es;
-  piece = piece / v * v;
-  if (piece == 0) piece = v;
-  const uint64_t npieces = (count + piece - 1) / piece;
-  // copy streams per direction (several copy engines; ranks alternate between them)
-  int ncs = g_team.e2e_streams;
-  if (ncs < 1) ncs = 1;
-  if (ncs > world) ncs = world;
-  struct Res {                                      // released on every return path
-    std::vector<cudaStream_t> h2d, d2h;
-    std::vector<cudaEvent_t> ev;
-    ~Res() {
-      for (auto& e : ev)
-        if (e) cudaEventDestroy(e);
-      for (auto x : h2d)
-        if (x) cudaStreamDestroy(x);
-      for (auto x : d2h)
-        if (x) cudaStreamDestroy(x);
-    }
-  } res;
-  res.h2d.assign(ncs, nullptr);
-  res.d2h.assign(ncs, nullptr);
-  for (int i = 0; i < ncs; ++i) {
-    CK(cudaStreamCreateWithFlags(&res.h2d[i], cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&res.d2h[i], cudaStreamNonBlocking));
-  }
-  // events: per piece, one after each H2D stream, one after the AllReduce, one after each D2H stream
-  const size_t per = 2 * ncs + 1;
-  res.ev.assign(per * npieces + 1, nullptr);
-  std::vector<cudaEvent_t>& ev = res.ev;
-  for (auto& e : ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  CK(cudaEventRecord(ev.back(), s));               // everything earlier on `stream` first
-  for (int i = 0; i < ncs; ++i) CK(cudaStreamWaitEvent(res.h2d[i], ev.back(), 0));
   std::vector<void*> sub(world);
-  st = STRAGGLAR_OK;
-  for (uint64_t k = 0; k < npieces && st == STRAGGLAR_OK; ++k) {
-    const uint64_t off = k * piece, n = (count - off) < piece ? (count - off) : piece;
-    const size_t boff = off * es, bytes = n * es;
-    cudaEvent_t* e = &ev[per * k];
-    for (int p = 0; p < world; ++p)
-      CK(cudaMemcpyAsync((char*)bufs[p] + boff, (const char*)host_in[p] + boff, bytes, cudaMemcpyHostToDevice,
-                         res.h2d[p % ncs]));
-    for (int i = 0; i < ncs; ++i) {
-      CK(cudaEventRecord(e[i], res.h2d[i]));
-      CK(cudaStreamWaitEvent(s, e[i], 0));
-    }
-    for (int p = 0; p < world; ++p) sub[p] = (char*)bufs[p] + boff;
-    st = stragglar_team_allreduce(sub.data(), n, dtype, op, stream);
-    CK(cudaEventRecord(e[ncs], s));
-    for (int i = 0; i < ncs; ++i) CK(cudaStreamWaitEvent(res.d2h[i], e[ncs], 0));
-    for (int p = 0; p < world; ++p)
-      CK(cudaMemcpyAsync((char*)host_out[p] + boff, (char*)bufs[p] + boff, bytes, cudaMemcpyDeviceToHost,
-                         res.d2h[p % ncs]));
-    for (int i = 0; i < ncs; ++i) CK(cudaEventRecord(e[ncs + 1 + i], res.d2h[i]));
+  return e2e_pipeline(world, host_in, host_out, bufs, count, es, (cudaStream_t)stream, g_team.e2e_piece_bytes,
+                      g_team.e2e_streams, [&](uint64_t off, uint64_t n) {
+                        for (int p = 0; p < world; ++p) sub[p] = (char*)bufs[p] + off * es;
+                        return stragglar_team_allreduce(sub.data(), n, dtype, op, stream);
+                      });
+}
+
+int stragglar_allreduce_host(const void* host_in, void* host_out, void* buf, size_t count, int dtype, int op,
+                             void* stream) {
+  int st;
+  uint64_t piece;
+  int ncs;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    Comm& c = g_proc;
+    if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
+    if ((st = check_args(buf, count, dtype, op))) return st;
+    if (count == 0) return STRAGGLAR_OK;
+    if (!host_in || !host_out) return STRAGGLAR_ERR_INVALID_ARG;
+    LaunchPlan P;
+    if ((st = proc_plan(buf, count, dtype, &P))) return st;   // the whole range must be registered
+    piece = c.e2e_piece_bytes;
+    ncs = c.e2e_streams;
   }
-  if (npieces)
-    for (int i = 0; i < ncs; ++i) CK(cudaStreamWaitEvent(s, ev[per * (npieces - 1) + ncs + 1 + i], 0));
-  CK(cudaStreamSynchronize(s));
-  return st;
+  const int es = esize_of(dtype);
+  const void* hin[1] = {host_in};
+  void* hout[1] = {host_out};
+  void* b[1] = {buf};
+  return e2e_pipeline(1, hin, hout, b, count, es, (cudaStream_t)stream, piece, ncs, [&](uint64_t off, uint64_t n) {
+    return stragglar_allreduce((char*)buf + off * es, n, dtype, op, stream);
+  });
 }
 
 int stragglar_team_set_trace(int enable) {

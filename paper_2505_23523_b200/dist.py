@@ -51,6 +51,10 @@ class ProcessComm:
     def allreduce(self, tensor, stream=None) -> None:
         self.lib.stragglar_allreduce(tensor, stream)
 
+    def allreduce_host(self, host_in, host_out, tensor, stream=None) -> None:
+        """host_in -> tensor (registered) -> StragglAR -> host_out, pipelined in pieces."""
+        self.lib.stragglar_allreduce_host(host_in, host_out, tensor, stream)
+
     def allreduce_ring(self, tensor, stream=None) -> None:
         self.lib.stragglar_allreduce_ring(tensor, stream)
 

@@ -56,6 +56,7 @@ _SIGS = {
     "stragglar_allreduce": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_allreduce_ring": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_allreduce_direct": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_allreduce_host": ([_vp, _vp, _vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_barrier": ([_vp], _c_int),
     "stragglar_inject_delay": ([_c_u64, _vp], _c_int),
     "stragglar_check_error": ([ctypes.POINTER(_c_int)], _c_int),
@@ -201,6 +202,16 @@ def stragglar_allreduce(t, stream=None) -> None:
 def stragglar_allreduce_ring(t, stream=None) -> None:
     _ck("stragglar_allreduce_ring",
         _lib.stragglar_allreduce_ring(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream)))
+
+
+def stragglar_allreduce_host(host_in, host_out, t, stream=None) -> None:
+    """host_in/host_out: contiguous CPU tensors (pinned for full bandwidth) shaped like t."""
+    for h in (host_in, host_out):
+        if h.is_cuda or h.numel() != t.numel() or h.dtype != t.dtype or not h.is_contiguous():
+            raise ValueError("host buffers must be contiguous CPU tensors matching the device buffer")
+    _ck("stragglar_allreduce_host",
+        _lib.stragglar_allreduce_host(host_in.data_ptr(), host_out.data_ptr(), t.data_ptr(), t.numel(),
+                                      _dtype_code(t), SUM, _stream_ptr(stream)))
 
 
 def stragglar_select(world: int, nbytes: float, delay_s: float, alpha_s: float, beta_s_per_byte: float):

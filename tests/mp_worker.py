@@ -23,6 +23,7 @@ def worker(rank, world, sigma, count, dtype, port, q):
     try:
         os.environ.setdefault("STRAGGLAR_TIMEOUT_MS", "60000")
         os.environ.setdefault("STRAGGLAR_SLICES", "8")
+        os.environ.setdefault("STRAGGLAR_E2E_PIECE_BYTES", "40000")   # several pieces for the host entry point
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
         torch.cuda.set_device(0)
         from paper_2505_23523_b200.dist import ProcessComm
@@ -34,7 +35,7 @@ def worker(rank, world, sigma, count, dtype, port, q):
         tdt = {"float32": torch.float32, "int32": torch.int32, "bfloat16": torch.bfloat16}[dtype]
         t = torch.empty(count, dtype=tdt, device="cuda")
         ring = torch.empty(count, dtype=tdt, device="cuda")
-        autos = [torch.empty(count, dtype=tdt, device="cuda") for _ in range(3)]
+        autos = [torch.empty(count, dtype=tdt, device="cuda") for _ in range(4)]
         comm.register(t)
         comm.register(ring)
         for a in autos:
@@ -57,11 +58,16 @@ def worker(rank, world, sigma, count, dtype, port, q):
         used = [S.stragglar_allreduce_auto(autos[0], 0), S.stragglar_allreduce_auto(autos[1], 10_000_000)]
         S.stragglar_allreduce_direct(autos[2])     # NEXT row N1(ii): same result as the schedule
         used.append(True)
+        # end to end from pinned host memory, pipelined pieces, result back in host memory
+        hin = host.clone().pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        comm.allreduce_host(hin.view(tdt), hout.view(tdt), autos[3])
         torch.cuda.synchronize()
         err = S.stragglar_check_error()
         out = t.view(host.dtype).cpu().numpy()
         rout = ring.view(host.dtype).cpu().numpy()
-        aout = [(u, a.view(host.dtype).cpu().numpy().tobytes()) for u, a in zip(used, autos)]
+        aout = [(u, a.view(host.dtype).cpu().numpy().tobytes()) for u, a in zip(used, autos[:3])]
+        aout.append((True, hout.numpy().tobytes()))
         dist.barrier()
         comm.close()
         q.put((rank, err, out.tobytes(), rout.tobytes(), aout))
