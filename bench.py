@@ -562,7 +562,7 @@ def bench_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)   # 5 warm-up + 50 measured
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="stragglar", choices=["stragglar", "reference"])
     ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
