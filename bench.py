@@ -293,7 +293,7 @@ def bench_team(args):
     pcie_floor = (time.perf_counter() - t0) * 1e6
     del host_out
 
-    # roofline of the dominant kernel (Phase B, k_complete): HBM bytes it must move
+    # roofline of the dominant kernel (Phase B, k_phase<..., KIND 1>): HBM bytes it must move
     C = chunk_bytes(count, world - 1, esize)
     bytes_B = 2 * world * (world - 1) * C           # (n-1)(n-2) copies x 2C + (n-1) exchanges x 4C
     bytes_A = world * (world - 1) * C               # each owner reads n-1 chunks, writes 1
@@ -306,7 +306,7 @@ def bench_team(args):
         try:
             tr = json.load(open(prof))
             if tr.get("workload") == args.workload:
-                traffic = tr.get("k_complete_dram_bytes")
+                traffic = tr.get("phase_b_dram_bytes")
         except Exception:
             pass
 

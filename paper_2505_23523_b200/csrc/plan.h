@@ -51,7 +51,7 @@ struct DevState {
 
 enum ErrCode : uint32_t { ERR_TIMEOUT = 1, ERR_BAD_PLAN = 2 };
 
-// How k_complete moves bytes: SM load/store instructions (16-byte vectors) or
+// How the data kernels move bytes: SM load/store instructions (16-byte vectors) or
 // TMA bulk copies (cp.async.bulk through a shared-memory stage ring).
 enum Mover : int { MOVER_LSU = 0, MOVER_TMA = 1 };
 

@@ -2,7 +2,7 @@
 
 usage: python scripts/ncu_summary.py <tag> <rep> [<rep> ...]
 writes profiles/<tag>/ncu_summary.json and .md; with --traffic also
-profiles/latest_traffic.json (k_complete DRAM bytes per launch, read by bench.py).
+profiles/latest_traffic.json (Phase-B kernel DRAM bytes per launch, read by bench.py).
 """
 import csv
 import io
@@ -75,9 +75,9 @@ def main():
     if "--traffic" in sys.argv:
         for r in res:
             name = r["kernel"].replace("(int)", "")
-            if "k_complete" in name or ("k_phase<" in name and name.split(">")[0].endswith(", 1")):
+            if ("k_phase<" in name and name.split(">")[0].endswith(", 1")):
                 tr = r["dram__bytes_read.sum"]["value"] + r["dram__bytes_write.sum"]["value"]
-                json.dump({"workload": "config2", "k_complete_dram_bytes": tr, "source": f"profiles/{tag}/ncu_summary.json",
+                json.dump({"workload": "config2", "phase_b_dram_bytes": tr, "source": f"profiles/{tag}/ncu_summary.json",
                            "kernel": r["kernel"]}, open(os.path.join(outdir, "latest_traffic.json"), "w"), indent=1)
     print(open(os.path.join(d, "ncu_summary.md")).read())
 
