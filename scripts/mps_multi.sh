@@ -10,7 +10,7 @@ sleep 2
 export CUDA_MPS_ACTIVE_THREAD_PERCENTAGE=${PCT:-12}
 export STRAGGLAR_SLICES=${SLICES:-64} STRAGGLAR_TIMEOUT_MS=30000
 N=${N:-8}
-timeout 600 python -m torch.distributed.run --standalone --nproc-per-node $N bench.py --gpus $N --steps 5 --warmup 3 \
+timeout 600 python -m torch.distributed.run --standalone --local-addr 127.0.0.1 --nproc-per-node $N bench.py --gpus $N --steps 5 --warmup 3 \
    --workload ${WL:-config2} > gpurun_out/mps_multi_$N.json 2> gpurun_out/mps_multi_$N.err
 echo "bench rc=$?"
 cat gpurun_out/mps_multi_$N.json
