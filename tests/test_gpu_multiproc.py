@@ -32,6 +32,7 @@ def _port():
     (8, 3, 500001, "float32", "tma"),    # the full n = 8 schedule across 8 processes
     (4, 1, 30001, "float32", "tma+ll"),  # LL protocol forced on, system scope
     (8, 5, 70001, "bfloat16", "lsu+ll"), # LL protocol forced on, 8 processes
+    (4, 3, 400003, "float32", "tma+sub"),  # several slices per CTA (sub-slices), system scope
 ])
 def test_multiprocess_ipc(world, sigma, count, dtype, mover):
     if not torch.cuda.is_available():
@@ -42,6 +43,9 @@ def test_multiprocess_ipc(world, sigma, count, dtype, mover):
     env = dict(os.environ, STRAGGLAR_MOVER=mover.split("+")[0])
     if mover.endswith("+ll"):
         env["STRAGGLAR_LL_MAX_CHUNK"] = "262144"
+    if mover.endswith("+sub"):
+        env["STRAGGLAR_SLICE_BYTES"] = "1024"       # 8 CTAs per rank (mp_worker), ~4 KB slices: 16 per CTA
+        env["STRAGGLAR_SUBSLICE_BYTES"] = "4096"
     r = subprocess.run([sys.executable, os.path.join(HERE, "mp_worker.py"), str(world), str(sigma), str(count), dtype,
                         str(_port())], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
