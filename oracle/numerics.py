@@ -249,6 +249,55 @@ def ring_allreduce(inputs: Sequence[np.ndarray], dtype: str) -> List[np.ndarray]
     return bufs
 
 
+def rhd_allreduce(inputs: Sequence[np.ndarray], dtype: str) -> List[np.ndarray]:
+    """Replay of the RHD schedule (oracle.schedule.generate_rhd)
+    over physical ranks with n chunks (the Ring's partition); partials travel
+    in the buffer dtype, so bf16 is rounded after every pairwise add."""
+    n = len(inputs)
+    bufs = [np.array(x, copy=True) for x in inputs]
+    if n == 1:
+        return bufs
+    replay_schedule(bufs, S.generate_rhd(n), list(range(n)), dtype, chunk_bounds(bufs[0].size, n, dtype))
+    return bufs
+
+
+def plain_rhd_allreduce(inputs: Sequence[np.ndarray], dtype: str) -> np.ndarray:
+    """Definition of the RHD result, written elementwise with no chunks or
+    rounds: a butterfly of pairwise sums, level k (k = 0..log n - 1) adding the
+    values of ranks i and i XOR n/2^(k+1) (halves with one partner,
+    then quarters with the next), one rounding per level.  Every rank ends with
+    the same bits (each add is commutative)."""
+    n = len(inputs)
+    v = [np.array(x, copy=True) for x in inputs]
+    d = n // 2
+    while d >= 1:
+        v = [add(v[i], v[i ^ d], dtype) for i in range(n)]
+        d //= 2
+    return v[0]
+
+
+def broadcast_allreduce(inputs: Sequence[np.ndarray], sigma_phys: int, dtype: str) -> List[np.ndarray]:
+    """Straggler-aware Broadcast baseline, step by step.
+
+    Precondition: the non-stragglers complete an AllReduce during
+    the delay.  Its summation order is unstated; reading: the canonical order
+    of StragglAR's Phase A (ascending physical rank, fp32 accumulation, bf16
+    rounded once), applied to the whole buffer.  Then the schedule of
+    ``schedule.generate_broadcast`` is replayed (the straggler's exchange adds
+    x_sigma once, the log n - 1 doubling rounds copy)."""
+    n = len(inputs)
+    bufs = [np.array(x, copy=True) for x in inputs]
+    if n == 1:
+        return bufs
+    ns = [p for p in range(n) if p != sigma_phys]
+    part = _canonical_partial(inputs, ns, dtype)
+    for p in ns:
+        bufs[p][:] = part
+    phys = logical_to_physical(n, sigma_phys)
+    replay_schedule(bufs, S.generate_broadcast(n), phys, dtype, chunk_bounds(bufs[0].size, n - 1, dtype))
+    return bufs
+
+
 def plain_ring_allreduce(inputs: Sequence[np.ndarray], dtype: str) -> np.ndarray:
     """Definition of the Ring result: chunk k is accumulated in rotation order
     x_k, x_{k+1}, ..., x_{k+n-1} (mod n) with one rounding per hop."""

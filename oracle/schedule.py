@@ -313,6 +313,85 @@ def generate_ring(n: int) -> Schedule:
 
 
 # --------------------------------------------------------------------------
+# Baseline: recursive halving/doubling ("Butterfly")
+# --------------------------------------------------------------------------
+def generate_rhd(n: int) -> Schedule:
+    """RHD AllReduce on n chunks (one per rank), 2 log n rounds.
+
+    P:364-365: "the buffer is first divided in 1/2 with one partner, then in
+    1/4 with another partner, etc. to achieve a ReduceScatter.  Then, a
+    mirror-image AllGather completes."  Reading (distance halving, the
+    order is not stated): in ReduceScatter round t (t = 0..L-1) rank i pairs
+    with i XOR n/2^(t+1); both hold the same block of n/2^t chunks; i keeps the
+    lower half if that bit of i is 0, else the upper half, and receives the
+    partner's copy of the half it keeps (Reduce).  After L rounds rank i holds
+    chunk i fully reduced.  AllGather round L+u (u = 0..L-1) mirrors
+    ReduceScatter round L-1-u: partners exchange their fully reduced blocks of
+    n/2^(L-u) chunks (Replace).
+    """
+    L = log2_exact(n)
+    s = Schedule("rhd", n, -1, n)
+    blocks = {i: (0, n) for i in range(n)}            # (first chunk, #chunks) each rank works on
+    for t in range(L):
+        d = n >> (t + 1)
+        rnd = []
+        new = {}
+        for i in range(n):
+            lo, m = blocks[i]
+            keep = lo if (i & d) == 0 else lo + m // 2
+            new[i] = (keep, m // 2)
+            rnd += [Transfer(i ^ d, i, c, REDUCE) for c in range(keep, keep + m // 2)]
+        blocks = new
+        s.rounds.append(rnd)
+    for u in range(L):
+        d = n >> (L - u)
+        rnd = []
+        new = {}
+        for i in range(n):
+            lo, m = blocks[i]                         # i's fully reduced block
+            p = i ^ d
+            plo, _ = blocks[p]
+            rnd += [Transfer(p, i, c, REPLACE) for c in range(plo, plo + m)]
+            new[i] = (min(lo, plo), 2 * m)
+        blocks = new
+        s.rounds.append(rnd)
+    return s
+
+
+# --------------------------------------------------------------------------
+# Baseline: straggler-aware Broadcast (P:368-372)
+# --------------------------------------------------------------------------
+def generate_broadcast(n: int) -> Schedule:
+    """Broadcast AllReduce, logical ranks (straggler sigma = n-1), n-1 chunks.
+
+    P:369-372: the non-stragglers complete an AllReduce during the delay
+    (the precondition, ``initial_state_broadcast``); "the straggler ...
+    exchanges its entire buffer with any other rank to fully reduce the
+    entire buffer and then initiates a broadcast with log n rounds and s bytes
+    per round".  Readings: the exchange partner is logical rank 0, and the
+    exchange is round 0 of the log n (T_Bcast = log n alpha + log n s beta,
+    P:373, counts log n messages of s bytes).  Round r >= 1: the ranks holding
+    the full sum, ascending, are zipped with the ranks that do not, ascending;
+    each pair copies the whole buffer (every chunk, Replace).  Holders double
+    per round: 2, 4, ..., n after ceil(log2 n) rounds.
+    """
+    if n < 2:
+        raise ScheduleError("broadcast needs n >= 2")
+    sigma = n - 1
+    s = Schedule("broadcast", n, sigma, n - 1)
+    s.rounds.append([Transfer(sigma, 0, c, REDUCE) for c in range(n - 1)] +
+                    [Transfer(0, sigma, c, REDUCE) for c in range(n - 1)])
+    holders = {0, sigma}
+    while len(holders) < n:
+        H = sorted(holders)
+        Q = [q for q in range(n) if q not in holders]
+        pairs = list(zip(H, Q))
+        s.rounds.append([Transfer(h, q, c, REPLACE) for h, q in pairs for c in range(n - 1)])
+        holders |= {q for _, q in pairs}
+    return s
+
+
+# --------------------------------------------------------------------------
 # Contributor-set verifier (S:52-98)
 # --------------------------------------------------------------------------
 State = Dict[Tuple[int, int], FrozenSet[int]]
@@ -335,6 +414,14 @@ def initial_state_uniform(n: int, num_chunks: int) -> State:
     return {(h, c): frozenset([h]) for h in range(n) for c in range(num_chunks)}
 
 
+def initial_state_broadcast(n: int) -> State:
+    """Broadcast precondition: the non-stragglers completed an
+    AllReduce among themselves; the straggler holds only its own data."""
+    sigma = n - 1
+    ns = frozenset(range(n - 1))
+    return {(h, c): (frozenset([h]) if h == sigma else ns) for h in range(n) for c in range(n - 1)}
+
+
 @dataclass
 class Report:
     valid: bool
@@ -345,13 +432,16 @@ class Report:
 
 
 def apply_round(state: State, rnd: List[Transfer], n: int, r: int = 0,
-                violations: Optional[list] = None, matching: bool = True) -> State:
+                violations: Optional[list] = None, matching: bool = True,
+                one_chunk: bool = True) -> State:
     """snapshot semantics; Reduce = disjoint union; Replace = superset copy.
 
     Single port: every rank sends <= 1 and receives <= 1 chunk per
     round.  With ``matching`` (StragglAR, P:204 / S:46) every rank also talks to
     a single partner; Ring sends to i+1 while receiving from i-1, so it is
-    checked with ``matching=False``.
+    checked with ``matching=False``.  RHD and Broadcast send a block of several
+    chunks to their single partner per round: ``one_chunk=False``
+    keeps the one-partner rule and lifts the one-chunk rule.
     """
     viol = violations if violations is not None else []
     partner: Dict[int, int] = {}
@@ -366,7 +456,7 @@ def apply_round(state: State, rnd: List[Transfer], n: int, r: int = 0,
         sends[t.src] = sends.get(t.src, 0) + 1
         recvs[t.dst] = recvs.get(t.dst, 0) + 1
     for k, v in list(sends.items()) + list(recvs.items()):
-        if v > 1:
+        if v > 1 and one_chunk:
             viol.append((r, f"port violation: rank {k} moves {v} chunks one way"))
     payload = [(t, state[(t.src, t.chunk)]) for t in rnd]   # snapshot first
     new = dict(state)
@@ -392,12 +482,15 @@ def verify_schedule(s: Schedule) -> Report:
     violations and every cell ends with contributors {0..n-1}."""
     if s.algorithm == "stragglar":
         st = initial_state_stragglar(s.n)
+    elif s.algorithm == "broadcast":
+        st = initial_state_broadcast(s.n)
     else:
         st = initial_state_uniform(s.n, s.num_chunks)
     viol: List[Tuple[int, str]] = []
     beta = Fraction(0)
+    blocks = s.algorithm in ("rhd", "broadcast")
     for r, rnd in enumerate(s.rounds):
-        st = apply_round(st, rnd, s.n, r, viol, matching=(s.algorithm == "stragglar"))
+        st = apply_round(st, rnd, s.n, r, viol, matching=(s.algorithm != "ring"), one_chunk=not blocks)
         per_port: Dict[Tuple[int, str], int] = {}
         for t in rnd:
             per_port[(t.src, "out")] = per_port.get((t.src, "out"), 0) + 1
