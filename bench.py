@@ -270,6 +270,39 @@ def bench_team(args):
     torch.cuda.synchronize()
     T_ring = statistics.mean(e0.elapsed_time(e1) * 1e3 for e0, e1 in rs)
 
+    # NEXT N3 baselines on the same buffers
+    T_rhd = None
+    if world & (world - 1) == 0:
+        for _ in range(args.warmup):
+            S.stragglar_team_allreduce_rhd(ring)
+        torch.cuda.synchronize()
+        rr = [(ev(), ev()) for _ in range(args.steps)]
+        torch.cuda._sleep(4_000_000)
+        for e0, e1 in rr:
+            e0.record()
+            S.stragglar_team_allreduce_rhd(ring)
+            e1.record()
+        torch.cuda.synchronize()
+        T_rhd = statistics.mean(e0.elapsed_time(e1) * 1e3 for e0, e1 in rr)
+
+    def bcast_step(evs):   # precondition hidden in the delay, then the timed completion
+        S.stragglar_team_bcast_precondition(ring)
+        S.stragglar_team_inject_delay(D_ns)
+        evs[0].record()
+        S.stragglar_team_bcast_complete(ring)
+        evs[1].record()
+
+    for _ in range(args.warmup):
+        bcast_step([ev(), ev()])
+    bsteps = [[ev(), ev()] for _ in range(args.steps)]
+    torch.cuda._sleep(4_000_000)
+    for evs in bsteps:
+        bcast_step(evs)
+    torch.cuda.synchronize()
+    T_bcast = statistics.mean(e[0].elapsed_time(e[1]) * 1e3 for e in bsteps)
+    if S.stragglar_team_check_error():
+        raise RuntimeError("device watchdog fired in a baseline")
+
     # end to end through the C ABI from pinned host buffers (H2D + allreduce + D2H)
     host = [bufs[p].cpu().pin_memory() for p in range(world)]
     S.stragglar_team_allreduce_host(host, host, bufs, stream)          # warm-up
@@ -348,6 +381,17 @@ def bench_team(args):
             "hbm_GBps": round((world + 2) * (world - 1) * chunk_bytes(count, world - 1, esize) / (T_direct * 1e-6) / 1e9, 1),
             "speedup_vs_schedule_post": round(T_post / T_direct, 3),
         },
+        "baselines_N3": {
+            "what": "NEXT row N3: the paper's other baselines (P:363-373), hand-written on the same transport",
+            "rhd_us": round(T_rhd, 2) if T_rhd else None,
+            "rhd_hbm_GBps": round(bytes_ring / (T_rhd * 1e-6) / 1e9, 1) if T_rhd else None,
+            "speedup_vs_rhd_post": round(T_rhd / T_post, 3) if T_rhd else None,
+            "bcast_post_us": round(T_bcast, 2),
+            "bcast_hbm_GBps": round(2 * world * S_bytes / (T_bcast * 1e-6) / 1e9, 1),
+            "speedup_vs_bcast_post": round(T_bcast / T_post, 3),
+            "note": "team mode: every link is HBM, so an algorithm costs its total bytes (RHD 5(n-1)S like the "
+                    "Ring; Broadcast completion 2nS like StragglAR's Phase B 2n(n-1)C), not its busiest port",
+        },
         "phaseA_hbm_GBps": round(bytes_A / (T_A * 1e-6) / 1e9, 1),
         "ring_hbm_GBps": round(bytes_ring / (T_ring * 1e-6) / 1e9, 1),
         "roofline": {"bound": "hbm", "kernel": "k_phase<..., KIND=1> (Phase B, Algorithm 1 schedule)", "achieved": round(achieved, 1),
@@ -399,8 +443,11 @@ def bench_multi(args):
     buf = to_tensor(make_input(count, dtype, rank, config=2), dtype).cuda()
     ring = buf.clone()
     nccl_buf = buf.clone()
+    rhd_buf, bc_buf = buf.clone(), buf.clone()
     comm.register(buf)
     comm.register(ring)
+    comm.register(rhd_buf)
+    comm.register(bc_buf)
     C = chunk_bytes(count, world - 1, esize)
     T_A_model = (world - 2) * C / (NVLINK_PEER_MEASURED * 1e9) * 1e6
     D_ns = int((1.5 * T_A_model + 20.0) * 1e3) if args.delay_us is None else int(args.delay_us * 1e3)
@@ -420,7 +467,10 @@ def bench_multi(args):
             res.append((e0, ea, e1))
         return res
 
-    algos = {"stragglar": lambda: comm.allreduce(buf), "ring": lambda: comm.allreduce_ring(ring)}
+    algos = {"stragglar": lambda: comm.allreduce(buf), "ring": lambda: comm.allreduce_ring(ring),
+             "bcast": lambda: comm.allreduce_bcast(bc_buf)}     # NEXT N3
+    if world & (world - 1) == 0:
+        algos["rhd"] = lambda: comm.allreduce_rhd(rhd_buf)   # NEXT N3
     if not shared:
         algos["nccl"] = lambda: dist.all_reduce(nccl_buf)
     results = {}
@@ -495,6 +545,10 @@ def bench_multi(args):
             "nccl_us": round(results["nccl"][0] - results["nccl"][1], 2) if "nccl" in results else None,
             "speedup_vs_ring_post": round((results["ring"][0] - results["ring"][1]) / T_post, 3),
             "speedup_vs_nccl_post": round((results["nccl"][0] - results["nccl"][1]) / T_post, 3) if "nccl" in results else None,
+            "rhd_us": round(results["rhd"][0] - results["rhd"][1], 2) if "rhd" in results else None,
+            "bcast_us": round(results["bcast"][0] - results["bcast"][1], 2),
+            "speedup_vs_rhd_post": round((results["rhd"][0] - results["rhd"][1]) / T_post, 3) if "rhd" in results else None,
+            "speedup_vs_bcast_post": round((results["bcast"][0] - results["bcast"][1]) / T_post, 3),
             "shared_device_test": shared,
             "roofline": roof,
             "cpu_baseline": None,

@@ -126,6 +126,27 @@ int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* s
  * (n+log2 n-2)/(n-1)*S, one round instead of n+log2 n-2.  Result identical
  * to stragglar_allreduce, bit for bit. */
 int stragglar_allreduce_direct(void* buf, size_t count, int dtype, int op, void* stream);
+/* NEXT row N3: the paper's other baselines,
+ * in-house on the same transport, in place, collective, same argument rules
+ * and errors as stragglar_allreduce.
+ * RHD — recursive halving/doubling ("Butterfly"): n chunks (the
+ *   Ring's partition); log2 n ReduceScatter steps in which rank j pairs with
+ *   j XOR n/2^(t+1) and adds the partner's copy of the half it keeps, then
+ *   log2 n mirror-image AllGather steps; bf16 partials rounded per step.
+ *   UNSUPPORTED unless world is a power of two.
+ * Broadcast — straggler-aware: the non-stragglers AllReduce
+ *   among themselves (canonical order of Phase A, then every non-straggler
+ *   copies the other partials), the straggler exchanges its entire buffer
+ *   with logical rank 0 (one add, the same bits as stragglar_allreduce), and
+ *   the full sum is copied along a doubling tree (stragglar_broadcast_tree),
+ *   s bytes per copy, ceil(log2 n) rounds in all. */
+int stragglar_allreduce_rhd(void* buf, size_t count, int dtype, int op, void* stream);
+int stragglar_allreduce_bcast(void* buf, size_t count, int dtype, int op, void* stream);
+/* The Broadcast baseline's tree in LOGICAL ranks (straggler = world-1):
+ * sender[q] = the rank q receives the full sum from (-1 for ranks 0 and
+ * world-1, which hold it after the exchange), round[q] = that copy's round
+ * (0 for the two holders).  Arrays of `world` ints; world in [2, 64]. */
+int stragglar_broadcast_tree(int world, int* sender, int* round);
 /* End to end from host memory (collective): host_in (count elements) is
  * copied into the registered device buffer `buf`, AllReduced with
  * stragglar_allreduce, and the result copied to host_out (may equal
@@ -149,7 +170,7 @@ int stragglar_check_error(int* code);
  * returning where the first failing spin-wait was: (kind << 8) | index with
  * kind 0x1 Phase-A arrival, 0x2 exchange (non-straggler side), 0x3 exchange
  * (straggler side), 0x4 copy, 0x5 completion, 0x6/0x7 ring, 0x8 barrier,
- * 0x9/0xA direct completion. */
+ * 0x9/0xA direct completion, 0xC/0xD Broadcast baseline, 0xE RHD. */
 int stragglar_check_error_where(int team, int* code, uint32_t* where);
 /* Phase breakdown of this rank's last stragglar_allreduce(_direct) call, from
  * %globaltimer stamps inside the kernel (this GPU's clock): *t_a_us = kernel
@@ -174,6 +195,15 @@ int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, in
  * and the whole direct-completion AllReduce. */
 int stragglar_team_complete_direct(void* const* bufs, size_t count, int dtype, int op, void* stream);
 int stragglar_team_allreduce_direct(void* const* bufs, size_t count, int dtype, int op, void* stream);
+/* NEXT N3 baselines on the team (see stragglar_allreduce_rhd / _bcast).
+ * bcast_precondition = the non-straggler AllReduce (n-1 ranks, the part the
+ * paper assumes hidden in the delay); bcast_complete = the
+ * straggler's exchange + doubling copies (requires the precondition on the
+ * same buffers first); allreduce_bcast = both in one launch. */
+int stragglar_team_allreduce_rhd(void* const* bufs, size_t count, int dtype, int op, void* stream);
+int stragglar_team_bcast_precondition(void* const* bufs, size_t count, int dtype, int op, void* stream);
+int stragglar_team_bcast_complete(void* const* bufs, size_t count, int dtype, int op, void* stream);
+int stragglar_team_allreduce_bcast(void* const* bufs, size_t count, int dtype, int op, void* stream);
 /* Measurement only: the whole AllReduce in one launch (Phase A + B) with the
  * straggler's CTAs arriving delay_ns after the launch, so the straggler's
  * exchanges can overlap the non-stragglers' Phase A tail slice by slice, as

@@ -29,7 +29,8 @@ using namespace stragglar;
 
 namespace {
 
-enum { K_RS = 0, K_COMPLETE = 1, K_RING = 2, K_DIRECT = 3, K_FUSED = 4, K_FUSED_DIRECT = 5 };
+enum { K_RS = 0, K_COMPLETE = 1, K_RING = 2, K_DIRECT = 3, K_FUSED = 4, K_FUSED_DIRECT = 5,
+       K_BCAST_A = 6, K_BCAST_B = 7, K_BCAST = 8, K_RHD = 9, K_NUM = 10 };
 constexpr int kDefaultMover = MOVER_TMA;   // measured faster (profiles/r01)
 
 std::atomic<uint64_t> g_launches{0};
@@ -54,6 +55,7 @@ struct Comm {
   int sub = 1;                 // slices per CTA at most (STRAGGLAR_SUBSLICES)
   uint64_t sub_bytes = 0;      // target slice size on large messages (STRAGGLAR_SUBSLICE_BYTES)
   bool rs_pending = false;     // team: a Phase A awaits its Phase B (same call epoch)
+  bool bc_pending = false;     // team: a Broadcast-baseline precondition awaits its completion
   uint32_t* flags = nullptr;   // own flag array(s) + LL area(s); team: world of them back to back
   uint32_t* peer_flags[kMaxWorld] = {nullptr};
   uint64_t* peer_ll[kMaxWorld] = {nullptr};
@@ -118,8 +120,9 @@ int resident_ctas(int world, int mover, int* sm_count) {
   int sms = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
   int best = 1 << 30;
-  for (int which = 0; which < 6; ++which)
+  for (int which = 0; which < K_NUM; ++which)
     for (int dt = 0; dt < 3; ++dt) {
+      if (!select_kernel(which, dt, world, mover)) continue;   // RHD: powers of two only
       int b = 0;
       if (occupancy_blocks_per_sm(which, dt, world, mover, &b) != cudaSuccess) return -1;
       best = b < best ? b : best;
@@ -162,6 +165,7 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   c.sigma = sigma;
   c.team = team;
   c.rs_pending = false;
+  c.bc_pending = false;
   c.timeout_ns = env_u64("STRAGGLAR_TIMEOUT_MS", 10000) * 1000000ull;
   c.slice_bytes = env_u64("STRAGGLAR_SLICE_BYTES", 16384);
   c.sub = (int)env_u64("STRAGGLAR_SUBSLICES", kMaxSub);
@@ -251,6 +255,7 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
   P.world = c.world;
   P.sigma = c.sigma;
   P.G = c.G;
+  P.fstride = c.G * kMaxSub;
   P.last_kernel = last_kernel ? 1 : 0;
   P.count = count;
   P.esize = esize_of(dtype);
@@ -268,10 +273,13 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
   }
   P.sys_scope = c.sys_scope;
   P.state = c.state;
+  P.bc_partner = c.progs.bc_partner;
   for (int p = 0; p < c.world; ++p) {
     P.flags[p] = c.peer_flags[p];
     P.ll[p] = c.peer_ll[p];
     P.logical_of_phys[p] = c.progs.logical_of_phys[p];
+    P.bc_sender[p] = c.progs.bc_sender[p];
+    P.bc_round[p] = c.progs.bc_round[p];
     P.nops[p] = c.progs.nops[p];
     for (int k = 0; k < c.progs.nops[p]; ++k) P.ops[p][k] = c.progs.ops[p][k];
   }
@@ -630,6 +638,42 @@ int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* s
   return launch(K_RING, dtype, P, P.G, stream);
 }
 
+int stragglar_allreduce_rhd(void* buf, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (c.world & (c.world - 1)) return STRAGGLAR_ERR_UNSUPPORTED;   // RHD needs a power of two
+  int st = check_args(buf, count, dtype, op);
+  if (st || count == 0) return st;
+  LaunchPlan P;
+  if ((st = proc_plan(buf, count, dtype, &P))) return st;
+  P.ce = chunk_elems(count, c.world, P.esize);
+  P.nchunks = c.world;
+  slices_for(c, P.ce * P.esize, &P.G, &P.sub);
+  return launch(K_RHD, dtype, P, P.G, stream);
+}
+
+int stragglar_allreduce_bcast(void* buf, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  int st = check_args(buf, count, dtype, op);
+  if (st || count == 0) return st;
+  LaunchPlan P;
+  if ((st = proc_plan(buf, count, dtype, &P))) return st;
+  return launch(K_BCAST, dtype, P, P.G, stream);
+}
+
+int stragglar_broadcast_tree(int world, int* sender, int* round) {
+  if (!sender || !round) return STRAGGLAR_ERR_INVALID_ARG;
+  try {
+    broadcast_tree(world, sender, round);
+  } catch (const std::exception&) {
+    return STRAGGLAR_ERR_UNSUPPORTED;
+  }
+  return STRAGGLAR_OK;
+}
+
 int stragglar_select(int world, double bytes, double delay_s, double alpha_s, double beta, int* use_stragglar,
                      double* critical_delay_s) {
   if (world < 2 || world > 64 || (world & 1)) return STRAGGLAR_ERR_UNSUPPORTED;
@@ -748,6 +792,7 @@ int stragglar_team_reduce_scatter(void* const* bufs, size_t count, int dtype, in
   std::lock_guard<std::mutex> lk(g_mu);
   int st = team_check(bufs, count, dtype, op);
   if (st || count == 0) return st;
+  if (g_team.rs_pending || g_team.bc_pending) return STRAGGLAR_ERR_INVALID_ARG;
   if ((st = team_rs(bufs, count, dtype, stream))) return st;
   g_team.rs_pending = true;
   return STRAGGLAR_OK;
@@ -766,7 +811,7 @@ int stragglar_team_allreduce(void* const* bufs, size_t count, int dtype, int op,
   std::lock_guard<std::mutex> lk(g_mu);
   int st = team_check(bufs, count, dtype, op);
   if (st || count == 0) return st;
-  if (g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;   // finish the pending Phase A first
+  if (g_team.rs_pending || g_team.bc_pending) return STRAGGLAR_ERR_INVALID_ARG;   // finish the pending Phase A first
   return team_b(bufs, count, dtype, stream, K_FUSED);        // Phase A + B in one launch
 }
 
@@ -783,7 +828,7 @@ int stragglar_team_allreduce_direct(void* const* bufs, size_t count, int dtype, 
   std::lock_guard<std::mutex> lk(g_mu);
   int st = team_check(bufs, count, dtype, op);
   if (st || count == 0) return st;
-  if (g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;
+  if (g_team.rs_pending || g_team.bc_pending) return STRAGGLAR_ERR_INVALID_ARG;
   return team_b(bufs, count, dtype, stream, K_FUSED_DIRECT);
 }
 
@@ -792,7 +837,7 @@ int stragglar_team_allreduce_delayed(void* const* bufs, size_t count, int dtype,
   std::lock_guard<std::mutex> lk(g_mu);
   int st = team_check(bufs, count, dtype, op);
   if (st || count == 0) return st;
-  if (g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;
+  if (g_team.rs_pending || g_team.bc_pending) return STRAGGLAR_ERR_INVALID_ARG;
   return team_b(bufs, count, dtype, stream, K_FUSED, delay_ns);
 }
 
@@ -801,7 +846,7 @@ int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, in
   int st = team_check(bufs, count, dtype, op);
   if (st || count == 0) return st;
   Comm& c = g_team;
-  if (c.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;   // a Phase A awaits its Phase B
+  if (c.rs_pending || c.bc_pending) return STRAGGLAR_ERR_INVALID_ARG;   // a Phase A awaits its Phase B
   LaunchPlan P = base_plan(c, count, dtype, true);
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
@@ -812,6 +857,62 @@ int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, in
   }
   P.nlocal = c.world;
   return launch(K_RING, dtype, P, c.world * P.G, stream);
+}
+
+int stragglar_team_allreduce_rhd(void* const* bufs, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int st = team_check(bufs, count, dtype, op);
+  if (st || count == 0) return st;
+  Comm& c = g_team;
+  if (c.world & (c.world - 1)) return STRAGGLAR_ERR_UNSUPPORTED;
+  if (c.rs_pending || c.bc_pending) return STRAGGLAR_ERR_INVALID_ARG;
+  LaunchPlan P = base_plan(c, count, dtype, true);
+  P.ce = chunk_elems(count, c.world, P.esize);
+  P.nchunks = c.world;
+  slices_for(c, P.ce * P.esize, &P.G, &P.sub);
+  for (int p = 0; p < c.world; ++p) {
+    P.buf[p] = (char*)bufs[p];
+    P.local_rank[p] = p;
+  }
+  P.nlocal = c.world;
+  return launch(K_RHD, dtype, P, c.world * P.G, stream);
+}
+
+// Broadcast baseline in team mode: the precondition (non-straggler AllReduce,
+// launched for the n-1 non-stragglers only), the completion (exchange +
+// doubling copies, all ranks) or both in one launch.
+int stragglar_team_bcast_precondition(void* const* bufs, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int st = team_check(bufs, count, dtype, op);
+  if (st || count == 0) return st;
+  Comm& c = g_team;
+  if (c.rs_pending || c.bc_pending) return STRAGGLAR_ERR_INVALID_ARG;
+  LaunchPlan P = base_plan(c, count, dtype, false);
+  for (int p = 0; p < c.world; ++p) P.buf[p] = (char*)bufs[p];
+  int k = 0;
+  for (int p = 0; p < c.world; ++p)
+    if (p != c.sigma) P.local_rank[k++] = p;
+  P.nlocal = k;
+  if ((st = launch(K_BCAST_A, dtype, P, k * P.G, stream))) return st;
+  c.bc_pending = true;
+  return STRAGGLAR_OK;
+}
+
+int stragglar_team_bcast_complete(void* const* bufs, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int st = team_check(bufs, count, dtype, op);
+  if (st || count == 0) return st;
+  if (!g_team.bc_pending) return STRAGGLAR_ERR_INVALID_ARG;   // needs its precondition
+  g_team.bc_pending = false;
+  return team_b(bufs, count, dtype, stream, K_BCAST_B);
+}
+
+int stragglar_team_allreduce_bcast(void* const* bufs, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  int st = team_check(bufs, count, dtype, op);
+  if (st || count == 0) return st;
+  if (g_team.rs_pending || g_team.bc_pending) return STRAGGLAR_ERR_INVALID_ARG;
+  return team_b(bufs, count, dtype, stream, K_BCAST);
 }
 
 int stragglar_team_inject_delay(uint64_t ns, void* stream) {

@@ -24,9 +24,9 @@ __global__ void k_barrier(const __grid_constant__ LaunchPlan P) {
   const int me = P.local_rank[0];
   const uint32_t ep = call_epoch(P);
   if (threadIdx.x < P.world && (int)threadIdx.x != me)
-    st_release(flag_at(P.flags[threadIdx.x], SLOT_BARRIER + me, P.G * P.sub, 0), ep, P.sys_scope);
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_BARRIER + me, P.fstride, 0), ep, P.sys_scope);
   if (threadIdx.x < P.world && (int)threadIdx.x != me)
-    spin_wait(flag_at(P.flags[me], SLOT_BARRIER + threadIdx.x, P.G * P.sub, 0), ep, P, 0x800 | threadIdx.x);
+    spin_wait(flag_at(P.flags[me], SLOT_BARRIER + threadIdx.x, P.fstride, 0), ep, P, 0x800 | threadIdx.x);
   finish_call(P);
 }
 
@@ -40,7 +40,7 @@ void* select_kernel(int which, int dtype, int world, int mover) {
   }
 }
 
-int dynamic_smem(int which, int mover) { return (which <= 5 && mover == MOVER_TMA) ? kTmaSmem : 0; }
+int dynamic_smem(int which, int mover) { return (which <= 9 && mover == MOVER_TMA) ? kTmaSmem : 0; }
 
 cudaError_t launch_plan_kernel(int which, int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream) {
   void* fn = select_kernel(which, dtype, P.world, P.mover);

@@ -13,7 +13,9 @@
 //     KIND 3  Phase B as a one-round direct completion (NEXT N1(ii)). [direct_body]
 //     KIND 4  Phase A then Phase B (schedule) in one launch (single-call API).
 //     KIND 5  Phase A then direct completion in one launch.
+//     KIND 6-8 the straggler-aware Broadcast baseline (NEXT N3).
 //   k_ring            hand-written Ring baseline, pull-based.
+//   k_rhd             recursive halving/doubling baseline (NEXT N3).
 //   k_delay           the paper's idle kernel on %globaltimer.
 //   k_barrier         device barrier among ranks (bench start line).
 //
@@ -82,8 +84,12 @@ __device__ __forceinline__ void finish_call(const LaunchPlan& P) {
   }
 }
 
-__device__ __forceinline__ uint32_t* flag_at(uint32_t* base, int slot, int G, int s) {
-  return base + (size_t)slot * G + s;
+// Slot k of a rank's flag array spans [k * stride, (k+1) * stride) with a
+// stride fixed per communicator (LaunchPlan::fstride = G_max * kMaxSub), not
+// per call: a fast peer's writes for its NEXT call (a different slice layout)
+// then land in the same slot as in this call, never in another slot's range.
+__device__ __forceinline__ uint32_t* flag_at(uint32_t* base, int slot, int stride, int s) {
+  return base + (size_t)slot * stride + s;
 }
 
 // ---------------------------------------------------------------- ranges
@@ -508,17 +514,19 @@ __device__ void rs_slice(const LaunchPlan& P, const char* const (&src)[W - 1], c
 }
 
 // Phase A body for non-straggler `me`, CTA slot s (slices s*sub .. s*sub+sub-1).
-template <int DT, int W, int MV>
+// BC (Broadcast baseline): the partial is announced to every other
+// non-straggler (they copy it in ag_body) instead of to the straggler.
+template <int DT, int W, int MV, bool BC = false>
 __device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
   const int NV = P.G * P.sub;   // slices per chunk (flag stride)
   if (blockIdx.x == 0 && threadIdx.x == 0) P.state->t_rs_start = globaltimer();
   // barrier (1) among the non-stragglers, per CTA slot
   if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
-    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, NV, s), ep, P.sys_scope);
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, P.fstride, s), ep, P.sys_scope);
   // one waiting thread per peer: the acquire loads overlap instead of queueing
   int ok = 1;
   if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
-    ok = spin_wait(flag_at(P.flags[me], SLOT_ARRIVE + threadIdx.x, NV, s), ep, P, 0x100 | threadIdx.x);
+    ok = spin_wait(flag_at(P.flags[me], SLOT_ARRIVE + threadIdx.x, P.fstride, s), ep, P, 0x100 | threadIdx.x);
   if (!__syncthreads_and(ok)) return;
 
   const int g = P.logical_of_phys[me];  // owned chunk
@@ -541,9 +549,133 @@ __device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t
         rs_slice<DT, W>(P, src, P.buf[me], r.lo * P.esize, r.hi * P.esize);
       }
     }
-    // "partial ready" for the straggler's half of the exchange
-    cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, NV, v), ep, P.sys_scope);
+    if constexpr (BC) {
+      __syncthreads();
+      if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
+        st_release(flag_at(P.flags[threadIdx.x], SLOT_RSDONE + g, P.fstride, v), ep, P.sys_scope);
+    } else {
+      // "partial ready" for the straggler's half of the exchange
+      cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, P.fstride, v), ep, P.sys_scope);
+    }
   }
+}
+
+// ---------------------------------------------------------------- Broadcast baseline (NEXT N3)
+// Straggler-aware Broadcast.  Precondition: the non-stragglers
+// complete an AllReduce during the delay = rs_body<BC> (canonical partials)
+// then ag_body (every non-straggler copies the other owners' partials).  Then
+// bcast_body: the straggler exchanges its entire buffer with its partner
+// (logical rank 0; half-split and fused with the add as in B1), and the full
+// sum is copied on along the doubling tree of RankPrograms::bc_sender, s
+// bytes per copy.  CTA s covers the union of its `sub` slices of every chunk.
+
+// Bytes [a, b) of chunk c covered by CTA slot s.
+__device__ __forceinline__ void cta_chunk_bytes(const LaunchPlan& P, int c, int s, uint64_t& a, uint64_t& b) {
+  const int NV = P.G * P.sub, V = 16 / P.esize;
+  const Range cr = chunk_range(P, c);
+  a = slice_of(cr.lo, cr.hi, s * P.sub, NV, V).lo * P.esize;
+  b = slice_of(cr.lo, cr.hi, s * P.sub + P.sub - 1, NV, V).hi * P.esize;
+}
+
+template <int MV>
+__device__ __forceinline__ void move_bytes(Pipe& pipe, char* dst, const char* src, uint64_t a, uint64_t b) {
+  const uint64_t body = (b - a) / 16 * 16;
+  if constexpr (MV == MOVER_TMA)
+    tma_copy(pipe, dst + a, src + a, body);
+  else
+    copy_vecs(dst + a, src + a, body / 16);
+  copy_tail(dst + a + body, src + a + body, (int)((b - a) % 16));
+}
+
+// d0 = d1 = x (+) y over bytes [a, b)
+template <int DT, int MV>
+__device__ __forceinline__ void add_bytes(const LaunchPlan& P, Pipe& pipe, char* d0, char* d1, const char* x,
+                                          const char* y, uint64_t a, uint64_t b) {
+  const uint64_t body = (b - a) / 16 * 16;
+  char* e1 = d1 ? d1 + a : nullptr;   // d1 == nullptr: one destination
+  if constexpr (MV == MOVER_TMA)
+    tma_add2<DT>(pipe, d0 + a, e1, x + a, y + a, body);
+  else
+    add2_vecs<DT>(d0 + a, e1, x + a, y + a, body / 16);
+  add2_tail<DT>(d0 + a + body, e1 ? e1 + body : nullptr, x + a + body, y + a + body, (int)((b - a) % 16) / P.esize,
+                P.esize);
+}
+
+// Non-straggler `me`: copy every other owner's partial (its CTA's slices).
+template <int DT, int W, int MV>
+__device__ void ag_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
+  const int NV = P.G * P.sub, V = 16 / P.esize;
+  const int own = P.logical_of_phys[me];
+  for (int c = 0; c < P.nchunks; ++c) {
+    if (c == own) continue;
+    int owner = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+      if (P.logical_of_phys[q] == c) owner = q;
+    const Range cr = chunk_range(P, c);
+    for (int j = 0; j < P.sub; ++j) {
+      const int v = s * P.sub + j;
+      // the owner's partial of slice v is final (and the owner is done reading my copy of it)
+      if (!cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, P.fstride, v), ep, P, 0xC00 | c)) return;
+      const Range sl = slice_of(cr.lo, cr.hi, v, NV, V);
+      move_bytes<MV>(pipe, P.buf[me], P.buf[owner], sl.lo * P.esize, sl.hi * P.esize);
+    }
+  }
+  // the partner tells the straggler its operand is ready; the others tell
+  // their sender in the doubling tree that they may now be overwritten
+  if (me == P.bc_partner)
+    cta_signal(flag_at(P.flags[P.sigma], SLOT_BC_AGDONE, P.fstride, s), ep, P.sys_scope);
+  else
+    cta_signal(flag_at(P.flags[P.bc_sender[me]], SLOT_BC_READY + me, P.fstride, s), ep, P.sys_scope);
+}
+
+template <int DT, int W, int MV>
+__device__ void bcast_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
+  const int NV = P.G * P.sub, V = 16 / P.esize;
+  const int p0 = P.bc_partner, sig = P.sigma;
+  char* mine = P.buf[me];
+  bool ok;
+  if (me == sig || me == p0) {
+    const int peer = (me == sig) ? p0 : sig;
+    if (me == sig) {
+      // the straggler arrives (barrier (2)); its operand is the partner's full non-straggler sum
+      if (threadIdx.x == 0) st_release(flag_at(P.flags[p0], SLOT_ARRIVE + sig, P.fstride, s), ep, P.sys_scope);
+      ok = cta_wait(flag_at(P.flags[me], SLOT_BC_AGDONE, P.fstride, s), ep, P, 0xD00);
+    } else {
+      ok = cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + sig, P.fstride, s), ep, P, 0xD01);
+    }
+    if (ok) {
+      // the exchange of the entire buffer: the partner computes the first half
+      // of every range, the straggler the second; both halves land at both ends
+      for (int c = 0; c < P.nchunks; ++c) {
+        uint64_t a, b;
+        cta_chunk_bytes(P, c, s, a, b);
+        const uint64_t nv = (b - a + 15) / 16;
+        const uint64_t m = a + (nv / 2) * 16 < b ? a + (nv / 2) * 16 : b;
+        if (me == p0)
+          add_bytes<DT, MV>(P, pipe, mine, P.buf[peer], mine, P.buf[peer], a, m);
+        else
+          add_bytes<DT, MV>(P, pipe, mine, P.buf[peer], P.buf[peer], mine, m, b);
+      }
+      cta_signal(flag_at(P.flags[peer], SLOT_HAVE, P.fstride, s), ep, P.sys_scope);
+      ok = cta_wait(flag_at(P.flags[me], SLOT_HAVE, P.fstride, s), ep, P, 0xD02);
+    }
+  } else {
+    ok = cta_wait(flag_at(P.flags[me], SLOT_HAVE, P.fstride, s), ep, P, 0xD03);
+  }
+  (void)V;
+  // holders copy the entire (CTA-range) buffer on, one receiver per round
+  for (int rd = 1; ok && rd < W; ++rd)
+    for (int q = 0; ok && q < W; ++q) {
+      if (P.bc_sender[q] != me || P.bc_round[q] != rd) continue;
+      if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_BC_READY + q, P.fstride, s), ep, P, 0xD10 | q))) break;
+      for (int c = 0; c < P.nchunks; ++c) {
+        uint64_t a, b;
+        cta_chunk_bytes(P, c, s, a, b);
+        move_bytes<MV>(pipe, P.buf[q], mine, a, b);
+      }
+      cta_signal(flag_at(P.flags[q], SLOT_HAVE, P.fstride, s), ep, P.sys_scope);
+    }
 }
 
 // ---------------------------------------------------------------- LL Phase B (small chunks)
@@ -751,7 +883,7 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
   }
   // the straggler reaches barrier (2): announce per CTA slot to the others
   if (me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
-    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, NV, s), ep, P.sys_scope);
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, P.fstride, s), ep, P.sys_scope);
   char* mine = P.buf[me];
   const int nops = P.nops[me];
   bool ok = true;
@@ -769,7 +901,7 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
       const uint64_t mid = sl.lo + (nvec_total / 2) * V < sl.hi ? sl.lo + (nvec_total / 2) * V : sl.hi;
       if (op.kind == OP_EXCH_LOW) {
         // non-straggler r: [lo, mid) of c_r = partial_r (+) x_sigma, stored at both ends
-        if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, NV, s), ep, P, 0x200 | k))) break;
+        if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, P.fstride, s), ep, P, 0x200 | k))) break;
         if (tr) tr[1] = globaltimer();
         const uint64_t a = sl.lo * P.esize, b = mid * P.esize, body = (b - a) / 16 * 16;
         if constexpr (tma)
@@ -780,7 +912,7 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
                       (int)((b - a) % 16) / P.esize, P.esize);
       } else if (op.kind == OP_EXCH_HIGH) {
         // straggler: [mid, hi) of c_r; waits for rank r's Phase-A partial
-        if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, NV, v), ep, P, 0x300 | k))) break;
+        if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, P.fstride, v), ep, P, 0x300 | k))) break;
         if (tr) tr[1] = globaltimer();
         const uint64_t a = mid * P.esize, b = sl.hi * P.esize, body = (b - a) / 16 * 16;
         if constexpr (tma)
@@ -791,7 +923,7 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
                       (int)((b - a) % 16) / P.esize, P.esize);
       } else {
         // copy of a fully reduced chunk (push)
-        if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, NV, v), ep, P, 0x400 | k))) break;
+        if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, P.fstride, v), ep, P, 0x400 | k))) break;
         if (tr) tr[1] = globaltimer();
         const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize, body = (b - a) / 16 * 16;
         if constexpr (tma)
@@ -800,7 +932,7 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
           copy_vecs(P.buf[peer] + a, mine + a, body / 16);
         copy_tail(P.buf[peer] + a + body, mine + a + body, (int)((b - a) % 16));
       }
-      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, NV, v), ep, P.sys_scope);
+      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, P.fstride, v), ep, P.sys_scope);
       if (tr) tr[2] = globaltimer();
     }
   }
@@ -808,7 +940,7 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
   // (chunk, slice) flag, so the acquire loads overlap)
   if (ok && (int)threadIdx.x < P.nchunks * P.sub) {
     const int c = threadIdx.x / P.sub, j = threadIdx.x % P.sub;
-    spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, NV, s * P.sub + j), ep, P, 0x500 | c);
+    spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, P.fstride, s * P.sub + j), ep, P, 0x500 | c);
   }
   __syncthreads();
 }
@@ -829,10 +961,10 @@ __device__ void direct_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint
   if (me == P.sigma) {
     // the straggler arrives: its buffer may now be read by every owner
     if (threadIdx.x < W && (int)threadIdx.x != me)
-      st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, NV, s), ep, P.sys_scope);
+      st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, P.fstride, s), ep, P.sys_scope);
   } else {
     own = P.logical_of_phys[me];
-    ok = cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + P.sigma, NV, s), ep, P, 0x900);
+    ok = cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + P.sigma, P.fstride, s), ep, P, 0x900);
     if (ok) {
       // the CTA's sub slices are adjacent: one pass over their union (no
       // pipeline drain between them), then one flag per slice
@@ -862,19 +994,21 @@ __device__ void direct_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint
       __syncthreads();
       for (int j = 0; j < P.sub; ++j)
         if (threadIdx.x < W && (int)threadIdx.x != me)
-          st_release(flag_at(P.flags[threadIdx.x], SLOT_HAVE + own, NV, s * P.sub + j), ep, P.sys_scope);
+          st_release(flag_at(P.flags[threadIdx.x], SLOT_HAVE + own, P.fstride, s * P.sub + j), ep, P.sys_scope);
     }
   }
   // postcondition: every other chunk has landed here (one waiting thread per flag)
   if (ok && (int)threadIdx.x < P.nchunks * P.sub) {
     const int c = threadIdx.x / P.sub, j = threadIdx.x % P.sub;
-    if (c != own) spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, NV, s * P.sub + j), ep, P, 0xA00 | c);
+    if (c != own) spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, P.fstride, s * P.sub + j), ep, P, 0xA00 | c);
   }
   __syncthreads();
 }
 
 // KIND: 0 Phase A only, 1 Phase B (schedule), 3 Phase B (direct),
-//       4 Phase A + schedule in one launch, 5 Phase A + direct in one launch.
+//       4 Phase A + schedule in one launch, 5 Phase A + direct in one launch,
+//       6 Broadcast baseline precondition (non-straggler AllReduce),
+//       7 Broadcast baseline completion, 8 both in one launch.
 template <int DT, int W, int MV, int KIND>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_constant__ LaunchPlan P) {
   const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
@@ -900,6 +1034,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_con
     atomicMax(reinterpret_cast<unsigned long long*>(&P.state->t_a_done), (unsigned long long)globaltimer());
   if constexpr (KIND == 1 || KIND == 4) complete_body<DT, W, MV>(P, pipe, s, me, ep);
   if constexpr (KIND == 3 || KIND == 5) direct_body<DT, W, MV>(P, pipe, s, me, ep);
+  if constexpr (KIND == 6 || KIND == 8)
+    if (me != P.sigma) {
+      rs_body<DT, W, MV, true>(P, pipe, s, me, ep);
+      ag_body<DT, W, MV>(P, pipe, s, me, ep);
+    }
+  if constexpr (KIND == 7 || KIND == 8) bcast_body<DT, W, MV>(P, pipe, s, me, ep);
   if (stamps && threadIdx.x == 0)
     atomicMax(reinterpret_cast<unsigned long long*>(&P.state->t_b_done), (unsigned long long)globaltimer());
   finish_call(P);
@@ -917,7 +1057,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
   const int V = 16 / P.esize;
   const uint32_t ep = call_epoch(P);
   const int left = (j + W - 1) % W, right = (j + 1) % W;
-  if (threadIdx.x == 0) st_release(flag_at(P.flags[right], SLOT_RING_ARRIVE, NV, s), ep, P.sys_scope);
+  if (threadIdx.x == 0) st_release(flag_at(P.flags[right], SLOT_RING_ARRIVE, P.fstride, s), ep, P.sys_scope);
   constexpr bool tma = MV == MOVER_TMA;
   Pipe pipe = make_pipe(tma);
   char* mine = P.buf[j];
@@ -928,8 +1068,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
     for (int q = 0; q < P.sub; ++q) {
       const int v = s * P.sub + q;
       // step 0 waits for the left neighbour's arrival (per CTA), step t for its step t-1 on slice v
-      const uint32_t* wf = (t == 0) ? flag_at(P.flags[j], SLOT_RING_ARRIVE, NV, s)
-                                    : flag_at(P.flags[j], SLOT_RING_READY + t - 1, NV, v);
+      const uint32_t* wf = (t == 0) ? flag_at(P.flags[j], SLOT_RING_ARRIVE, P.fstride, s)
+                                    : flag_at(P.flags[j], SLOT_RING_READY + t - 1, P.fstride, v);
       if (!cta_wait(wf, ep, P, 0x600 | t)) {
         finish_call(P);
         return;
@@ -951,12 +1091,80 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
           copy_vecs(mine + a, lbuf + a, nv);
         copy_tail(mine + a + nv * 16, lbuf + a + nv * 16, (int)((b - a) % 16));
       }
-      if (t < 2 * (W - 1) - 1) cta_signal(flag_at(P.flags[right], SLOT_RING_READY + t, NV, v), ep, P.sys_scope);
+      if (t < 2 * (W - 1) - 1) cta_signal(flag_at(P.flags[right], SLOT_RING_READY + t, P.fstride, v), ep, P.sys_scope);
     }
   }
   // I am done reading the left buffer; wait until the right neighbour is done with mine
-  cta_signal(flag_at(P.flags[left], SLOT_RING_DONE, NV, s), ep, P.sys_scope);
-  cta_wait(flag_at(P.flags[j], SLOT_RING_DONE, NV, s), ep, P, 0x700);
+  cta_signal(flag_at(P.flags[left], SLOT_RING_DONE, P.fstride, s), ep, P.sys_scope);
+  cta_wait(flag_at(P.flags[j], SLOT_RING_DONE, P.fstride, s), ep, P, 0x700);
+  finish_call(P);
+}
+
+// ---------------------------------------------------------------- RHD (NEXT N3)
+// Recursive halving/doubling, pull-based, n chunks (the Ring's
+// partition).  Step t < L (ReduceScatter): partner j ^ n/2^(t+1); both hold the
+// same block of n/2^t chunks; j keeps the lower half if that bit of j is 0 and
+// adds the partner's copy of it into its own.  Step L+u (AllGather): partner
+// j ^ 2^u; j copies the partner's fully reduced block.  Step tau's partner is
+// told when j finished step tau-1 (SLOT_RHD_READY + tau, per slice); AllGather
+// readers report back (SLOT_RHD_DONE) so no rank leaves while its buffer is read.
+template <int DT, int W, int MV>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) k_rhd(const __grid_constant__ LaunchPlan P) {
+  constexpr int L = (W >= 8) ? 3 : (W >= 4) ? 2 : 1;
+  static_assert((1 << L) == W, "RHD needs a power-of-two world");
+  const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
+  const int j = P.local_rank[li];
+  const int NV = P.G * P.sub;
+  const int V = 16 / P.esize;
+  const uint32_t ep = call_epoch(P);
+  auto partner = [&](int tau) { return j ^ (tau < L ? (W >> (tau + 1)) : (1 << (tau - L))); };
+  if (threadIdx.x == 0) st_release(flag_at(P.flags[partner(0)], SLOT_RHD_READY, P.fstride, s), ep, P.sys_scope);
+  Pipe pipe = make_pipe(MV == MOVER_TMA);
+  char* mine = P.buf[j];
+  int blo = 0, m = W;   // the block of chunks j works on
+  bool ok = true;
+  for (int tau = 0; tau < 2 * L && ok; ++tau) {
+    const int p = partner(tau);
+    const char* pbuf = P.buf[p];
+    int clo, cn;        // chunks moved this step
+    if (tau < L) {
+      m /= 2;
+      blo = (j & (W >> (tau + 1))) ? blo + m : blo;
+      clo = blo;
+      cn = m;
+    } else {
+      clo = blo ^ m;    // the partner's block (aligned siblings)
+      cn = m;
+    }
+    for (int q = 0; q < P.sub; ++q) {
+      const int v = s * P.sub + q;
+      const uint32_t* wf = flag_at(P.flags[j], SLOT_RHD_READY + tau, P.fstride, tau == 0 ? s : v);
+      if (!(ok = cta_wait(wf, ep, P, 0xE00 | tau))) break;
+      for (int c = clo; c < clo + cn; ++c) {
+        const Range cr = chunk_range(P, c);
+        const Range sl = slice_of(cr.lo, cr.hi, v, NV, V);
+        const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
+        if (tau < L)
+          add_bytes<DT, MV>(P, pipe, mine, nullptr, pbuf, mine, a, b);
+        else
+          move_bytes<MV>(pipe, mine, pbuf, a, b);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (tau + 1 < 2 * L) st_release(flag_at(P.flags[partner(tau + 1)], SLOT_RHD_READY + tau + 1, P.fstride, v), ep, P.sys_scope);
+        if (tau >= L) st_release(flag_at(P.flags[p], SLOT_RHD_DONE + tau - L, P.fstride, v), ep, P.sys_scope);
+      }
+    }
+    if (tau >= L) {
+      blo = blo < clo ? blo : clo;
+      m *= 2;
+    }
+  }
+  // every AllGather partner finished reading my buffer (one waiting thread per flag)
+  if (ok && (int)threadIdx.x < L * P.sub) {
+    const int u = threadIdx.x / P.sub, q = threadIdx.x % P.sub;
+    spin_wait(flag_at(P.flags[j], SLOT_RHD_DONE + u, P.fstride, s * P.sub + q), ep, P, 0xE10 | u);
+  }
   finish_call(P);
 }
 
@@ -969,6 +1177,12 @@ inline void* kernel_ptr_mv(int which) {
     case 3: return (void*)k_phase<DT, W, MV, 3>;   // Phase B, direct completion
     case 4: return (void*)k_phase<DT, W, MV, 4>;   // A + B (schedule), one launch
     case 5: return (void*)k_phase<DT, W, MV, 5>;   // A + B (direct), one launch
+    case 6: return (void*)k_phase<DT, W, MV, 6>;   // Broadcast baseline: non-straggler AllReduce
+    case 7: return (void*)k_phase<DT, W, MV, 7>;   // Broadcast baseline: exchange + doubling copies
+    case 8: return (void*)k_phase<DT, W, MV, 8>;   // Broadcast baseline, one launch
+    case 9:
+      if constexpr ((W & (W - 1)) == 0) return (void*)k_rhd<DT, W, MV>;   // RHD baseline
+      return nullptr;
     default: return nullptr;
   }
 }

@@ -6,9 +6,10 @@
 
 namespace stragglar {
 
-// Flag slots.  Every rank owns kSlots * G * sub uint32 flags; slot k, slice v
-// lives at flags[k * G * sub + v] (G CTAs per rank, each covering `sub`
-// consecutive slices of every chunk; see LaunchPlan::sub).  Flags hold the call's epoch (monotonic, never reset):
+// Flag slots.  Every rank owns kSlots * G_max * kMaxSub uint32 flags; slot k,
+// slice v lives at flags[k * G_max * kMaxSub + v] (a call uses G <= G_max CTAs
+// per rank, each covering `sub` consecutive slices of every chunk; see
+// LaunchPlan::sub and flag_at).  Flags hold the call's epoch (monotonic, never reset):
 // a waiter proceeds when (int32)(flag - epoch) >= 0.  Producers write peers'
 // flags (remote store, release at system scope); consumers spin on their own
 // (local load, acquire at system scope).
@@ -20,7 +21,12 @@ enum Slot : int {
   SLOT_RING_READY = 25,  // + step (0..13): left neighbour finished ring step
   SLOT_RING_DONE = 39,   // right neighbour finished reading my buffer
   SLOT_BARRIER = 40,     // + physical rank
-  kSlots = 48
+  // NEXT N3 baselines
+  SLOT_BC_AGDONE = 48,   // Broadcast: the straggler's partner finished the non-straggler AllReduce (at sigma)
+  SLOT_BC_READY = 49,    // + physical rank q: q finished the non-straggler AllReduce (at q's sender)
+  SLOT_RHD_READY = 57,   // + step (0..5): the step's partner finished its previous step (step 0: arrived)
+  SLOT_RHD_DONE = 63,    // + AllGather step (0..2): that step's partner finished reading my buffer
+  kSlots = 72
 };
 
 #ifndef STRAGGLAR_THREADS
@@ -63,6 +69,7 @@ struct LaunchPlan {
                              // handles slices s*sub .. s*sub+sub-1, one flag each (finer-grained
                              // hand-offs between ranks with the same CTAs); 1 = one slice per CTA
   int nlocal;                // ranks served by this launch (1, or world in team mode)
+  int fstride;               // flags per slot (G_max * kMaxSub, fixed per communicator; see flag_at)
   int local_rank[kMaxWorld]; // physical rank of local index i (blockIdx.x / G)
   char* buf[kMaxWorld];      // data buffer of each physical rank (local or peer mapping)
   uint32_t* flags[kMaxWorld];// flag array of each physical rank
@@ -82,6 +89,9 @@ struct LaunchPlan {
   uint64_t sigma_delay_ns;   // team measurement only: straggler CTAs start this late (KIND 4/5)
   uint64_t* trace;           // optional: [rank][slice][op][3] %globaltimer stamps (wait, data, done) of Phase B
   int logical_of_phys[kMaxWorld];
+  int bc_partner;            // Broadcast baseline: the straggler's exchange partner (physical)
+  int bc_sender[kMaxWorld];  //   per physical rank: who copies the full sum to it (-1: a holder)
+  int bc_round[kMaxWorld];   //   and in which round
   int nops[kMaxWorld];       // by physical rank
   Op ops[kMaxWorld][kMaxOps];// by physical rank
 };

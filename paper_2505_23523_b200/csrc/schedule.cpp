@@ -233,6 +233,27 @@ std::vector<Round> generate_any(int n) {
   return generate_even(n);
 }
 
+void broadcast_tree(int n, int* sender, int* round) {
+  if (n < 2 || n > 64) throw std::runtime_error("world must be in [2, 64]");
+  uint64_t held = bit(0) | bit(n - 1);
+  for (int q = 0; q < n; ++q) {
+    sender[q] = -1;
+    round[q] = 0;
+  }
+  for (int r = 1; __builtin_popcountll(held) < n; ++r) {
+    const uint64_t before = held;
+    int q = 0;
+    for (int h = 0; h < n; ++h) {
+      if (!has(before, h)) continue;
+      while (q < n && has(held, q)) ++q;            // next non-holder, ascending
+      if (q == n) break;
+      sender[q] = h;
+      round[q] = r;
+      held |= bit(q);
+    }
+  }
+}
+
 RankPrograms build_programs(int n, int sigma_phys) {
   if (n < 2 || n > kMaxWorld || (n & 1)) throw std::runtime_error("world must be 2, 4, 6 or 8");
   if (sigma_phys < 0 || sigma_phys >= n) throw std::runtime_error("straggler rank out of range");
@@ -267,6 +288,17 @@ RankPrograms build_programs(int n, int sigma_phys) {
       if (pr.nops[pa] >= kMaxOps) throw std::runtime_error("op table overflow");
       pr.ops[pa][pr.nops[pa]++] = op;
     }
+  }
+  int snd[kMaxWorld], rnd[kMaxWorld];
+  broadcast_tree(n, snd, rnd);
+  pr.bc_partner = pr.phys_of_logical[0];
+  for (int p = 0; p < kMaxWorld; ++p) {
+    pr.bc_sender[p] = -1;
+    pr.bc_round[p] = 0;
+  }
+  for (int l = 0; l < n; ++l) {
+    pr.bc_sender[pr.phys_of_logical[l]] = snd[l] < 0 ? -1 : pr.phys_of_logical[snd[l]];
+    pr.bc_round[pr.phys_of_logical[l]] = rnd[l];
   }
   return pr;
 }

@@ -40,7 +40,19 @@ struct RankPrograms {
   int logical_of_phys[kMaxWorld];
   int nops[kMaxWorld];
   Op ops[kMaxWorld][kMaxOps];
+  // straggler-aware Broadcast baseline, physical ranks: the
+  // straggler's exchange partner, and per rank the rank it receives the full
+  // sum from (-1: it holds it after the exchange) and that copy's round
+  int bc_partner;
+  int bc_sender[kMaxWorld];
+  int bc_round[kMaxWorld];
 };
+
+// Broadcast baseline tree in logical ranks (straggler n-1): round 0 is the
+// straggler's exchange with rank 0; in round r >= 1 the holders of the full
+// sum, ascending, each copy it to the next non-holder, ascending.  sender[q]
+// = -1 and round[q] = 0 for q in {0, n-1}.  n in [2, 64].
+void broadcast_tree(int n, int* sender, int* round);
 RankPrograms build_programs(int n, int sigma_phys);
 
 }  // namespace stragglar

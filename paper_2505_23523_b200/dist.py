@@ -58,5 +58,11 @@ class ProcessComm:
     def allreduce_ring(self, tensor, stream=None) -> None:
         self.lib.stragglar_allreduce_ring(tensor, stream)
 
+    def allreduce_rhd(self, tensor, stream=None) -> None:
+        self.lib.stragglar_allreduce_rhd(tensor, stream)
+
+    def allreduce_bcast(self, tensor, stream=None) -> None:
+        self.lib.stragglar_allreduce_bcast(tensor, stream)
+
     def close(self) -> None:
         self.lib.stragglar_finalize()

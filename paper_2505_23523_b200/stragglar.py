@@ -57,6 +57,9 @@ _SIGS = {
     "stragglar_allreduce_ring": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_allreduce_direct": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_allreduce_host": ([_vp, _vp, _vp, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_allreduce_rhd": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_allreduce_bcast": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_broadcast_tree": ([_c_int, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)], _c_int),
     "stragglar_barrier": ([_vp], _c_int),
     "stragglar_inject_delay": ([_c_u64, _vp], _c_int),
     "stragglar_check_error": ([ctypes.POINTER(_c_int)], _c_int),
@@ -74,6 +77,10 @@ _SIGS = {
     "stragglar_team_allreduce_ring": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_team_complete_direct": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_team_allreduce_direct": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_team_allreduce_rhd": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_team_bcast_precondition": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_team_bcast_complete": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_team_allreduce_bcast": ([_PP, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_team_inject_delay": ([_c_u64, _vp], _c_int),
     "stragglar_team_allreduce_delayed": ([_PP, _c_size, _c_int, _c_int, _c_u64, _vp], _c_int),
     "stragglar_team_allreduce_host": ([_PP, _PP, _PP, _c_size, _c_int, _c_int, _vp], _c_int),
@@ -240,6 +247,23 @@ def stragglar_allreduce_direct(t, stream=None) -> None:
         _lib.stragglar_allreduce_direct(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream)))
 
 
+def stragglar_allreduce_rhd(t, stream=None) -> None:
+    _ck("stragglar_allreduce_rhd",
+        _lib.stragglar_allreduce_rhd(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream)))
+
+
+def stragglar_allreduce_bcast(t, stream=None) -> None:
+    _ck("stragglar_allreduce_bcast",
+        _lib.stragglar_allreduce_bcast(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream)))
+
+
+def stragglar_broadcast_tree(world: int):
+    """-> (sender, round) lists in logical ranks (sender -1 for the two holders)."""
+    snd, rnd = (_c_int * world)(), (_c_int * world)()
+    _ck("stragglar_broadcast_tree", _lib.stragglar_broadcast_tree(world, snd, rnd))
+    return list(snd), list(rnd)
+
+
 def stragglar_barrier(stream=None) -> None:
     _ck("stragglar_barrier", _lib.stragglar_barrier(_stream_ptr(stream)))
 
@@ -314,6 +338,22 @@ def stragglar_team_complete_direct(bufs, stream=None) -> None:
 
 def stragglar_team_allreduce_direct(bufs, stream=None) -> None:
     _team_call("stragglar_team_allreduce_direct", bufs, stream)
+
+
+def stragglar_team_allreduce_rhd(bufs, stream=None) -> None:
+    _team_call("stragglar_team_allreduce_rhd", bufs, stream)
+
+
+def stragglar_team_bcast_precondition(bufs, stream=None) -> None:
+    _team_call("stragglar_team_bcast_precondition", bufs, stream)
+
+
+def stragglar_team_bcast_complete(bufs, stream=None) -> None:
+    _team_call("stragglar_team_bcast_complete", bufs, stream)
+
+
+def stragglar_team_allreduce_bcast(bufs, stream=None) -> None:
+    _team_call("stragglar_team_allreduce_bcast", bufs, stream)
 
 
 def stragglar_team_allreduce_delayed(bufs, delay_ns: int, stream=None) -> None:

@@ -85,6 +85,30 @@ def measure(n, sigma, count, dtype, iters, warm, delay_factor=1.25):
         b.record()
     torch.cuda.synchronize()
     T_ring = statistics.median(a.elapsed_time(b) * 1e3 for a, b in R)
+    # NEXT N3 baselines: RHD (whole AllReduce, like the Ring) and the Broadcast
+    # baseline's post-arrival part (its precondition runs before the delay)
+    T_rhd = None
+    if n & (n - 1) == 0:
+        for _ in range(warm):
+            S.stragglar_team_allreduce_rhd(ring)
+        R = [(ev(), ev()) for _ in range(iters)]
+        blocker()
+        for a, b in R:
+            a.record()
+            S.stragglar_team_allreduce_rhd(ring)
+            b.record()
+        torch.cuda.synchronize()
+        T_rhd = statistics.median(a.elapsed_time(b) * 1e3 for a, b in R)
+    B = [(ev(), ev()) for _ in range(iters + warm)]
+    blocker()
+    for a, b in B:
+        S.stragglar_team_bcast_precondition(ring)
+        S.stragglar_team_inject_delay(D)
+        a.record()
+        S.stragglar_team_bcast_complete(ring)
+        b.record()
+    torch.cuda.synchronize()
+    T_bcast = statistics.median(a.elapsed_time(b) * 1e3 for a, b in B[warm:])
     assert S.stragglar_team_check_error() == 0
     S.stragglar_team_finalize()
     nbytes = count * ESZ[dtype]
@@ -99,6 +123,10 @@ def measure(n, sigma, count, dtype, iters, warm, delay_factor=1.25):
         "speedup_post_vs_ring": round(T_ring / T_post, 3),
         "speedup_total_vs_ring_masked": round((D_meas + T_ring) / T_tot, 3),
         "speedup_nodelay_vs_ring": round(T_ring / T_nod, 3),
+        "T_rhd_us": round(T_rhd, 2) if T_rhd else None,
+        "T_bcast_post_us": round(T_bcast, 2),
+        "speedup_post_vs_rhd": round(T_rhd / T_post, 3) if T_rhd else None,
+        "speedup_post_vs_bcast": round(T_bcast / T_post, 3),
     }
 
 

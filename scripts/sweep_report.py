@@ -16,13 +16,13 @@ def main(path, out):
     L = ["# Size / world / delay sweep (1 B200, single-device team; device time, bf16)", "",
          "Rows: message size S per rank.  T_A = Phase A (ReduceScatter among the non-stragglers), "
          "T_post = Phase B after the straggler arrives with a masking delay (D = 1.25 T_A + 20 us), "
-         "T_nodelay = A + B back to back with no delay, T_ring = hand-written Ring.  "
+         "T_nodelay = A + B back to back with no delay, T_ring = hand-written Ring, T_rhd = recursive halving/doubling (P:363-366), T_bcast post = the straggler-aware Broadcast's completion after its precondition and the same delay (P:368-373).  "
          "HBM fractions: algorithmic HBM bytes (Phase A n(n-1)C, Phase B 2n(n-1)C, Ring 5(n-1)S) / time / "
          f"{PEAK:.0f} GB/s measured.  busbw = S/T_post * 2(n-1)/n (nccl-tests convention).", ""]
     for n in (2, 4, 8):
         L += [f"## n = {n}", "",
-              "| S | T_A us | T_post us | T_nodelay us | T_ring us | algbw GB/s | busbw GB/s | B frac HBM | A frac HBM | ring frac HBM | speedup post | speedup total (D masked) | speedup no delay |",
-              "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+              "| S | T_A us | T_post us | T_nodelay us | T_ring us | T_rhd us | T_bcast post us | algbw GB/s | busbw GB/s | B frac HBM | A frac HBM | ring frac HBM | speedup post | speedup total (D masked) | speedup no delay | vs RHD | vs Bcast |",
+              "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
         for r in d["sizes"]:
             if r["n"] != n:
                 continue
@@ -33,8 +33,10 @@ def main(path, out):
             fr = 5 * (n - 1) * S / (r["T_ring_us"] * 1e3) / PEAK
             size = f"{S >> 20} MiB" if S < (1 << 30) else f"{S >> 30} GiB"
             L.append(f"| {size} | {r['T_phaseA_us']} | {r['T_post_us']} | {r['T_nodelay_us']} | {r['T_ring_us']} | "
+                     f"{r.get('T_rhd_us', '')} | {r.get('T_bcast_post_us', '')} | "
                      f"{r['algbw_post_GBps']} | {r['busbw_post_GBps']} | {fb:.2f} | {fa:.2f} | {fr:.2f} | "
-                     f"{r['speedup_post_vs_ring']} | {r['speedup_total_vs_ring_masked']} | {r['speedup_nodelay_vs_ring']} |")
+                     f"{r['speedup_post_vs_ring']} | {r['speedup_total_vs_ring_masked']} | {r['speedup_nodelay_vs_ring']} | "
+                     f"{r.get('speedup_post_vs_rhd', '')} | {r.get('speedup_post_vs_bcast', '')} |")
         L.append("")
     L += ["## BASELINE configs", "", "| config | T_A us | T_post us | T_nodelay us | T_ring us | speedup post |", "|---|---|---|---|---|---|"]
     for k, r in d["configs"].items():

@@ -36,14 +36,17 @@ def worker(rank, world, sigma, count, dtype, port, q):
         t = torch.empty(count, dtype=tdt, device="cuda")
         ring = torch.empty(count, dtype=tdt, device="cuda")
         autos = [torch.empty(count, dtype=tdt, device="cuda") for _ in range(4)]
+        base = {k: torch.empty(count, dtype=tdt, device="cuda") for k in ("rhd", "bcast")}   # NEXT N3
         comm.register(t)
         comm.register(ring)
+        for b in base.values():
+            comm.register(b)
         for a in autos:
             comm.register(a)
         host = torch.from_numpy(x.view(np.int16) if dtype == "bfloat16" else x)
         t.view(host.dtype).copy_(host)
         ring.view(host.dtype).copy_(host)
-        for a in autos:
+        for a in list(autos) + list(base.values()):
             a.view(host.dtype).copy_(host)
         torch.cuda.synchronize()
         dist.barrier()
@@ -54,6 +57,9 @@ def worker(rank, world, sigma, count, dtype, port, q):
         ta, tk = S.stragglar_phase_times()          # in-kernel stamps of that call
         assert 0.0 <= ta <= tk < 60e6, (ta, tk)
         comm.allreduce_ring(ring)
+        if world & (world - 1) == 0:
+            comm.allreduce_rhd(base["rhd"])
+        comm.allreduce_bcast(base["bcast"])
         # NEXT row N2: selection for an expected delay (0 and 10 ms)
         used = [S.stragglar_allreduce_auto(autos[0], 0), S.stragglar_allreduce_auto(autos[1], 10_000_000)]
         S.stragglar_allreduce_direct(autos[2])     # NEXT row N1(ii): same result as the schedule
@@ -63,14 +69,16 @@ def worker(rank, world, sigma, count, dtype, port, q):
         hout = torch.empty_like(hin).pin_memory()
         comm.allreduce_host(hin.view(tdt), hout.view(tdt), autos[3])
         torch.cuda.synchronize()
-        err = S.stragglar_check_error()
+        code, where = S.stragglar_check_error_where(False)
+        err = f"{code} at 0x{where:x}" if code else 0
         out = t.view(host.dtype).cpu().numpy()
         rout = ring.view(host.dtype).cpu().numpy()
         aout = [(u, a.view(host.dtype).cpu().numpy().tobytes()) for u, a in zip(used, autos[:3])]
         aout.append((True, hout.numpy().tobytes()))
+        bout = {k: b.view(host.dtype).cpu().numpy().tobytes() for k, b in base.items()}
         dist.barrier()
         comm.close()
-        q.put((rank, err, out.tobytes(), rout.tobytes(), aout))
+        q.put((rank, err, out.tobytes(), rout.tobytes(), (aout, bout)))
         dist.destroy_process_group()
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e), None, None, None))
@@ -84,8 +92,8 @@ def run(world, sigma, count, dtype, port):
         p.start()
     res = {}
     for _ in range(world):
-        r, err, out, rout, aout = q.get(timeout=600)
-        res[r] = (err, out, rout, aout)
+        r, err, out, rout, ab = q.get(timeout=600)
+        res[r] = (err, out, rout, ab)
     for p in procs:
         p.join(timeout=60)
     from oracle import numerics as N
@@ -94,13 +102,21 @@ def run(world, sigma, count, dtype, port):
     xs = make_inputs(world, count, dtype, config=7)
     want = N.stragglar_allreduce(xs, sigma, dtype)
     rwant = N.ring_allreduce(xs, dtype)
+    bwant = {"bcast": N.broadcast_allreduce(xs, sigma, dtype)}
+    if world & (world - 1) == 0:
+        bwant["rhd"] = N.rhd_allreduce(xs, dtype)
     ok = True
     for r in range(world):
-        err, out, rout, aout = res[r]
+        err, out, rout, ab = res[r]
         if out is None or err:
             print(f"rank {r}: error {err}")
             ok = False
             continue
+        aout, bout = ab
+        for k, w in bwant.items():
+            if bout[k] != w[r].tobytes():
+                print(f"rank {r}: {k} baseline result differs from the oracle")
+                ok = False
         if out != want[r].tobytes():
             print(f"rank {r}: stragglar result differs from the oracle")
             ok = False

@@ -117,3 +117,16 @@ def test_cpp_appendix_b_equals_oracle(S, world):
         got = {(a, b, c, "reduce" if k == 0 else "replace") for a, b, c, k in S.stragglar_schedule_round(world, r)}
         want = {(t.src, t.dst, t.chunk, t.kind) for t in o.rounds[r]}
         assert got == want, (world, r)
+
+
+@pytest.mark.parametrize("world", [2, 4, 6, 8, 10, 16, 64])
+def test_cpp_broadcast_tree_equals_oracle(S, world):
+    """NEXT N3 Broadcast baseline: the library's doubling tree (C++) vs the
+    oracle's generate_broadcast, copy by copy and round by round."""
+    sender, rnd = S.stragglar_broadcast_tree(world)
+    o = OS.generate_broadcast(world)
+    want_sender, want_round = [-1] * world, [0] * world
+    for r, transfers in enumerate(o.rounds[1:], start=1):
+        for t in transfers:
+            want_sender[t.dst], want_round[t.dst] = t.src, r
+    assert sender == want_sender and rnd == want_round

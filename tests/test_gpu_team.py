@@ -67,10 +67,16 @@ def run_team(S, n, sigma, dtype, count, pattern="normal", config=1, algo="stragg
         S.stragglar_team_allreduce(bufs)
     elif algo == "direct":
         S.stragglar_team_allreduce_direct(bufs)
+    elif algo == "rhd":
+        S.stragglar_team_allreduce_rhd(bufs)
+    elif algo == "bcast":
+        S.stragglar_team_allreduce_bcast(bufs)
     else:
         S.stragglar_team_allreduce_ring(bufs)
     torch.cuda.synchronize()
-    assert S.stragglar_team_check_error() == 0
+    code, where = S.stragglar_check_error_where(True)
+    assert code == 0, f"{algo}: device error {code} at 0x{where:x}"
+
     outs = [to_host(b, dtype) for b in bufs]
     return xs, outs
 
@@ -468,3 +474,135 @@ def test_subslices(S, dtype):
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
+
+
+# ---------------------------------------------------------------- NEXT N3 baselines
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_rhd_baseline(S, dtype, n):
+    """Recursive halving/doubling against the oracle's RHD replay (butterfly
+    order, bf16 rounded per step), ragged counts incl. fewer elements than ranks."""
+    for count in [1, 3, 8 * n + 5, 1001, (1 << 18) + 7, (1 << 20) + 3]:
+        xs, outs = run_team(S, n, 0, dtype, count, algo="rhd", config=80)
+        check_equal(outs, N.rhd_allreduce(xs, dtype), xs, dtype, f"rhd n={n} count={count}")
+
+
+def test_rhd_needs_power_of_two(S):
+    S.stragglar_team_init(6, 0)
+    bufs = [torch.zeros(64, device="cuda") for _ in range(6)]
+    with pytest.raises(S.StragglarError) as e:
+        S.stragglar_team_allreduce_rhd(bufs)
+    assert e.value.status == 2
+
+
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+@pytest.mark.parametrize("n", [2, 4, 6, 8])
+def test_bcast_baseline(S, dtype, n):
+    """Straggler-aware Broadcast (one launch): every straggler rank, ragged
+    counts; equals the oracle's step-by-step replay (= the plain definition)."""
+    for sigma in range(n):
+        for count in [3, 8 * (n - 1) + 5, 70001]:
+            xs, outs = run_team(S, n, sigma, dtype, count, algo="bcast", config=81)
+            check_equal(outs, N.broadcast_allreduce(xs, sigma, dtype), xs, dtype, f"bcast n={n} s={sigma} c={count}")
+    xs, outs = run_team(S, n, n // 2, dtype, (1 << 20) + 3, algo="bcast", config=82)
+    check_equal(outs, N.broadcast_allreduce(xs, n // 2, dtype), xs, dtype, "bcast large")
+
+
+@pytest.mark.parametrize("n,sigma", [(8, 0), (4, 3), (2, 1)])
+def test_bcast_split_with_delay(S, n, sigma):
+    """Precondition -> injected delay -> completion (how the bench times the
+    Broadcast baseline's post-arrival part) gives the same bits; a completion
+    without its precondition is rejected."""
+    dtype, count = "bfloat16", 250007
+    S.stragglar_team_init(n, sigma)
+    bufs = [torch.zeros(64, device="cuda") for _ in range(n)]
+    with pytest.raises(S.StragglarError):
+        S.stragglar_team_bcast_complete(bufs)
+    xs = make_inputs(n, count, dtype, config=83)
+    bufs = [to_dev(x, dtype) for x in xs]
+    S.stragglar_team_bcast_precondition(bufs)
+    with pytest.raises(S.StragglarError):
+        S.stragglar_team_allreduce(bufs)          # a precondition is pending
+    S.stragglar_team_inject_delay(30_000)
+    S.stragglar_team_bcast_complete(bufs)
+    torch.cuda.synchronize()
+    assert S.stragglar_team_check_error() == 0
+    check_equal([to_host(b, dtype) for b in bufs], N.broadcast_allreduce(xs, sigma, dtype), xs, dtype, "bcast split")
+
+
+def test_all_algorithms_back_to_back(S):
+    """Every algorithm of the library on the same communicator, queued back to
+    back with no host synchronisation: the flag slots of one algorithm never
+    satisfy a wait of another (epochs), and each result equals its oracle."""
+    n, sigma, dtype, count = 8, 5, "float32", 180001
+    S.stragglar_team_init(n, sigma)
+    algos = ["stragglar", "rhd", "bcast", "ring", "direct", "bcast", "rhd", "stragglar"]
+    runs = []
+    for it, algo in enumerate(algos):
+        xs = make_inputs(n, count, dtype, config=84 + it)
+        bufs = [to_dev(x, dtype) for x in xs]
+        runs.append((algo, xs, bufs))
+    torch.cuda.synchronize()
+    for algo, xs, bufs in runs:
+        {"stragglar": S.stragglar_team_allreduce, "rhd": S.stragglar_team_allreduce_rhd,
+         "bcast": S.stragglar_team_allreduce_bcast, "ring": S.stragglar_team_allreduce_ring,
+         "direct": S.stragglar_team_allreduce_direct}[algo](bufs)
+    torch.cuda.synchronize()
+    assert S.stragglar_team_check_error() == 0
+    for algo, xs, bufs in runs:
+        want = {"rhd": lambda: N.rhd_allreduce(xs, dtype), "ring": lambda: N.ring_allreduce(xs, dtype),
+                "bcast": lambda: N.broadcast_allreduce(xs, sigma, dtype)}.get(
+                    algo, lambda: N.stragglar_allreduce(xs, sigma, dtype))()
+        check_equal([to_host(b, dtype) for b in bufs], want, xs, dtype, algo)
+
+
+def test_baselines_full_size(S):
+    """BASELINE config 2 size (n=8, 256 MiB fp32 per rank) in the bench's
+    launch configuration: RHD vs its butterfly definition and Broadcast vs the
+    plain definition on 300k sampled indices; all ranks bitwise identical."""
+    n, sigma, dtype, count = 8, 0, "float32", 1 << 26
+    xs_full = make_inputs(n, count, dtype, config=2)
+    rng = np.random.default_rng(11)
+    idx = np.unique(np.concatenate([rng.integers(0, count, 300_000), [0, count - 1]]))
+    xs = [x[idx] for x in xs_full]
+    S.stragglar_team_init(n, sigma)
+    for algo in ("rhd", "bcast"):
+        bufs = [to_dev(x, dtype) for x in xs_full]
+        if algo == "rhd":
+            S.stragglar_team_allreduce_rhd(bufs)
+            want = N.plain_rhd_allreduce(xs, dtype)
+        else:
+            S.stragglar_team_bcast_precondition(bufs)
+            S.stragglar_team_inject_delay(1_000_000)
+            S.stragglar_team_bcast_complete(bufs)
+            want = N.plain_allreduce(xs, sigma, dtype)
+        torch.cuda.synchronize()
+        assert S.stragglar_team_check_error() == 0
+        for p in range(1, n):
+            assert torch.equal(bufs[p].view(torch.int32), bufs[0].view(torch.int32)), (algo, p)
+        got = bufs[0][torch.from_numpy(idx).cuda()].cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), algo
+        del bufs
+        torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("algo", ["rhd", "bcast", "stragglar", "ring"])
+def test_baselines_many_subslices(S, algo):
+    """8 CTAs per rank and ~4 KB slices: every CTA walks up to 16 sub-slices,
+    one flag each (the hand-off granularity of large messages, exercised at a
+    size the oracle replays in full)."""
+    keys = ("STRAGGLAR_TEAM_SLICES", "STRAGGLAR_SLICE_BYTES", "STRAGGLAR_SUBSLICE_BYTES")
+    old = {k: os.environ.get(k) for k in keys}
+    os.environ.update({"STRAGGLAR_TEAM_SLICES": "8", "STRAGGLAR_SLICE_BYTES": "1024", "STRAGGLAR_SUBSLICE_BYTES": "4096"})
+    try:
+        n, sigma, dtype, count = 4, 3, "float32", 400003
+        xs, outs = run_team(S, n, sigma, dtype, count, algo=algo, config=85)
+    finally:
+        for k, v in old.items():
+            os.environ.pop(k, None)
+            if v is not None:
+                os.environ[k] = v
+    want = {"rhd": lambda: N.rhd_allreduce(xs, dtype), "ring": lambda: N.ring_allreduce(xs, dtype),
+            "bcast": lambda: N.broadcast_allreduce(xs, sigma, dtype)}.get(
+                algo, lambda: N.stragglar_allreduce(xs, sigma, dtype))()
+    check_equal(outs, want, xs, dtype, algo)
