@@ -1,5 +1,6 @@
 """Minimal driver for ncu: config-2 team workload (n=8, 256 MiB fp32 per rank),
-a few StragglAR steps (Phase A, delay, Phase B) and Ring calls."""
+a few StragglAR steps (Phase A, delay, Phase B), Ring, direct completion and
+the N3 baselines (RHD, Broadcast precondition + completion)."""
 import os
 import sys
 
@@ -27,6 +28,9 @@ for _ in range(steps):
     S.stragglar_team_allreduce_ring(bufs)
     S.stragglar_team_reduce_scatter(bufs)
     S.stragglar_team_complete_direct(bufs)
+    S.stragglar_team_allreduce_rhd(bufs)           # NEXT N3 baselines
+    S.stragglar_team_bcast_precondition(bufs)
+    S.stragglar_team_bcast_complete(bufs)
 torch.cuda.synchronize()
 assert S.stragglar_team_check_error() == 0
 print("profile step ok", S.stragglar_launch_count())
