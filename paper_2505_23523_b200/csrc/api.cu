@@ -74,6 +74,11 @@ struct Comm {
   uint64_t e2e_piece_bytes = 8ull << 20;// STRAGGLAR_E2E_PIECE_BYTES (8 MiB measured best)
   int e2e_streams = 1;                  // STRAGGLAR_E2E_STREAMS (1 measured best)
   int last_slices = 0;                  // slices per chunk of the last Phase-B call (trace layout)
+  // LL layout of the previous call if it ran Phase B through the LL areas
+  // (count, element size, CTAs per rank); see LaunchPlan::ll_gate
+  bool ll_last = false;
+  uint64_t ll_count = 0;
+  int ll_esize = 0, ll_G = 0;
   double alpha_s = 3e-6;               // P:450 per-message latency used in the paper's model
   double beta_s_per_byte = 1.0 / 770e9; // measured B200 peer copy per direction (B200_PROFILING.md)
   std::vector<Registration> regs;
@@ -307,10 +312,25 @@ int team_check(void* const* bufs, size_t count, int dtype, int op) {
   return STRAGGLAR_OK;
 }
 
-int launch(int which, int dtype, const LaunchPlan& P, int nblocks, void* stream) {
-  if (which == 1 || which == 4) (g_team.active && P.state == g_team.state ? g_team : g_proc).last_slices = P.G * P.sub;
+int launch(int which, int dtype, const LaunchPlan& P0, int nblocks, void* stream) {
+  Comm& c = (g_team.active && P0.state == g_team.state) ? g_team : g_proc;
+  if (which == K_COMPLETE || which == K_FUSED) c.last_slices = P0.G * P0.sub;
+  // A peer is at most one call ahead (every call needs every rank's arrival to
+  // complete anywhere).  If the previous call ran LL Phase B with another
+  // layout, this call's up-front LL pushes must wait for their receivers'
+  // arrival (per-process mode only: a team launch serves every rank at once).
+  const bool runs_ll = P0.use_ll && (which == K_COMPLETE || which == K_FUSED);
+  LaunchPlan P = P0;
+  P.ll_gate = (runs_ll && !c.team && c.ll_last &&
+               (c.ll_count != P.count || c.ll_esize != P.esize || c.ll_G != P.G)) ? 1 : 0;
   cudaError_t e = launch_plan_kernel(which, dtype, P, nblocks, (cudaStream_t)stream);
   if (e != cudaSuccess) return STRAGGLAR_ERR_CUDA;
+  if (P.last_kernel) {
+    c.ll_last = runs_ll;
+    c.ll_count = P.count;
+    c.ll_esize = P.esize;
+    c.ll_G = P.G;
+  }
   g_launches.fetch_add(1);
   return STRAGGLAR_OK;
 }

@@ -520,8 +520,9 @@ template <int DT, int W, int MV, bool BC = false>
 __device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
   const int NV = P.G * P.sub;   // slices per chunk (flag stride)
   if (blockIdx.x == 0 && threadIdx.x == 0) P.state->t_rs_start = globaltimer();
-  // barrier (1) among the non-stragglers, per CTA slot
-  if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
+  // barrier (1) among the non-stragglers, per CTA slot (with LL also
+  // announced to the straggler, which may gate its up-front pushes on it)
+  if (threadIdx.x < W && (int)threadIdx.x != me && ((int)threadIdx.x != P.sigma || P.use_ll))
     st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, P.fstride, s), ep, P.sys_scope);
   // one waiting thread per peer: the acquire loads overlap instead of queueing
   int ok = 1;
@@ -820,16 +821,22 @@ __device__ void ll_phase_b(const LaunchPlan& P, int s, int me, uint32_t ep) {
   // not for the partner to reach that round: non-stragglers send the
   // straggler their partial of its half of their chunk; the straggler sends
   // every owner x_sigma for the owner's half.
+  // ll_gate (per-process mode, set by the host when the previous call used the
+  // LL areas with another layout): a peer may still be consuming words of that
+  // call which this call's up-front pushes would overwrite, so each push waits
+  // for the receiver's arrival in this call (it then finished the previous one).
   if (me == P.sigma) {
     for (int c = 0; c < P.nchunks; ++c) {
       int owner = 0;
 #pragma unroll
       for (int q = 0; q < W; ++q)
         if (P.logical_of_phys[q] == c) owner = q;
+      if (P.ll_gate && !cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + owner, P.fstride, s), ep, P, 0xF00 | c)) return;
       const Words w = words_of(c);
       ll_words<DT, LL_PUSH>(ub, w.cb0, end, nullptr, P.ll[owner] + (size_t)c * kLLChunkWords, w.wa, w.wm, ep, P, 0);
     }
   } else {
+    if (P.ll_gate && !cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + P.sigma, P.fstride, s), ep, P, 0xF10)) return;
     const Words w = words_of(own);
     ll_words<DT, LL_PUSH>(ub, w.cb0, end, nullptr, P.ll[P.sigma] + (size_t)own * kLLChunkWords, w.wm, w.wb, ep, P,
                           0);
@@ -877,13 +884,13 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
   const int NV = P.G * P.sub;   // slices per chunk (flag stride)
   const int V = 16 / P.esize;
   constexpr bool tma = MV == MOVER_TMA;
+  // the straggler reaches barrier (2) (P:349): announce per CTA slot to the others
+  if (me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, P.fstride, s), ep, P.sys_scope);
   if (P.use_ll) {
     ll_phase_b<DT, W>(P, s, me, ep);
     return;
   }
-  // the straggler reaches barrier (2) (P:349): announce per CTA slot to the others
-  if (me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
-    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, P.fstride, s), ep, P.sys_scope);
   char* mine = P.buf[me];
   const int nops = P.nops[me];
   bool ok = true;

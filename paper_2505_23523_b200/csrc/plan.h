@@ -85,7 +85,7 @@ struct LaunchPlan {
   DevState* state;
   uint64_t* ll[kMaxWorld];   // LL area of each physical rank: [chunk][word] (payload | epoch << 32)
   int use_ll;                // Phase B through the LL areas (small chunks)
-  int pad2;
+  int ll_gate;               // LL up-front pushes wait for the receiver's arrival (see ll_phase_b)
   uint64_t sigma_delay_ns;   // team measurement only: straggler CTAs start this late (KIND 4/5)
   uint64_t* trace;           // optional: [rank][slice][op][3] %globaltimer stamps (wait, data, done) of Phase B
   int logical_of_phys[kMaxWorld];

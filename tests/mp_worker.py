@@ -19,6 +19,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def mixed_lengths(count):
+    return [count, count // 3, 17, count // 2 + 5, 4099, count]
+
+
 def worker(rank, world, sigma, count, dtype, port, q):
     try:
         os.environ.setdefault("STRAGGLAR_TIMEOUT_MS", "60000")
@@ -36,7 +40,7 @@ def worker(rank, world, sigma, count, dtype, port, q):
         t = torch.empty(count, dtype=tdt, device="cuda")
         ring = torch.empty(count, dtype=tdt, device="cuda")
         autos = [torch.empty(count, dtype=tdt, device="cuda") for _ in range(4)]
-        base = {k: torch.empty(count, dtype=tdt, device="cuda") for k in ("rhd", "bcast")}   # NEXT N3
+        base = {k: torch.empty(count, dtype=tdt, device="cuda") for k in ("rhd", "bcast", "mixed")}   # NEXT N3
         comm.register(t)
         comm.register(ring)
         for b in base.values():
@@ -60,6 +64,11 @@ def worker(rank, world, sigma, count, dtype, port, q):
         if world & (world - 1) == 0:
             comm.allreduce_rhd(base["rhd"])
         comm.allreduce_bcast(base["bcast"])
+        # back-to-back StragglAR calls of different sizes on prefixes of one
+        # buffer, no host sync: a fast rank's next call (another slice / LL
+        # layout) must not disturb a slow rank's current one
+        for n_el in mixed_lengths(count):
+            comm.allreduce(base["mixed"][:n_el])
         # NEXT row N2: selection for an expected delay (0 and 10 ms)
         used = [S.stragglar_allreduce_auto(autos[0], 0), S.stragglar_allreduce_auto(autos[1], 10_000_000)]
         S.stragglar_allreduce_direct(autos[2])     # NEXT row N1(ii): same result as the schedule
@@ -103,6 +112,12 @@ def run(world, sigma, count, dtype, port):
     want = N.stragglar_allreduce(xs, sigma, dtype)
     rwant = N.ring_allreduce(xs, dtype)
     bwant = {"bcast": N.broadcast_allreduce(xs, sigma, dtype)}
+    state = [x.copy() for x in xs]
+    for n_el in mixed_lengths(count):
+        out = N.stragglar_allreduce([x[:n_el] for x in state], sigma, dtype)
+        for r in range(world):
+            state[r][:n_el] = out[r]
+    bwant["mixed"] = state
     if world & (world - 1) == 0:
         bwant["rhd"] = N.rhd_allreduce(xs, dtype)
     ok = True
