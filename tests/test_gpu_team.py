@@ -606,3 +606,45 @@ def test_baselines_many_subslices(S, algo):
             "bcast": lambda: N.broadcast_allreduce(xs, sigma, dtype)}.get(
                 algo, lambda: N.stragglar_allreduce(xs, sigma, dtype))()
     check_equal(outs, want, xs, dtype, algo)
+
+
+def test_baselines_randomized_and_graph(S):
+    """Seeded random sweep over the NEXT-N3 baselines (world, straggler, dtype,
+    count, pattern), then RHD + Broadcast (split, with the delay) captured in
+    one CUDA graph and replayed on fresh inputs."""
+    rng = np.random.default_rng(2506)
+    for case in range(24):
+        algo = str(rng.choice(["rhd", "bcast"]))
+        n = int(rng.choice([2, 4, 8] if algo == "rhd" else [2, 4, 6, 8]))
+        sigma = int(rng.integers(0, n))
+        dtype = str(rng.choice(["int32", "float32", "bfloat16"]))
+        count = int(rng.choice([rng.integers(1, 64), rng.integers(64, 5000), rng.integers(5000, 600_000)]))
+        pattern = str(rng.choice(["normal", "intval", "bitmask"]))
+        xs, outs = run_team(S, n, sigma, dtype, count, pattern=pattern, config=120 + case, algo=algo)
+        want = N.rhd_allreduce(xs, dtype) if algo == "rhd" else N.broadcast_allreduce(xs, sigma, dtype)
+        check_equal(outs, want, xs, dtype, f"case {case}: {algo} n={n} s={sigma} {dtype} {count} {pattern}")
+    n, sigma, dtype, count = 8, 4, "bfloat16", 150001
+    S.stragglar_team_init(n, sigma)
+    rb = [torch.zeros(count, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+    bb = [torch.zeros_like(b) for b in rb]
+    S.stragglar_team_allreduce_rhd(rb)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(g, stream=side):
+            S.stragglar_team_allreduce_rhd(rb, side)
+            S.stragglar_team_bcast_precondition(bb, side)
+            S.stragglar_team_inject_delay(5_000, side)
+            S.stragglar_team_bcast_complete(bb, side)
+    for it in range(2):
+        xs = make_inputs(n, count, dtype, config=150 + it)
+        for r, b, x in zip(rb, bb, xs):
+            r.copy_(to_dev(x, dtype))
+            b.copy_(to_dev(x, dtype))
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        assert S.stragglar_team_check_error() == 0
+        check_equal([to_host(b, dtype) for b in rb], N.rhd_allreduce(xs, dtype), xs, dtype, f"graph rhd {it}")
+        check_equal([to_host(b, dtype) for b in bb], N.broadcast_allreduce(xs, sigma, dtype), xs, dtype, f"graph bcast {it}")
