@@ -131,6 +131,19 @@ def chunk_bytes(count, parts, esize):
     return (-(-per // v) * v) * esize
 
 
+def host_cpu():
+    """the oracle's timing is quoted as "1 of N host cores" with the CPU model."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
 def oracle_cpu_baseline(world, sigma, dtype, count, max_count=1 << 26):
     """The oracle as it stands, single thread, on a bounded sample."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
@@ -157,6 +170,7 @@ def oracle_cpu_baseline(world, sigma, dtype, count, max_count=1 << 26):
         "kind": "oracle",
         "sample": f"{world} ranks x {sample} {dtype} elements ({'full workload' if scale == 1 else f'1/{scale:g} of it, scaled linearly'}); "
                   f"single-threaded numpy; value = Phase B replay, total = schedule + Phase A + Phase B",
+        "host": host_cpu(),
         "total_us": (t3 - t0) * 1e6 * scale,
         "schedule_us": (t1 - t0) * 1e6,
         "phase_a_us": (t2 - t1) * 1e6 * scale,
@@ -602,7 +616,7 @@ def bench_reference(args):
     tot = statistics.mean(r[0] + r[1] for r in res) * 1e6 * scale
     cpu = {"value": round(post, 1), "unit": "us", "cores": 1, "kind": "oracle",
            "sample": f"{world} ranks x {sample} {dtype} elements per step (1/{scale:g} of the workload, scaled "
-                     "linearly); single-threaded numpy; value = Phase B replay"}
+                     "linearly); single-threaded numpy; value = Phase B replay", "host": host_cpu()}
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(post, 1), "unit": "us", "n_gpus": world_env,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / 1e3, 3), "higher_is_better": False,
