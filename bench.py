@@ -449,8 +449,8 @@ def bench_multi(args):
         dist.init_process_group("gloo")
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    _, _, dtype, count, _ = WORKLOADS[args.workload]
-    sigma = 0
+    _, sigma_w, dtype, count, _ = WORKLOADS[args.workload]
+    sigma = sigma_w if sigma_w < world else 0      # the workload's straggler (config 5: rank 3)
     esize = ESIZE[dtype]
     S_bytes = count * esize
     comm = ProcessComm(sigma)
@@ -549,7 +549,7 @@ def bench_multi(args):
             "dtype": {"float32": "f32", "bfloat16": "bf16", "int32": "i32"}[dtype],
             "data": "synthetic (seeded N(0,1))",
             "config": {"workload": f"{args.workload} per-rank buffer ({count} {dtype}, SUM), {world} ranks, straggler "
-                                   "rank 0; one process per GPU, CUDA IPC over NVLink/NVSwitch",
+                                   f"rank {sigma}; one process per GPU, CUDA IPC over NVLink/NVSwitch",
                        "world": world, "straggler_rank": sigma, "count": count, "delay_us": D_ns / 1e3,
                        "parallelism": f"allreduce{world}"},
             "T_total_us": round(T_tot, 2), "D_meas_us": round(D_meas, 2), "phase_times_in_kernel": phase_times,
@@ -585,9 +585,9 @@ def bench_reference(args):
         return
     world, sigma, dtype, count, desc = WORKLOADS[args.workload]
     if world_env > 1:
-        # our arm at N GPUs runs N ranks (one per GPU, straggler 0) on the same per-rank buffer
-        world, sigma = world_env, 0
-        desc = f"{world} ranks, straggler rank 0, {count} {dtype} per rank SUM"
+        # our arm at N GPUs runs N ranks (one per GPU) on the same per-rank buffer and straggler
+        world, sigma = world_env, (sigma if sigma < world_env else 0)
+        desc = f"{world} ranks, straggler rank {sigma}, {count} {dtype} per rank SUM"
     sample = min(count, 1 << 22)
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import numerics as N

@@ -172,10 +172,12 @@ int stragglar_check_error(int* code);
  * (straggler side), 0x4 copy, 0x5 completion, 0x6/0x7 ring, 0x8 barrier,
  * 0x9/0xA direct completion, 0xC/0xD Broadcast baseline, 0xE RHD. */
 int stragglar_check_error_where(int team, int* code, uint32_t* where);
-/* Phase breakdown of this rank's last stragglar_allreduce(_direct) call, from
- * %globaltimer stamps inside the kernel (this GPU's clock): *t_a_us = kernel
- * start to the end of the rank's Phase A (the straggler has none: ~0),
- * *t_total_us = kernel start to the end of its Phase B.  Synchronizes. */
+/* Phase breakdown of this rank's last call, which must have been
+ * stragglar_allreduce(_direct) (INVALID_ARG otherwise), from %globaltimer
+ * stamps inside the kernel (this GPU's clock): *t_a_us = kernel start to the
+ * end of the rank's Phase A (the straggler has none: ~0), *t_total_us =
+ * kernel start to the end of its Phase B.  The stamps are re-armed on the
+ * device by the previous call (no per-call host work).  Synchronizes. */
 int stragglar_phase_times(double* t_a_us, double* t_total_us);
 int stragglar_finalize(void);
 
@@ -262,7 +264,9 @@ int stragglar_allreduce_auto(void* buf, size_t count, int dtype, int op, void* s
 /* Environment knobs, read once by stragglar_init / stragglar_team_init:
  * STRAGGLAR_MOVER=tma|lsu (data mover), STRAGGLAR_SLICE_BYTES (target bytes
  * per slice, 16384), STRAGGLAR_SLICES (per-process CTA cap, 2 x SMs),
- * STRAGGLAR_SUBSLICES (slices per CTA at most, 1..16) and
+ * STRAGGLAR_SUBSLICES (slices per CTA at most, 1..16; default 16 with
+ * gpu-scope flags (team mode), 1 with system-scope flags (per-process mode,
+ * where each extra flag costs a system-scope fence)) and
  * STRAGGLAR_SUBSLICE_BYTES (their target size on large messages, 131072: each
  * hop hands over ~128 KB pieces, so a forwarded slice is still in L2 when
  * the next hop reads it),

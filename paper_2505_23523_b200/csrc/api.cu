@@ -173,13 +173,17 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   c.bc_pending = false;
   c.timeout_ns = env_u64("STRAGGLAR_TIMEOUT_MS", 10000) * 1000000ull;
   c.slice_bytes = env_u64("STRAGGLAR_SLICE_BYTES", 16384);
-  c.sub = (int)env_u64("STRAGGLAR_SUBSLICES", kMaxSub);
+  c.sys_scope = team ? (int)env_u64("STRAGGLAR_SYS_SCOPE", 0) : 1;
+  // Sub-slices (finer hand-offs) pay with gpu-scope flags (team: Phase B -3.7 %)
+  // but not with system-scope ones: every extra flag costs a fence.acq_rel.sys
+  // (team mode at sys scope: 693 vs 690 us; per-process under MPS, n = 2/4/8:
+  // 275/554/1082 us with them, 187/431/1027 without).
+  c.sub = (int)env_u64("STRAGGLAR_SUBSLICES", c.sys_scope ? 1 : kMaxSub);
   c.sub_bytes = env_u64("STRAGGLAR_SUBSLICE_BYTES", 128 * 1024);
   if (c.sub < 1) c.sub = 1;
   if (c.sub > kMaxSub) c.sub = kMaxSub;
   c.ll_max_chunk = env_u64("STRAGGLAR_LL_MAX_CHUNK", 0);       // off by default: slower on one GPU
   if (c.ll_max_chunk > kLLChunkBytes) c.ll_max_chunk = kLLChunkBytes;
-  c.sys_scope = team ? (int)env_u64("STRAGGLAR_SYS_SCOPE", 0) : 1;
   c.e2e_piece_bytes = env_u64("STRAGGLAR_E2E_PIECE_BYTES", 8ull << 20);
   c.e2e_streams = (int)env_u64("STRAGGLAR_E2E_STREAMS", 1);
   c.flags_bytes = ((size_t)kSlots * G * kMaxSub * sizeof(uint32_t) + 255) / 256 * 256;
@@ -192,9 +196,13 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
     c.state = nullptr;
     return STRAGGLAR_ERR_CUDA;
   };
+  DevState init;
+  std::memset(&init, 0, sizeof(init));
+  init.stamp[0][0] = init.stamp[1][0] = ~0ull;   // armed: the first call's min start
   if (cudaMalloc(&c.flags, nbytes) != cudaSuccess || cudaMemset(c.flags, 0, nbytes) != cudaSuccess ||
       cudaMalloc(&c.state, sizeof(DevState)) != cudaSuccess ||
-      cudaMemset(c.state, 0, sizeof(DevState)) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+      cudaMemcpy(c.state, &init, sizeof(DevState), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess)
     return fail_free();
   for (int p = 0; p < kMaxWorld; ++p) {
     c.peer_flags[p] = nullptr;
@@ -357,14 +365,6 @@ int team_b(void* const* bufs, size_t count, int dtype, void* stream, int which =
   }
   P.nlocal = c.world;
   return launch(which, dtype, P, c.world * P.G, stream);
-}
-
-// Phase stamps of the next fused call: t_start = max (atomicMin target), the
-// two ends = 0 (atomicMax targets).  Stream-ordered, graph-capturable.
-int reset_stamps(Comm& c, void* stream) {
-  CK(cudaMemsetAsync(&c.state->t_start, 0xff, sizeof(uint64_t), (cudaStream_t)stream));
-  CK(cudaMemsetAsync(&c.state->t_a_done, 0, 2 * sizeof(uint64_t), (cudaStream_t)stream));
-  return STRAGGLAR_OK;
 }
 
 int read_error(Comm& c, int* code, uint32_t* where = nullptr) {
@@ -626,7 +626,6 @@ int stragglar_allreduce(void* buf, size_t count, int dtype, int op, void* stream
   if (st || count == 0) return st;
   LaunchPlan P;
   if ((st = proc_plan(buf, count, dtype, &P))) return st;
-  if ((st = reset_stamps(c, stream))) return st;
   // one persistent launch: non-stragglers run Phase A then Phase B, the
   // straggler Phase B only (its delay is whatever precedes it on its stream)
   return launch(K_FUSED, dtype, P, P.G, stream);
@@ -640,7 +639,6 @@ int stragglar_allreduce_direct(void* buf, size_t count, int dtype, int op, void*
   if (st || count == 0) return st;
   LaunchPlan P;
   if ((st = proc_plan(buf, count, dtype, &P))) return st;
-  if ((st = reset_stamps(c, stream))) return st;
   return launch(K_FUSED_DIRECT, dtype, P, P.G, stream);
 }
 
@@ -777,9 +775,10 @@ int stragglar_phase_times(double* t_a_us, double* t_total_us) {
   CK(cudaDeviceSynchronize());
   DevState h;
   CK(cudaMemcpy(&h, g_proc.state, sizeof(h), cudaMemcpyDeviceToHost));
-  if (h.t_start == ~0ull || h.t_b_done < h.t_start) return STRAGGLAR_ERR_INVALID_ARG;   // no fused call yet
-  *t_a_us = (h.t_a_done - h.t_start) * 1e-3;
-  *t_total_us = (h.t_b_done - h.t_start) * 1e-3;
+  const uint64_t* t = h.stamp[h.epoch & 1u];   // the last completed call
+  if (h.epoch == 0 || t[0] == ~0ull || t[2] < t[0]) return STRAGGLAR_ERR_INVALID_ARG;   // not a fused call
+  *t_a_us = (t[1] - t[0]) * 1e-3;
+  *t_total_us = (t[2] - t[0]) * 1e-3;
   return STRAGGLAR_OK;
 }
 

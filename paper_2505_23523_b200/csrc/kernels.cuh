@@ -78,6 +78,11 @@ __device__ __forceinline__ void finish_call(const LaunchPlan& P) {
     const uint32_t prev = atomicAdd(&P.state->exit_count, 1u);
     if (prev == gridDim.x - 1) {
       P.state->exit_count = 0;
+      const uint32_t e = *(volatile uint32_t*)&P.state->epoch + 1u;   // this call
+      uint64_t* nx = P.state->stamp[(e + 1u) & 1u];                      // re-arm for the next call
+      nx[0] = ~0ull;
+      nx[1] = 0;
+      nx[2] = 0;
       __threadfence();
       atomicAdd(&P.state->epoch, 1u);
     }
@@ -1023,8 +1028,9 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_con
   const uint32_t ep = call_epoch(P);
   Pipe pipe = make_pipe(MV == MOVER_TMA);
   const bool stamps = (KIND == 4 || KIND == 5) && P.nlocal == 1;   // per-process fused call
-  if (stamps && threadIdx.x == 0)   // (reset by the host in stream order before the launch)
-    atomicMin(reinterpret_cast<unsigned long long*>(&P.state->t_start), (unsigned long long)globaltimer());
+  uint64_t* stamp = P.state->stamp[ep & 1u];   // armed by the previous call's last CTA (or at init)
+  if (stamps && threadIdx.x == 0)
+    atomicMin(reinterpret_cast<unsigned long long*>(&stamp[0]), (unsigned long long)globaltimer());
   if constexpr (KIND == 4 || KIND == 5) {
     // measurement only (team mode): the straggler's CTAs arrive sigma_delay_ns
     // after the launch (P:405-407 idle time, inside the kernel), so Phase B of
@@ -1038,7 +1044,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_con
   if constexpr (KIND == 0 || KIND == 4 || KIND == 5)
     if (me != P.sigma) rs_body<DT, W, MV>(P, pipe, s, me, ep);
   if (stamps && threadIdx.x == 0)
-    atomicMax(reinterpret_cast<unsigned long long*>(&P.state->t_a_done), (unsigned long long)globaltimer());
+    atomicMax(reinterpret_cast<unsigned long long*>(&stamp[1]), (unsigned long long)globaltimer());
   if constexpr (KIND == 1 || KIND == 4) complete_body<DT, W, MV>(P, pipe, s, me, ep);
   if constexpr (KIND == 3 || KIND == 5) direct_body<DT, W, MV>(P, pipe, s, me, ep);
   if constexpr (KIND == 6 || KIND == 8)
@@ -1048,7 +1054,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_con
     }
   if constexpr (KIND == 7 || KIND == 8) bcast_body<DT, W, MV>(P, pipe, s, me, ep);
   if (stamps && threadIdx.x == 0)
-    atomicMax(reinterpret_cast<unsigned long long*>(&P.state->t_b_done), (unsigned long long)globaltimer());
+    atomicMax(reinterpret_cast<unsigned long long*>(&stamp[2]), (unsigned long long)globaltimer());
   finish_call(P);
 }
 

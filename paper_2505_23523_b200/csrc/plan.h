@@ -49,10 +49,11 @@ struct DevState {
   uint64_t t_release;    // when the last injected delay released
   uint32_t epoch;        // calls completed; the running call uses epoch + 1
   uint32_t exit_count;   // CTAs that finished the call's last kernel (reset by the last one)
-  uint64_t t_start;      // phase stamps of the last fused call (%globaltimer, this GPU):
-  uint64_t t_a_done;     //   min CTA start, max end of Phase A, max end of Phase B
-  uint64_t t_b_done;
-  uint64_t pad;
+  // phase stamps of the per-process fused calls (%globaltimer, this GPU), by
+  // call-epoch parity: [e & 1] = {min CTA start, max end of Phase A, max end of
+  // Phase B} of call e.  The last CTA of call e re-arms [(e + 1) & 1] for the
+  // next call (no host memset per call).
+  uint64_t stamp[2][3];
 };
 
 enum ErrCode : uint32_t { ERR_TIMEOUT = 1, ERR_BAD_PLAN = 2 };

@@ -46,6 +46,7 @@ def test_multiprocess_ipc(world, sigma, count, dtype, mover):
     if mover.endswith("+sub"):
         env["STRAGGLAR_SLICE_BYTES"] = "1024"       # 8 CTAs per rank (mp_worker), ~4 KB slices: 16 per CTA
         env["STRAGGLAR_SUBSLICE_BYTES"] = "4096"
+        env["STRAGGLAR_SUBSLICES"] = "16"            # (default 1 at system scope)
     r = subprocess.run([sys.executable, os.path.join(HERE, "mp_worker.py"), str(world), str(sigma), str(count), dtype,
                         str(_port())], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
