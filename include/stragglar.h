@@ -251,15 +251,28 @@ int stragglar_team_finalize(void);
  * Host only; world must be 2, 4 or 8 (or any power of two up to 64). */
 int stragglar_select(int world, double bytes, double delay_s, double alpha_s, double beta_s_per_byte,
                      int* use_stragglar, double* critical_delay_s);
+/* Algorithm codes of stragglar_select_algorithm / stragglar_allreduce_auto. */
+enum { STRAGGLAR_ALGO_RING = 0, STRAGGLAR_ALGO_STRAGGLAR = 1, STRAGGLAR_ALGO_RHD = 2 };
+/* The same model over every algorithm the library has that does not need the
+ * straggler-specific precondition, predicted completion from the
+ * non-stragglers' start: StragglAR max(delay, T_RS) + T_SAR; the
+ * bulk-synchronous Ring delay + T_Ring and RHD delay + T_RHD (T_RHD = 2 log2 n
+ * alpha + 2(n-1)/n bytes beta; powers of two only).  *algo = the
+ * fastest (ties: StragglAR, then Ring), *t_pred_s (may be NULL) = its time.
+ * With small buffers RHD's 2 log2 n latency terms win, as the paper measured
+ * (P:398-400); with a masking delay and large buffers StragglAR does. */
+int stragglar_select_algorithm(int world, double bytes, double delay_s, double alpha_s, double beta_s_per_byte,
+                               int* algo, double* t_pred_s);
 /* Cost-model constants of the per-process communicator used by
  * stragglar_allreduce_auto (defaults: alpha = 3 us; beta = 1/(770 GB/s),
  * the measured B200 peer-copy bandwidth per direction). */
 int stragglar_set_cost_model(double alpha_s, double beta_s_per_byte);
-/* Collective: every rank passes the same expected straggler delay; runs
- * StragglAR if stragglar_select says so, else the Ring; *used_stragglar tells
- * which (may be NULL). */
+/* Collective: every rank passes the same expected straggler delay; runs the
+ * algorithm stragglar_select_algorithm picks (StragglAR, Ring or RHD) with the
+ * communicator's cost model; *used_algorithm (may be NULL) = its
+ * STRAGGLAR_ALGO_* code (1 = StragglAR, 0 = Ring as before, 2 = RHD). */
 int stragglar_allreduce_auto(void* buf, size_t count, int dtype, int op, void* stream, uint64_t expected_delay_ns,
-                             int* used_stragglar);
+                             int* used_algorithm);
 
 /* Environment knobs, read once by stragglar_init / stragglar_team_init:
  * STRAGGLAR_MOVER=tma|lsu (data mover), STRAGGLAR_SLICE_BYTES (target bytes

@@ -714,6 +714,39 @@ int stragglar_select(int world, double bytes, double delay_s, double alpha_s, do
   return STRAGGLAR_OK;
 }
 
+int stragglar_select_algorithm(int world, double bytes, double delay_s, double alpha_s, double beta, int* algo,
+                               double* t_pred_s) {
+  if (!algo) return STRAGGLAR_ERR_INVALID_ARG;
+  double crit = 0.0;
+  int use = 0;
+  int st = stragglar_select(world, bytes, delay_s, alpha_s, beta, &use, &crit);
+  if (st) return st;
+  // completion from the non-stragglers' start: StragglAR hides its
+  // ReduceScatter in the delay; the bulk-synchronous baselines start after it
+  const double n = world, R = (double)generate_any(world).size();
+  const double t_rs = (world > 2 ? alpha_s : 0.0) + (n - 2) / (n - 1) * bytes * beta;
+  const double t_sar = (delay_s > t_rs ? delay_s : t_rs) + R * alpha_s + R / (n - 1) * bytes * beta;
+  const double t_ring = delay_s + 2 * (n - 1) * alpha_s + 2 * (n - 1) / n * bytes * beta;
+  double best = t_sar;
+  int a = STRAGGLAR_ALGO_STRAGGLAR;
+  if (t_ring < best) {
+    best = t_ring;
+    a = STRAGGLAR_ALGO_RING;
+  }
+  if ((world & (world - 1)) == 0) {
+    int L = 0;
+    while ((1 << L) < world) ++L;
+    const double t_rhd = delay_s + 2 * L * alpha_s + 2 * (n - 1) / n * bytes * beta;
+    if (t_rhd < best) {
+      best = t_rhd;
+      a = STRAGGLAR_ALGO_RHD;
+    }
+  }
+  *algo = a;
+  if (t_pred_s) *t_pred_s = best;
+  return STRAGGLAR_OK;
+}
+
 int stragglar_set_cost_model(double alpha_s, double beta) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_proc.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
@@ -724,7 +757,7 @@ int stragglar_set_cost_model(double alpha_s, double beta) {
 }
 
 int stragglar_allreduce_auto(void* buf, size_t count, int dtype, int op, void* stream, uint64_t expected_delay_ns,
-                             int* used_stragglar) {
+                             int* used_algorithm) {
   double a, b;
   int world;
   {
@@ -736,11 +769,15 @@ int stragglar_allreduce_auto(void* buf, size_t count, int dtype, int op, void* s
   }
   const int es = esize_of(dtype);
   if (!es) return STRAGGLAR_ERR_UNSUPPORTED;
-  int use = 1;
-  int st = stragglar_select(world, (double)count * es, expected_delay_ns * 1e-9, a, b, &use, nullptr);
+  int algo = STRAGGLAR_ALGO_STRAGGLAR;
+  int st = stragglar_select_algorithm(world, (double)count * es, expected_delay_ns * 1e-9, a, b, &algo, nullptr);
   if (st) return st;
-  if (used_stragglar) *used_stragglar = use;
-  return use ? stragglar_allreduce(buf, count, dtype, op, stream) : stragglar_allreduce_ring(buf, count, dtype, op, stream);
+  if (used_algorithm) *used_algorithm = algo;
+  switch (algo) {
+    case STRAGGLAR_ALGO_RING: return stragglar_allreduce_ring(buf, count, dtype, op, stream);
+    case STRAGGLAR_ALGO_RHD: return stragglar_allreduce_rhd(buf, count, dtype, op, stream);
+    default: return stragglar_allreduce(buf, count, dtype, op, stream);
+  }
 }
 
 int stragglar_barrier(void* stream) {

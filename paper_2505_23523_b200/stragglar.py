@@ -68,6 +68,8 @@ _SIGS = {
     "stragglar_phase_times": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], _c_int),
     "stragglar_select": ([_c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                           ctypes.POINTER(_c_int), ctypes.POINTER(ctypes.c_double)], _c_int),
+    "stragglar_select_algorithm": ([_c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                    ctypes.POINTER(_c_int), ctypes.POINTER(ctypes.c_double)], _c_int),
     "stragglar_set_cost_model": ([ctypes.c_double, ctypes.c_double], _c_int),
     "stragglar_allreduce_auto": ([_vp, _c_size, _c_int, _c_int, _vp, _c_u64, ctypes.POINTER(_c_int)], _c_int),
     "stragglar_team_init": ([_c_int, _c_int], _c_int),
@@ -229,17 +231,30 @@ def stragglar_select(world: int, nbytes: float, delay_s: float, alpha_s: float, 
     return bool(use.value), crit.value
 
 
+ALGO_RING, ALGO_STRAGGLAR, ALGO_RHD = 0, 1, 2
+ALGO_NAMES = {ALGO_RING: "ring", ALGO_STRAGGLAR: "stragglar", ALGO_RHD: "rhd"}
+
+
+def stragglar_select_algorithm(world: int, nbytes: float, delay_s: float, alpha_s: float, beta_s_per_byte: float):
+    """-> (algorithm name, predicted completion in s) — see include/stragglar.h."""
+    a, t = _c_int(0), ctypes.c_double(0.0)
+    _ck("stragglar_select_algorithm",
+        _lib.stragglar_select_algorithm(world, float(nbytes), float(delay_s), float(alpha_s), float(beta_s_per_byte),
+                                        ctypes.byref(a), ctypes.byref(t)))
+    return ALGO_NAMES[a.value], t.value
+
+
 def stragglar_set_cost_model(alpha_s: float, beta_s_per_byte: float) -> None:
     _ck("stragglar_set_cost_model", _lib.stragglar_set_cost_model(float(alpha_s), float(beta_s_per_byte)))
 
 
-def stragglar_allreduce_auto(t, expected_delay_ns: int, stream=None) -> bool:
-    """Returns True if StragglAR ran, False if the Ring did."""
+def stragglar_allreduce_auto(t, expected_delay_ns: int, stream=None) -> str:
+    """Runs the algorithm the cost model picks; returns its name ("stragglar", "ring" or "rhd")."""
     used = _c_int(0)
     _ck("stragglar_allreduce_auto",
         _lib.stragglar_allreduce_auto(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream),
                                       int(expected_delay_ns), ctypes.byref(used)))
-    return bool(used.value)
+    return ALGO_NAMES[used.value]
 
 
 def stragglar_allreduce_direct(t, stream=None) -> None:

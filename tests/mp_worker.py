@@ -72,7 +72,7 @@ def worker(rank, world, sigma, count, dtype, port, q):
         # NEXT row N2: selection for an expected delay (0 and 10 ms)
         used = [S.stragglar_allreduce_auto(autos[0], 0), S.stragglar_allreduce_auto(autos[1], 10_000_000)]
         S.stragglar_allreduce_direct(autos[2])     # NEXT row N1(ii): same result as the schedule
-        used.append(True)
+        used.append("stragglar")
         # end to end from pinned host memory, pipelined pieces, result back in host memory
         hin = host.clone().pin_memory()
         hout = torch.empty_like(hin).pin_memory()
@@ -83,7 +83,7 @@ def worker(rank, world, sigma, count, dtype, port, q):
         out = t.view(host.dtype).cpu().numpy()
         rout = ring.view(host.dtype).cpu().numpy()
         aout = [(u, a.view(host.dtype).cpu().numpy().tobytes()) for u, a in zip(used, autos[:3])]
-        aout.append((True, hout.numpy().tobytes()))
+        aout.append(("stragglar", hout.numpy().tobytes()))
         bout = {k: b.view(host.dtype).cpu().numpy().tobytes() for k, b in base.items()}
         dist.barrier()
         comm.close()
@@ -106,6 +106,7 @@ def run(world, sigma, count, dtype, port):
     for p in procs:
         p.join(timeout=60)
     from oracle import numerics as N
+    from paper_2505_23523_b200 import stragglar as S
     from paper_2505_23523_b200.inputs import make_inputs
 
     xs = make_inputs(world, count, dtype, config=7)
@@ -139,12 +140,15 @@ def run(world, sigma, count, dtype, port):
             print(f"rank {r}: ring result differs from the oracle")
             ok = False
         for used, b in aout:
-            if b != (want[r] if used else rwant[r]).tobytes():
-                print(f"rank {r}: auto ({'stragglar' if used else 'ring'}) result differs from the oracle")
+            w = {"stragglar": want, "ring": rwant}.get(used) or N.rhd_allreduce(xs, dtype)
+            if b != w[r].tobytes():
+                print(f"rank {r}: auto ({used}) result differs from the oracle")
                 ok = False
-        if not aout[1][0]:
-            print(f"rank {r}: a 10 ms expected delay did not select StragglAR")
-            ok = False
+        esz = 2 if dtype == "bfloat16" else 4
+        for (used, _), d in zip(aout[:2], (0.0, 10e-3)):
+            if used != S.stragglar_select_algorithm(world, count * esz, d, 3e-6, 1 / 770e9)[0]:
+                print(f"rank {r}: auto picked {used}, not the cost model's choice for delay {d}")
+                ok = False
     return ok
 
 

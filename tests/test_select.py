@@ -59,3 +59,37 @@ def test_large_buffers_without_delay_prefer_ring_at_n8(S):
 def test_select_rejects_bad_world(S):
     with pytest.raises(S.StragglarError):
         S.stragglar_select(5, 1.0, 0.0, 0.0, 1.0)
+
+
+@pytest.mark.parametrize("n", [4, 8, 16])
+@pytest.mark.parametrize("nbytes", [2 ** 20, 2 ** 26, 2 ** 30])
+@pytest.mark.parametrize("delay", [0.0, 1e-4, 2e-3])
+@pytest.mark.parametrize("alpha", [0.0, 3e-6])
+def test_select_algorithm_is_the_model_argmin(S, n, nbytes, delay, alpha):
+    """N2 + N3: the library picks the fastest of StragglAR / Ring / RHD by
+    completion from the non-stragglers' start.  The baselines' costs
+    are the oracle's Table-1 forms; StragglAR's ReduceScatter is
+    this implementation's one direct-pull step (alpha + (n-2)/(n-1) s beta),
+    which equals the oracle's ReduceScatter at alpha = 0."""
+    beta = 1 / 770e9
+    algo, t = S.stragglar_select_algorithm(n, nbytes, delay, alpha, beta)
+    t_rs = alpha + (n - 2) / (n - 1) * nbytes * beta
+    if alpha == 0.0:
+        assert t_rs == pytest.approx(C.t_reduce_scatter(n - 1, nbytes, 0.0, beta), rel=1e-12)
+    cand = {"stragglar": max(delay, t_rs) + C.t_stragglar(n, nbytes, alpha, beta),
+            "ring": delay + C.t_ring(n, nbytes, alpha, beta),
+            "rhd": delay + C.t_rhd(n, nbytes, alpha, beta)}
+    best = min(cand.values())
+    assert t == pytest.approx(best, rel=1e-12)
+    assert cand[algo] == pytest.approx(best, rel=1e-12)
+    order = ["stragglar", "ring", "rhd"]     # tie-break
+    assert algo == next(a for a in order if cand[a] <= best * (1 + 1e-12))
+
+
+def test_small_buffers_pick_rhd_large_delayed_pick_stragglar(S):
+    """at small sizes the latency-optimal RHD wins; with a delay
+    that masks the ReduceScatter and a large buffer StragglAR wins."""
+    beta = 1 / 770e9
+    assert S.stragglar_select_algorithm(8, 2 ** 20, 0.0, 3e-6, beta)[0] == "rhd"
+    assert S.stragglar_select_algorithm(8, 2 ** 30, 2e-3, 3e-6, beta)[0] == "stragglar"
+    assert S.stragglar_select_algorithm(6, 2 ** 20, 0.0, 3e-6, beta)[0] != "rhd"   # RHD needs a power of two
