@@ -16,11 +16,13 @@ by the section / algorithm / equation the line falls in.
 
 Modules
 -------
-schedule   Algorithm 1 schedule generator, Ring schedule,
-           contributor-set verifier, per-round invariants of App. A.
+schedule   Algorithm 1 schedule generator, Appendix B matcher,
+           Ring / RHD / Broadcast baseline schedules, contributor-set
+           verifier, per-round invariants of App. A.
 numerics   Plain definition of the AllReduce result, Phase A (ReduceScatter among
-           non-stragglers) and the snapshot replay of Phase B, ring-order
-           oracle, bf16 round-to-nearest-even, tolerance of SURVEY.md §8(c).6.
+           non-stragglers) and the snapshot replay of Phase B, direct
+           completion, ring-order / butterfly (RHD) / Broadcast oracles, bf16
+           round-to-nearest-even, tolerance of SURVEY.md §8(c).6.
 cost       alpha-beta closed forms of Table 1, T_RS, critical delay
            (P:423-424).
 
