@@ -20,9 +20,20 @@ import torch.distributed as dist
 
 
 class StragglarHookState:
-    def __init__(self, comm, use_direct: bool = False):
+    """mode: "schedule" (StragglAR, Algorithm 1), "direct" (one-round direct
+    completion, NEXT N1(ii)) or "auto": P:744-748 — only the first AllReduce of
+    a backward pass meets the straggler (the later ones are synchronised by it),
+    so bucket 0 runs the cost model's choice for `expected_delay_ns` and every
+    later bucket its choice for no delay (RHD / Ring / StragglAR by size,
+    stragglar_allreduce_auto)."""
+
+    def __init__(self, comm, use_direct: bool = False, mode: str = None, expected_delay_ns: int = 0):
         self.comm = comm
-        self.use_direct = use_direct
+        self.mode = mode or ("direct" if use_direct else "schedule")
+        if self.mode not in ("schedule", "direct", "auto"):
+            raise ValueError(f"unknown mode {self.mode}")
+        self.expected_delay_ns = int(expected_delay_ns)
+        self.picks: list = []        # "auto": (bucket index, algorithm) per call, for inspection
         self._registered: list = []  # (data_ptr, nbytes) of peer-mapped bucket buffers
 
     def _ensure_registered(self, buf: torch.Tensor) -> None:
@@ -38,8 +49,11 @@ def stragglar_hook(state: StragglarHookState, bucket: dist.GradBucket) -> torch.
     buf = bucket.buffer()
     state._ensure_registered(buf)
     buf.div_(state.comm.world)
-    if state.use_direct:
+    if state.mode == "direct":
         state.comm.lib.stragglar_allreduce_direct(buf)
+    elif state.mode == "auto":
+        delay = state.expected_delay_ns if bucket.index() == 0 else 0
+        state.picks.append((bucket.index(), state.comm.lib.stragglar_allreduce_auto(buf, delay)))
     else:
         state.comm.allreduce(buf)
     fut: torch.futures.Future[torch.Tensor] = torch.futures.Future()

@@ -19,7 +19,7 @@ def model():
                                torch.nn.GELU(), torch.nn.Linear(129, 7)).cuda()
 
 
-def worker(rank, world, sigma, port, use_direct, q):
+def worker(rank, world, sigma, port, mode, q):
     try:
         os.environ.setdefault("STRAGGLAR_SLICES", "8")
         os.environ.setdefault("STRAGGLAR_TIMEOUT_MS", "60000")
@@ -30,7 +30,8 @@ def worker(rank, world, sigma, port, use_direct, q):
 
         comm = ProcessComm(sigma)
         ddp_s = torch.nn.parallel.DistributedDataParallel(model(), bucket_cap_mb=0.25)
-        ddp_s.register_comm_hook(StragglarHookState(comm, use_direct), stragglar_hook)
+        state = StragglarHookState(comm, mode=mode, expected_delay_ns=10_000_000)
+        ddp_s.register_comm_hook(state, stragglar_hook)
         ddp_r = torch.nn.parallel.DistributedDataParallel(model(), bucket_cap_mb=0.25)
         g = torch.Generator().manual_seed(100 + rank)
         for step in range(3):
@@ -48,6 +49,11 @@ def worker(rank, world, sigma, port, use_direct, q):
             if err > 1e-5 or not same:
                 q.put((rank, f"step {step}: rel err {err:.3g}, ranks identical {same}"))
                 return
+        if mode == "auto":
+            # bucket 0 behind a 10 ms expected delay -> StragglAR; later buckets the no-delay choice
+            if not state.picks or any(a != "stragglar" for i, a in state.picks if i == 0):
+                q.put((rank, f"auto picks {state.picks[:6]}"))
+                return
         code = comm.lib.stragglar_check_error()
         comm.close()
         q.put((rank, "ok" if code == 0 else f"device error {code}"))
@@ -57,10 +63,10 @@ def worker(rank, world, sigma, port, use_direct, q):
 
 
 if __name__ == "__main__":
-    world, sigma, port, use_direct = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4] == "direct"
+    world, sigma, port, mode = int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=worker, args=(r, world, sigma, port, use_direct, q)) for r in range(world)]
+    ps = [ctx.Process(target=worker, args=(r, world, sigma, port, mode, q)) for r in range(world)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=600) for _ in range(world))

@@ -66,7 +66,7 @@ def test_watchdog_reports_missing_peer():
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
 
-@pytest.mark.parametrize("world,sigma,mode", [(2, 1, "schedule"), (4, 2, "schedule"), (4, 0, "direct")])
+@pytest.mark.parametrize("world,sigma,mode", [(2, 1, "schedule"), (4, 2, "schedule"), (4, 0, "direct"), (4, 3, "auto")])
 def test_ddp_comm_hook(world, sigma, mode):
     """data-parallel training with StragglAR as the
     gradient AllReduce — DDP comm hook vs DDP's default hook, 3 steps."""
