@@ -30,3 +30,25 @@ def test_sanitizer_clean(tool, mover):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-3000:]
     assert "sanitize step ok" in out
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+def test_sanitizer_clean_ipc_ranks(tool):
+    """The per-process mode: two ranks (torchrun, each under its own
+    compute-sanitizer) exchanging CUDA-IPC peer mappings; every algorithm runs
+    once and is checked against the oracle inside tests/mp_rank_sanitize.py."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(cs):
+        pytest.skip("compute-sanitizer not installed")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--standalone", "--local-addr", "127.0.0.1",
+                        "--nproc-per-node", "2", "--no-python", cs, "--tool", tool, "--error-exitcode", "9",
+                        sys.executable, os.path.join(ROOT, "tests", "mp_rank_sanitize.py")],
+                       capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-3000:]
+    assert out.count("mismatches []") == 2, out[-3000:]
