@@ -573,15 +573,8 @@ __device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t
 // bcast_body: the straggler exchanges its entire buffer with its partner
 // (logical rank 0; half-split and fused with the add as in B1), and the full
 // sum is copied on along the doubling tree of RankPrograms::bc_sender, s
-// bytes per copy.  CTA s covers the union of its `sub` slices of every chunk.
-
-// Bytes [a, b) of chunk c covered by CTA slot s.
-__device__ __forceinline__ void cta_chunk_bytes(const LaunchPlan& P, int c, int s, uint64_t& a, uint64_t& b) {
-  const int NV = P.G * P.sub, V = 16 / P.esize;
-  const Range cr = chunk_range(P, c);
-  a = slice_of(cr.lo, cr.hi, s * P.sub, NV, V).lo * P.esize;
-  b = slice_of(cr.lo, cr.hi, s * P.sub + P.sub - 1, NV, V).hi * P.esize;
-}
+// bytes per copy.  The precondition is chunk-sliced (CTA s: its `sub` slices of
+// every chunk); the completion slices the whole buffer contiguously.
 
 template <int MV>
 __device__ __forceinline__ void move_bytes(Pipe& pipe, char* dst, const char* src, uint64_t a, uint64_t b) {
@@ -629,57 +622,69 @@ __device__ void ag_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t
   }
   // the partner tells the straggler its operand is ready; the others tell
   // their sender in the doubling tree that they may now be overwritten
-  if (me == P.bc_partner)
-    cta_signal(flag_at(P.flags[P.sigma], SLOT_BC_AGDONE, P.fstride, s), ep, P.sys_scope);
-  else
+  if (me == P.bc_partner) {
+    // (also to itself: its completion slices the buffer differently, so each
+    // of its CTAs waits for all of them)
+    __syncthreads();
+    if (threadIdx.x == 0) st_release(flag_at(P.flags[P.sigma], SLOT_BC_AGDONE, P.fstride, s), ep, P.sys_scope);
+    if (threadIdx.x == 1) st_release(flag_at(P.flags[me], SLOT_BC_AGDONE, P.fstride, s), ep, P.sys_scope);
+  } else
     cta_signal(flag_at(P.flags[P.bc_sender[me]], SLOT_BC_READY + me, P.fstride, s), ep, P.sys_scope);
 }
 
+// Whole-CTA wait for slot `slot` of rank `me` at every CTA index 0..P.G-1 (one
+// waiting thread per flag, so the acquire loads overlap).
+__device__ __forceinline__ bool cta_wait_all(const LaunchPlan& P, int me, int slot, uint32_t ep, uint32_t where) {
+  int ok = 1;
+  for (int i = threadIdx.x; i < P.G; i += blockDim.x)
+    ok &= spin_wait(flag_at(P.flags[me], slot, P.fstride, i), ep, P, where) ? 1 : 0;
+  return __syncthreads_and(ok);
+}
+
+// The completion treats the buffer as a whole (the paper's Broadcast moves s
+// bytes per round): CTA s owns the s-th of G contiguous slices of the
+// entire buffer, so each step is one TMA pipeline over one range.  Its inputs
+// come from the chunk-sliced precondition, so it starts after the peer's
+// whole precondition (all G flags).
 template <int DT, int W, int MV>
 __device__ void bcast_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
-  const int NV = P.G * P.sub, V = 16 / P.esize;
   const int p0 = P.bc_partner, sig = P.sigma;
   char* mine = P.buf[me];
+  const Range sl = slice_of(0, P.count, s, P.G, 16 / P.esize);
+  const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize;
   bool ok;
   if (me == sig || me == p0) {
     const int peer = (me == sig) ? p0 : sig;
     if (me == sig) {
       // the straggler arrives (barrier (2)); its operand is the partner's full non-straggler sum
       if (threadIdx.x == 0) st_release(flag_at(P.flags[p0], SLOT_ARRIVE + sig, P.fstride, s), ep, P.sys_scope);
-      ok = cta_wait(flag_at(P.flags[me], SLOT_BC_AGDONE, P.fstride, s), ep, P, 0xD00);
+      ok = cta_wait_all(P, me, SLOT_BC_AGDONE, ep, 0xD00);
     } else {
-      ok = cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + sig, P.fstride, s), ep, P, 0xD01);
+      ok = cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + sig, P.fstride, s), ep, P, 0xD01) &&
+           cta_wait_all(P, me, SLOT_BC_AGDONE, ep, 0xD04);
     }
     if (ok) {
       // the exchange of the entire buffer: the partner computes the first half
-      // of every range, the straggler the second; both halves land at both ends
-      for (int c = 0; c < P.nchunks; ++c) {
-        uint64_t a, b;
-        cta_chunk_bytes(P, c, s, a, b);
-        const uint64_t nv = (b - a + 15) / 16;
-        const uint64_t m = a + (nv / 2) * 16 < b ? a + (nv / 2) * 16 : b;
-        if (me == p0)
-          add_bytes<DT, MV>(P, pipe, mine, P.buf[peer], mine, P.buf[peer], a, m);
-        else
-          add_bytes<DT, MV>(P, pipe, mine, P.buf[peer], P.buf[peer], mine, m, b);
-      }
+      // of the slice, the straggler the second; both halves land at both ends
+      const uint64_t nv = (b - a + 15) / 16;
+      const uint64_t m = a + (nv / 2) * 16 < b ? a + (nv / 2) * 16 : b;
+      if (me == p0)
+        add_bytes<DT, MV>(P, pipe, mine, P.buf[peer], mine, P.buf[peer], a, m);
+      else
+        add_bytes<DT, MV>(P, pipe, mine, P.buf[peer], P.buf[peer], mine, m, b);
       cta_signal(flag_at(P.flags[peer], SLOT_HAVE, P.fstride, s), ep, P.sys_scope);
       ok = cta_wait(flag_at(P.flags[me], SLOT_HAVE, P.fstride, s), ep, P, 0xD02);
     }
   } else {
     ok = cta_wait(flag_at(P.flags[me], SLOT_HAVE, P.fstride, s), ep, P, 0xD03);
   }
-  (void)V;
-  // holders copy the entire (CTA-range) buffer on, one receiver per round
+  // holders copy the slice on, one receiver per round, once the receiver's
+  // whole precondition is done (it no longer writes its own buffer)
   for (int rd = 1; ok && rd < W; ++rd)
     for (int q = 0; ok && q < W; ++q) {
       if (P.bc_sender[q] != me || P.bc_round[q] != rd) continue;
-      if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_BC_READY + q, P.fstride, s), ep, P, 0xD10 | q))) break;
-      for (int c = 0; c < P.nchunks; ++c) {
-        uint64_t a, b;
-        cta_chunk_bytes(P, c, s, a, b);
-        move_bytes<MV>(pipe, P.buf[q], mine, a, b);
-      }
+      if (!(ok = cta_wait_all(P, me, SLOT_BC_READY + q, ep, 0xD10 | q))) break;
+      move_bytes<MV>(pipe, P.buf[q], mine, a, b);
       cta_signal(flag_at(P.flags[q], SLOT_HAVE, P.fstride, s), ep, P.sys_scope);
     }
 }
