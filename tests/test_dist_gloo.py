@@ -46,6 +46,15 @@ class FakeLib:
     def stragglar_allreduce(self, t, stream=None):
         self.calls.append(("allreduce", t.ptr))
 
+    def stragglar_allreduce_ring(self, t, stream=None):
+        self.calls.append(("ring", t.ptr))
+
+    def stragglar_allreduce_rhd(self, t, stream=None):
+        self.calls.append(("rhd", t.ptr))
+
+    def stragglar_allreduce_bcast(self, t, stream=None):
+        self.calls.append(("bcast", t.ptr))
+
     def stragglar_finalize(self):
         self.calls.append(("finalize",))
 
@@ -58,6 +67,9 @@ def _worker(rank, world, port, q):
     comm = ProcessComm(straggler_rank=1, lib=lib)
     comm.register(FakeTensor(1000 + rank))
     comm.allreduce(FakeTensor(1000 + rank))
+    comm.allreduce_ring(FakeTensor(1000 + rank))
+    comm.allreduce_rhd(FakeTensor(1000 + rank))
+    comm.allreduce_bcast(FakeTensor(1000 + rank))
     comm.close()
     q.put((rank, lib.calls))
     dist.destroy_process_group()
@@ -83,4 +95,5 @@ def test_handle_exchange_gloo(world):
         assert calls[1] == ("import_handles", want_handles, world)
         assert calls[2] == ("import_buffer", 1000 + r, want_bufs, world)
         assert calls[3] == ("allreduce", 1000 + r)
-        assert calls[4] == ("finalize",)
+        assert calls[4:7] == [("ring", 1000 + r), ("rhd", 1000 + r), ("bcast", 1000 + r)]
+        assert calls[7] == ("finalize",)
