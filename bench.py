@@ -284,6 +284,20 @@ def bench_team(args):
     torch.cuda.synchronize()
     T_ring = statistics.mean(e0.elapsed_time(e1) * 1e3 for e0, e1 in rs)
 
+    # the single-launch call (Phase A then B in one persistent kernel, KIND 4: the kernel the
+    # per-process stragglar_allreduce launches), no delay
+    for _ in range(args.warmup):
+        S.stragglar_team_allreduce(ring)
+    torch.cuda.synchronize()
+    fr = [(ev(), ev()) for _ in range(args.steps)]
+    torch.cuda._sleep(4_000_000)
+    for e0, e1 in fr:
+        e0.record()
+        S.stragglar_team_allreduce(ring)
+        e1.record()
+    torch.cuda.synchronize()
+    T_fused = statistics.mean(e0.elapsed_time(e1) * 1e3 for e0, e1 in fr)
+
     # NEXT N3 baselines on the same buffers
     T_rhd = None
     if world & (world - 1) == 0:
@@ -405,6 +419,13 @@ def bench_team(args):
             "speedup_vs_bcast_post": round(T_bcast / T_post, 3),
             "note": "team mode: every link is HBM, so an algorithm costs its total bytes (RHD 5(n-1)S like the "
                     "Ring; Broadcast completion 2nS like StragglAR's Phase B 2n(n-1)C), not its busiest port",
+        },
+        "fused_call": {
+            "what": "stragglar_team_allreduce: Phase A + Phase B in one launch (k_phase KIND 4, the per-process "
+                    "call's kernel), no delay",
+            "us": round(T_fused, 2), "hbm_bytes": bytes_A + bytes_B,
+            "hbm_GBps": round((bytes_A + bytes_B) / (T_fused * 1e-6) / 1e9, 1),
+            "vs_split_nodelay_us": round(T_A + T_post, 2),
         },
         "phaseA_hbm_GBps": round(bytes_A / (T_A * 1e-6) / 1e9, 1),
         "ring_hbm_GBps": round(bytes_ring / (T_ring * 1e-6) / 1e9, 1),

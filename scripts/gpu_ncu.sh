@@ -14,8 +14,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpuru
 fi
 # kernel-name regexes on the demangled names: k_phase<dtype, world, mover, KIND>
 declare -A PAT=( [phaseB]='k_phase<.*\(int\)1>' [phaseA]='k_phase<.*\(int\)0>' [ring]='k_ring<' [direct]='k_phase<.*\(int\)3>'
-                  [rhd]='k_rhd<' [bcast]='k_phase<.*\(int\)7>' )
-for k in phaseB phaseA ring direct rhd bcast; do
+                  [rhd]='k_rhd<' [bcast]='k_phase<.*\(int\)7>' [fused]='k_phase<.*\(int\)4>' )
+for k in phaseB phaseA ring direct rhd bcast fused; do
   timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
       -k "regex:${PAT[$k]}" -s 1 -c 1 \
       -o gpurun_out/${TAG}_$k python scripts/profile_step.py > gpurun_out/${TAG}_$k.log 2>&1; echo "$k rc=$?"
@@ -23,7 +23,7 @@ done
 # summaries on the box (the .ncu-rep files are large); keep only the Phase-B report
 NCU_SUMMARY_DIR=gpurun_out/ncu_summary python scripts/ncu_summary.py $TAG gpurun_out/${TAG}_phaseB.ncu-rep \
     gpurun_out/${TAG}_phaseA.ncu-rep gpurun_out/${TAG}_ring.ncu-rep gpurun_out/${TAG}_direct.ncu-rep \
-    gpurun_out/${TAG}_rhd.ncu-rep gpurun_out/${TAG}_bcast.ncu-rep --traffic > /dev/null
+    gpurun_out/${TAG}_rhd.ncu-rep gpurun_out/${TAG}_bcast.ncu-rep gpurun_out/${TAG}_fused.ncu-rep --traffic > /dev/null
 rm -f gpurun_out/${TAG}_phaseA.ncu-rep gpurun_out/${TAG}_ring.ncu-rep gpurun_out/${TAG}_direct.ncu-rep \
-    gpurun_out/${TAG}_rhd.ncu-rep gpurun_out/${TAG}_bcast.ncu-rep
+    gpurun_out/${TAG}_rhd.ncu-rep gpurun_out/${TAG}_bcast.ncu-rep gpurun_out/${TAG}_fused.ncu-rep
 du -sh gpurun_out

@@ -28,6 +28,7 @@ for _ in range(steps):
     S.stragglar_team_allreduce_ring(bufs)
     S.stragglar_team_reduce_scatter(bufs)
     S.stragglar_team_complete_direct(bufs)
+    S.stragglar_team_allreduce(bufs)               # Phase A + B in one launch (KIND 4)
     S.stragglar_team_allreduce_rhd(bufs)           # NEXT N3 baselines
     S.stragglar_team_bcast_precondition(bufs)
     S.stragglar_team_bcast_complete(bufs)
