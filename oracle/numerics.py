@@ -264,15 +264,15 @@ def rhd_allreduce(inputs: Sequence[np.ndarray], dtype: str) -> List[np.ndarray]:
 def plain_rhd_allreduce(inputs: Sequence[np.ndarray], dtype: str) -> np.ndarray:
     """Definition of the RHD result, written elementwise with no chunks or
     rounds: a butterfly of pairwise sums, level k (k = 0..log n - 1) adding the
-    values of ranks i and i XOR n/2^(k+1) (halves with one partner,
-    then quarters with the next), one rounding per level.  Every rank ends with
-    the same bits (each add is commutative)."""
+    values of ranks i and i XOR 2^k (halves with one partner, then
+    quarters with the next; partner order as SPEC S:266), one rounding per
+    level.  Every rank ends with the same bits (each add is commutative)."""
     n = len(inputs)
     v = [np.array(x, copy=True) for x in inputs]
-    d = n // 2
-    while d >= 1:
+    d = 1
+    while d < n:
         v = [add(v[i], v[i ^ d], dtype) for i in range(n)]
-        d //= 2
+        d *= 2
     return v[0]
 
 

@@ -320,20 +320,21 @@ def generate_rhd(n: int) -> Schedule:
 
     P:364-365: "the buffer is first divided in 1/2 with one partner, then in
     1/4 with another partner, etc. to achieve a ReduceScatter.  Then, a
-    mirror-image AllGather completes."  Reading (distance halving, the
-    order is not stated): in ReduceScatter round t (t = 0..L-1) rank i pairs
-    with i XOR n/2^(t+1); both hold the same block of n/2^t chunks; i keeps the
-    lower half if that bit of i is 0, else the upper half, and receives the
-    partner's copy of the half it keeps (Reduce).  After L rounds rank i holds
-    chunk i fully reduced.  AllGather round L+u (u = 0..L-1) mirrors
+    mirror-image AllGather completes."  The partner order is not stated; the
+    reading is SPEC's ("round k of phase 1 pairs ranks differing in
+    bit k"): in ReduceScatter round t (t = 0..L-1) rank i pairs with
+    i XOR 2^t; both hold the same block of n/2^t chunks; i keeps the lower half
+    if bit t of i is 0, else the upper half, and receives the partner's copy of
+    the half it keeps (Reduce).  After L rounds rank i holds one chunk fully
+    reduced (chunk bitreverse(i)).  AllGather round L+u (u = 0..L-1) mirrors
     ReduceScatter round L-1-u: partners exchange their fully reduced blocks of
-    n/2^(L-u) chunks (Replace).
+    2^u chunks (Replace).
     """
     L = log2_exact(n)
     s = Schedule("rhd", n, -1, n)
     blocks = {i: (0, n) for i in range(n)}            # (first chunk, #chunks) each rank works on
     for t in range(L):
-        d = n >> (t + 1)
+        d = 1 << t
         rnd = []
         new = {}
         for i in range(n):
@@ -344,7 +345,7 @@ def generate_rhd(n: int) -> Schedule:
         blocks = new
         s.rounds.append(rnd)
     for u in range(L):
-        d = n >> (L - u)
+        d = 1 << (L - 1 - u)
         rnd = []
         new = {}
         for i in range(n):

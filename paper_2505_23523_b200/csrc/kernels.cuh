@@ -1120,10 +1120,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
 
 // ---------------------------------------------------------------- RHD (NEXT N3)
 // Recursive halving/doubling, pull-based, n chunks (the Ring's
-// partition).  Step t < L (ReduceScatter): partner j ^ n/2^(t+1); both hold the
-// same block of n/2^t chunks; j keeps the lower half if that bit of j is 0 and
-// adds the partner's copy of it into its own.  Step L+u (AllGather): partner
-// j ^ 2^u; j copies the partner's fully reduced block.  Step tau's partner is
+// partition).  Step t < L (ReduceScatter): partner j ^ 2^t (round
+// k pairs ranks differing in bit k); both hold the same block of n/2^t chunks;
+// j keeps the lower half if bit t of j is 0 and adds the partner's copy of it
+// into its own.  Step L+u (AllGather) mirrors step L-1-u: partner
+// j ^ 2^(L-1-u); j copies the partner's fully reduced block (its sibling).  Step tau's partner is
 // told when j finished step tau-1 (SLOT_RHD_READY + tau, per slice); AllGather
 // readers report back (SLOT_RHD_DONE) so no rank leaves while its buffer is read.
 template <int DT, int W, int MV>
@@ -1135,7 +1136,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_rhd(const __grid_const
   const int NV = P.G * P.sub;
   const int V = 16 / P.esize;
   const uint32_t ep = call_epoch(P);
-  auto partner = [&](int tau) { return j ^ (tau < L ? (W >> (tau + 1)) : (1 << (tau - L))); };
+  auto partner = [&](int tau) { return j ^ (tau < L ? (1 << tau) : (1 << (2 * L - 1 - tau))); };
   if (threadIdx.x == 0) st_release(flag_at(P.flags[partner(0)], SLOT_RHD_READY, P.fstride, s), ep, P.sys_scope);
   Pipe pipe = make_pipe(MV == MOVER_TMA);
   char* mine = P.buf[j];
@@ -1147,7 +1148,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_rhd(const __grid_const
     int clo, cn;        // chunks moved this step
     if (tau < L) {
       m /= 2;
-      blo = (j & (W >> (tau + 1))) ? blo + m : blo;
+      blo = (j & (1 << tau)) ? blo + m : blo;
       clo = blo;
       cn = m;
     } else {

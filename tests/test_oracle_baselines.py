@@ -64,12 +64,40 @@ def test_rhd_halving_structure(n):
     assert sizes[L:] == sizes[:L][::-1]
     assert all(t.kind == S.REDUCE for r in s.rounds[:L] for t in r)
     assert all(t.kind == S.REPLACE for r in s.rounds[L:] for t in r)
-    # after the ReduceScatter rank i holds chunk i fully reduced
+    # round k of the ReduceScatter pairs ranks differing in bit k
+    for k in range(L):
+        assert all(t.src ^ t.dst == 1 << k for t in s.rounds[k])
+        assert all(t.src ^ t.dst == 1 << (L - 1 - k) for t in s.rounds[L + k])
+    # after the ReduceScatter every rank holds exactly one chunk fully reduced, all different
     st = S.initial_state_uniform(n, n)
     for rnd in s.rounds[:L]:
         st = S.apply_round(st, rnd, n, one_chunk=False)
     full = frozenset(range(n))
-    assert all(st[(i, i)] == full for i in range(n))
+    owned = [[c for c in range(n) if st[(i, c)] == full] for i in range(n)]
+    assert all(len(o) == 1 for o in owned) and sorted(o[0] for o in owned) == list(range(n))
+
+
+def test_rhd_spec_examples():
+    """n=8 -> 6 rounds; n=2 -> 2 rounds of one chunk each; n=4 ->
+    beta = 1/2 + 1/4 + 1/4 + 1/2 = 3/2."""
+    assert S.generate_rhd(8).num_rounds == 6
+    s2 = S.generate_rhd(2)
+    assert s2.num_rounds == 2 and all(len(r) == 2 for r in s2.rounds)
+    assert S.verify_schedule(S.generate_rhd(4)).beta_coefficient == Fraction(3, 2)
+
+
+def test_broadcast_spec_examples():
+    """n=8 -> 3 rounds, beta 3; n=2 -> 1 round; n=16 -> 4 rounds,
+    verifier-valid from the AllReduce-precondition state.  S:289: in round k
+    the holders send to the lowest-index non-holders, pairing in index order."""
+    r8 = S.verify_schedule(S.generate_broadcast(8))
+    assert S.generate_broadcast(8).num_rounds == 3 and r8.beta_coefficient == 3
+    assert S.generate_broadcast(2).num_rounds == 1
+    assert S.generate_broadcast(16).num_rounds == 4 and S.verify_schedule(S.generate_broadcast(16)).valid
+    for rnd in S.generate_broadcast(16).rounds[1:]:
+        pairs = sorted({(t.src, t.dst) for t in rnd})
+        srcs, dsts = [p[0] for p in pairs], [p[1] for p in pairs]
+        assert srcs == sorted(srcs) and dsts == sorted(dsts)
 
 
 def test_rhd_rejects_non_power_of_two():
