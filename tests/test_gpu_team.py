@@ -648,3 +648,46 @@ def test_baselines_randomized_and_graph(S):
         assert S.stragglar_team_check_error() == 0
         check_equal([to_host(b, dtype) for b in rb], N.rhd_allreduce(xs, dtype), xs, dtype, f"graph rhd {it}")
         check_equal([to_host(b, dtype) for b in bb], N.broadcast_allreduce(xs, sigma, dtype), xs, dtype, f"graph bcast {it}")
+
+
+def test_sweep_max_size_bf16_sampled(S):
+    """BASELINE config 3's largest point (1 GiB bf16 per rank, n = 8, straggler 0)
+    through StragglAR (split, with delay), RHD and the Broadcast baseline:
+    inputs drawn on the device, each result checked on 200k sampled indices
+    (chunk edges included) against its plain definition, and all ranks bitwise
+    identical."""
+    n, sigma, count = 8, 0, 1 << 29
+    S.stragglar_team_init(n, sigma)
+    ce = N.chunk_elems(count, n - 1, "bfloat16")
+    ce_r = N.chunk_elems(count, n, "bfloat16")
+    edges = [0, 1, count - 1] + [j * c + d for c in (ce, ce_r) for j in range(1, n) for d in (-1, 0, 1) if j * c + d < count]
+    rng = np.random.default_rng(17)
+    idx = np.unique(np.concatenate([np.array(edges), rng.integers(0, count, 200_000)]))
+    tidx = torch.from_numpy(idx).cuda()
+    for algo in ("stragglar", "rhd", "bcast"):
+        bufs = []
+        for p in range(n):
+            g = torch.Generator(device="cuda").manual_seed(2505_23523 + 10 * p)
+            bufs.append(torch.randn(count, device="cuda", generator=g).to(torch.bfloat16))
+        xs = [b[tidx].view(torch.int16).cpu().numpy().view(np.uint16) for b in bufs]
+        if algo == "stragglar":
+            S.stragglar_team_reduce_scatter(bufs)
+            S.stragglar_team_inject_delay(200_000)
+            S.stragglar_team_complete(bufs)
+            want = N.plain_allreduce(xs, sigma, "bfloat16")
+        elif algo == "rhd":
+            S.stragglar_team_allreduce_rhd(bufs)
+            want = N.plain_rhd_allreduce(xs, "bfloat16")
+        else:
+            S.stragglar_team_bcast_precondition(bufs)
+            S.stragglar_team_inject_delay(200_000)
+            S.stragglar_team_bcast_complete(bufs)
+            want = N.plain_allreduce(xs, sigma, "bfloat16")
+        torch.cuda.synchronize()
+        assert S.stragglar_team_check_error() == 0
+        for p in range(1, n):
+            assert torch.equal(bufs[p].view(torch.int16), bufs[0].view(torch.int16)), (algo, p)
+        got = bufs[0][tidx].view(torch.int16).cpu().numpy().view(np.uint16)
+        assert np.array_equal(got, want), algo
+        del bufs
+        torch.cuda.empty_cache()
