@@ -24,7 +24,7 @@ def worker(rank, world, sigma, port, mode, q):
         os.environ.setdefault("STRAGGLAR_SLICES", "8")
         os.environ.setdefault("STRAGGLAR_TIMEOUT_MS", "60000")
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-        torch.cuda.set_device(0)
+        torch.cuda.set_device(rank % torch.cuda.device_count() if os.environ.get("STRAGGLAR_MP_SPREAD") else 0)   # one GPU per rank on a multi-GPU box
         from paper_2505_23523_b200.ddp import StragglarHookState, stragglar_hook
         from paper_2505_23523_b200.dist import ProcessComm
 

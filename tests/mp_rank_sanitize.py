@@ -24,7 +24,7 @@ def main():
     os.environ.setdefault("STRAGGLAR_SLICES", "4")
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
-    torch.cuda.set_device(0)
+    torch.cuda.set_device(rank % torch.cuda.device_count() if os.environ.get("STRAGGLAR_MP_SPREAD") else 0)   # one GPU per rank on a multi-GPU box
     from oracle import numerics as N
     from paper_2505_23523_b200 import stragglar as S
     from paper_2505_23523_b200.dist import ProcessComm
