@@ -178,16 +178,50 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// L2 eviction-priority hints on the bulk copies: 0 = none, 1 = evict_first,
+// 2 = evict_last (default for both).  Measured at config 2 (DESIGN.md §6b,
+// profiles/r01/hint_ab/): evict_last on loads and stores takes Phase B from
+// 664-666 to 655 us (forwarded slices stay in L2 for the next hop), the Ring
+// -1.6 %, the fused call -0.8 %; evict_first hurts everything.
+#ifndef STRAGGLAR_LOAD_HINT
+#define STRAGGLAR_LOAD_HINT 2
+#endif
+#ifndef STRAGGLAR_STORE_HINT
+#define STRAGGLAR_STORE_HINT 2
+#endif
+template <int H>
+__device__ __forceinline__ uint64_t l2_policy() {
+  uint64_t pol;
+  if constexpr (H == 1)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+#if STRAGGLAR_LOAD_HINT
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_policy<STRAGGLAR_LOAD_HINT>())
+      : "memory");
+#else
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(smem_dst)),
                "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+#if STRAGGLAR_STORE_HINT
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes), "l"(l2_policy<STRAGGLAR_STORE_HINT>())
+               : "memory");
+#else
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
                "r"(bytes)
                : "memory");
+#endif
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }

@@ -28,7 +28,18 @@ VARIANTS_LL = {
     "ll_gentle32": ["STRAGGLAR_LL_GENTLE=32"],
     "ll_gentle200": ["STRAGGLAR_LL_GENTLE=200"],
 }
-VARIANTS = VARIANTS_LL if "--ll" in sys.argv else VARIANTS_LAG if "--lag" in sys.argv else VARIANTS_ALL
+VARIANTS_HINT = {
+    "st_ef": ["STRAGGLAR_STORE_HINT=1"],
+    "ld_ef": ["STRAGGLAR_LOAD_HINT=1"],
+    "st_ef_ld_ef": ["STRAGGLAR_STORE_HINT=1", "STRAGGLAR_LOAD_HINT=1"],
+    "st_el": ["STRAGGLAR_STORE_HINT=2"],
+    "ld_el": ["STRAGGLAR_LOAD_HINT=2"],
+    "st_el_ld_el": ["STRAGGLAR_STORE_HINT=2", "STRAGGLAR_LOAD_HINT=2"],
+}
+if "--hint2" in sys.argv:
+    VARIANTS_HINT = {k: VARIANTS_HINT[k] for k in ("st_el", "ld_el", "st_el_ld_el")}
+VARIANTS = (VARIANTS_LL if "--ll" in sys.argv else VARIANTS_LAG if "--lag" in sys.argv
+            else VARIANTS_HINT if ("--hint" in sys.argv or "--hint2" in sys.argv) else VARIANTS_ALL)
 os.makedirs(os.path.join(ROOT, "build", "variants"), exist_ok=True)
 with ThreadPoolExecutor(4) as ex:
     futs = {k: ex.submit(B.build, True, False, v, os.path.join(ROOT, "build", "variants", f"lib_{k}.so")) for k, v in VARIANTS.items()}
