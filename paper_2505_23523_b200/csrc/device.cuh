@@ -198,30 +198,38 @@ __device__ __forceinline__ uint64_t l2_policy() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
+// HINT = false: no cache policy (the direct completion's write-heavy stream, where
+// nothing is re-read, measured slightly faster without it).
+template <bool HINT = true>
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
 #if STRAGGLAR_LOAD_HINT
+  if constexpr (HINT) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
           smem_u32(smem_dst)),
       "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_policy<STRAGGLAR_LOAD_HINT>())
       : "memory");
-#else
+  return;
+  }
+#endif
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(smem_dst)),
                "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
-#endif
 }
+template <bool HINT = true>
 __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
 #if STRAGGLAR_STORE_HINT
+  if constexpr (HINT) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
                "r"(smem_u32(smem_src)), "r"(bytes), "l"(l2_policy<STRAGGLAR_STORE_HINT>())
                : "memory");
-#else
+  return;
+  }
+#endif
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
                "r"(bytes)
                : "memory");
-#endif
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }

@@ -403,8 +403,8 @@ __device__ void tma_add_bcast(Pipe& p, char* const* dst, const char* a, const ch
     const uint64_t off = lo_b + (uint64_t)i * kPiece;
     const uint32_t len = piece_len(i);
     mbar_expect_tx(&p.bar[s], 2 * len);
-    bulk_load(p.buf(s), a + off, len, &p.bar[s]);
-    bulk_load(p.buf(s) + kPiece, b + off, len, &p.bar[s]);
+    bulk_load<false>(p.buf(s), a + off, len, &p.bar[s]);
+    bulk_load<false>(p.buf(s) + kPiece, b + off, len, &p.bar[s]);
   };
   if (threadIdx.x == 0 && np) {
     fence_proxy_async_global();
@@ -424,7 +424,7 @@ __device__ void tma_add_bcast(Pipe& p, char* const* dst, const char* a, const ch
     if (threadIdx.x == 0) {
       const uint64_t off = lo_b + (uint64_t)i * kPiece;
 #pragma unroll
-      for (int d = 0; d < W; ++d) bulk_store(dst[d] + off, A, len);
+      for (int d = 0; d < W; ++d) bulk_store<false>(dst[d] + off, A, len);
       bulk_commit();
       if (i + kAhead < np) {
         ring_release_wait();
