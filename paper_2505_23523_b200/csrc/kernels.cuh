@@ -350,7 +350,7 @@ __device__ void tma_reduce(Pipe& p, char* dst, const char* const (&src)[W - 1], 
     const uint32_t len = piece_len(i);
     mbar_expect_tx(&p.bar[s], (W - 1) * len);
 #pragma unroll
-    for (int j = 0; j < W - 1; ++j) bulk_load(p.buf(s) + j * kPiece, src[j] + off, len, &p.bar[s]);
+    for (int j = 0; j < W - 1; ++j) bulk_load<false>(p.buf(s) + j * kPiece, src[j] + off, len, &p.bar[s]);
   };
   if (threadIdx.x == 0 && np) {
     fence_proxy_async_global();
