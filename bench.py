@@ -343,15 +343,18 @@ def bench_team(args):
     # PCIe floor of the same traffic: every rank's H2D and D2H as concurrent plain copies, no kernels
     host_out = [torch.empty_like(h).pin_memory() for h in host]
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for p in range(world):
-        with torch.cuda.stream(s_in):
-            bufs[p].copy_(host[p], non_blocking=True)
-        with torch.cuda.stream(s_out):
-            host_out[p].copy_(ring[p], non_blocking=True)
-    torch.cuda.synchronize()
-    pcie_floor = (time.perf_counter() - t0) * 1e6
+    floors = []
+    for _ in range(3):             # best of 3 (the first touches freshly pinned pages)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for p in range(world):
+            with torch.cuda.stream(s_in):
+                bufs[p].copy_(host[p], non_blocking=True)
+            with torch.cuda.stream(s_out):
+                host_out[p].copy_(ring[p], non_blocking=True)
+        torch.cuda.synchronize()
+        floors.append((time.perf_counter() - t0) * 1e6)
+    pcie_floor = min(floors)
     del host_out
 
     # roofline of the dominant kernel (Phase B, k_phase<..., KIND 1>): HBM bytes it must move
