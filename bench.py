@@ -344,7 +344,7 @@ def bench_team(args):
     host_out = [torch.empty_like(h).pin_memory() for h in host]
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
     floors = []
-    for _ in range(3):             # best of 3 (the first touches freshly pinned pages)
+    for _ in range(5):             # best of 5 (the first touches freshly pinned pages)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for p in range(world):
