@@ -26,7 +26,11 @@ numerics   Plain definition of the AllReduce result, Phase A (ReduceScatter amon
 cost       alpha-beta closed forms of Table 1, T_RS, critical delay
            (P:423-424).
 
-Parity status: every function here is pinned by a ``-m "not gpu"`` test in
-``tests/test_oracle_*.py`` (see DESIGN.md §"Oracle pins"); none is "parity
-unpinned".
+Parity status: every public function here is pinned by a ``-m "not gpu"``
+test in ``tests/test_oracle_*.py`` (DESIGN.md §8 lists each with its pin); the
+private helpers (``_canonical_partial``, ``log2_exact``, ``generate``,
+``replay_schedule``, ``initial_state_*``) are exercised only through the pinned
+functions that call them, and DESIGN.md §8 names those.  Helpers that no pin
+covered (a holder-set trace and a JSON exporter) were removed in round 2 rather
+than left "parity unpinned".
 """

@@ -275,7 +275,7 @@ def generate_stragglar_even(n: int, max_rounds: Optional[int] = None) -> Schedul
         sched.rounds.append(tx)
         new = {h: set(c) for h, c in full.items()}
         for t in tx:
-            new[t.dst].add(t.chunk) if t.kind == REPLACE else new[t.dst].add(t.chunk)
+            new[t.dst].add(t.chunk)
         if r < n - 1:
             new[r].add(r)
             new[sigma].add(r)
@@ -502,35 +502,3 @@ def verify_schedule(s: Schedule) -> Report:
         if v != full:
             viol.append((len(s.rounds), f"postcondition: rank {h} chunk {c} has {sorted(v)}"))
     return Report(not viol, len(s.rounds), viol, beta, st)
-
-
-# --------------------------------------------------------------------------
-# Holder-set trace used to state Lemma 1 / I(r) / Lemma 2 / Remark 1
-# --------------------------------------------------------------------------
-def fully_reduced_holders(s: Schedule) -> List[Dict[int, FrozenSet[int]]]:
-    """Before each round r (index r) and after the last (index R): chunk -> set of
-    ranks holding it fully reduced, obtained by replaying the verifier."""
-    st = initial_state_stragglar(s.n)
-    full = frozenset(range(s.n))
-    out = []
-
-    def snap(state: State) -> Dict[int, FrozenSet[int]]:
-        return {c: frozenset(h for h in range(s.n) if state[(h, c)] == full) for c in range(s.num_chunks)}
-
-    out.append(snap(st))
-    for r, rnd in enumerate(s.rounds):
-        st = apply_round(st, rnd, s.n, r)
-        out.append(snap(st))
-    return out
-
-
-def to_json(s: Schedule) -> dict:
-    """S:114 schedule JSON (pairs derived from transfers)."""
-    rounds = []
-    for rnd in s.rounds:
-        pairs: Dict[Tuple[int, int], list] = {}
-        for t in rnd:
-            key = (min(t.src, t.dst), max(t.src, t.dst))
-            pairs.setdefault(key, []).append({"src": t.src, "dst": t.dst, "chunks": [t.chunk], "kind": t.kind})
-        rounds.append([{"pair": list(k), "transfers": v} for k, v in sorted(pairs.items())])
-    return {"algorithm": s.algorithm, "n": s.n, "straggler": s.straggler, "num_chunks": s.num_chunks, "rounds": rounds}

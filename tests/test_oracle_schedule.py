@@ -254,11 +254,3 @@ def test_ring_rounds_and_beta(n):
     assert rep.beta_coefficient == Fraction(2 * (n - 1), n)
     for t in range(n - 1):
         assert {(x.src, x.dst, x.chunk) for x in s.rounds[t]} == {(i, (i + 1) % n, (i - t) % n) for i in range(n)}
-
-
-def test_schedule_json_roundtrip_shape():
-    """S:114 field layout."""
-    j = S.to_json(S.generate_stragglar(4))
-    assert j["algorithm"] == "stragglar" and j["n"] == 4 and j["num_chunks"] == 3
-    assert len(j["rounds"]) == 4
-    assert j["rounds"][0][0]["pair"] == [0, 3]
