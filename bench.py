@@ -448,56 +448,208 @@ def bench_team(args):
     print(json.dumps(out))
 
 
-# ------------------------------------------------------------------ N > 1: one process per GPU
+# ------------------------------------------------------------------ N > 1: one process per rank
+def _free_port():
+    import socket
+
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    return port
+
+
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` without torchrun: start N ranks through
+    torch.distributed.run on 127.0.0.1 (the launch the driver uses) and return
+    its exit code.  With fewer GPUs than ranks the ranks share devices; --mps
+    then runs them concurrently under an MPS daemon started (and stopped) here."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    mps = None
+    if args.mps:
+        pipe = env.setdefault("CUDA_MPS_PIPE_DIRECTORY", "/tmp/stragglar_mps_pipe")
+        logd = env.setdefault("CUDA_MPS_LOG_DIRECTORY", "/tmp/stragglar_mps_log")
+        os.makedirs(pipe, exist_ok=True)
+        os.makedirs(logd, exist_ok=True)
+        r = subprocess.run(["nvidia-cuda-mps-control", "-d"], env=env, capture_output=True, text=True)
+        mps = r.returncode == 0
+        env["STRAGGLAR_BENCH_MPS"] = "1" if mps else "0"
+        time.sleep(1.0)
+    try:
+        return subprocess.call(cmd, env=env)
+    finally:
+        if mps:
+            subprocess.run(["nvidia-cuda-mps-control"], input="quit\n", env=env, text=True, capture_output=True)
+
+
+def launch_check():
+    """CPU check of the self-launch path (tests/test_bench_launch.py): every
+    rank joins a gloo group from the torchrun environment; rank 0 prints the
+    world it saw."""
+    import torch
+    import torch.distributed as dist
+
+    dist.init_process_group("gloo")
+    t = torch.tensor([dist.get_rank() + 1.0])
+    dist.all_reduce(t)
+    if dist.get_rank() == 0:
+        print(json.dumps({"launch_check": True, "world": dist.get_world_size(), "rank_sum": t.item(),
+                          "env": {k: os.environ.get(k) for k in ("RANK", "WORLD_SIZE", "MASTER_ADDR")}}))
+    dist.destroy_process_group()
+
+
+def _nccl_log_summary(path_glob):
+    """NCCL_DEBUG=INFO files of this rank: version, nranks of each communicator,
+    the algorithms its AllReduce calls were tuned to (TUNING lines)."""
+    import glob
+    import re
+
+    out = {"version": None, "nranks": [], "algos": {}, "nvls_lines": 0, "files": 0}
+    for f in glob.glob(path_glob):
+        out["files"] += 1
+        for line in open(f, errors="replace"):
+            m = re.search(r"NCCL version (\S+)", line)
+            if m:
+                out["version"] = m.group(1)
+            m = re.search(r"nRanks (\d+)", line) or re.search(r"nranks[ =](\d+)", line)
+            if m and "Init COMPLETE" in line:
+                out["nranks"].append(int(m.group(1)))
+            if "AllReduce" in line:
+                m = re.search(r"[Aa]lgo (\w+)", line)
+                if m:
+                    out["algos"][m.group(1)] = out["algos"].get(m.group(1), 0) + 1
+            if "NVLS" in line:
+                out["nvls_lines"] += 1
+    return out
+
+
 def bench_multi(args):
     import torch
     import torch.distributed as dist
 
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    logdir = os.path.join(ROOT, "gpurun_out") if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "/tmp"
+    # NCCL's own log (read once per process, before the first communicator):
+    # version, nranks and the algorithm each AllReduce was tuned to
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,TUNING")
+    os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(logdir, f"nccl_bench_r{rank}.%p.log"))
+
     import __graft_entry__
 
-    __graft_entry__.build()
-    from paper_2505_23523_b200 import stragglar as S
+    if local == 0:
+        __graft_entry__.build()
     from paper_2505_23523_b200.dist import ProcessComm
     from paper_2505_23523_b200.inputs import make_input
 
-    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
     ndev = torch.cuda.device_count()
-    # more ranks than GPUs: a functional test of this path with ranks sharing a
-    # device (kernels time-slice; gloo plumbing; no NCCL baseline; numbers are
-    # not performance numbers)
-    shared = ndev < world
+    shared = ndev < world          # more ranks than GPUs: ranks share devices (functional unless --mps)
     local = local % ndev
     torch.cuda.set_device(local)
     if shared:
         dist.init_process_group("gloo")
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist.barrier()
+    if local != 0:
+        __graft_entry__.build()        # rank 0 of the node compiled it; this only loads
+    from paper_2505_23523_b200 import stragglar as S
+
     _, sigma_w, dtype, count, _ = WORKLOADS[args.workload]
     sigma = sigma_w if sigma_w < world else 0      # the workload's straggler (config 5: rank 3)
     esize = ESIZE[dtype]
     S_bytes = count * esize
     comm = ProcessComm(sigma)
+    ranks_per_gpu, ctas = S.stragglar_shared_device_ranks()
+    mps = os.environ.get("STRAGGLAR_BENCH_MPS") == "1"
+    red_dev = "cpu" if shared else "cuda"
+
+    def gmax(x):
+        t = torch.tensor([float(x)], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def gmax_i(x):   # exact for %globaltimer stamps (~1.7e18 ns: beyond float64's integer range)
+        t = torch.tensor([int(x)], dtype=torch.int64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return int(t.item())
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    # ---------------- K0: the transport's measured ceilings (SURVEY §2.3 K0; P:386-388, P:449-451)
+    pb = (8 << 20) if (shared and not mps) else (64 << 20)
+    kbuf = torch.zeros(world * pb, dtype=torch.uint8, device="cuda")
+    comm.register(kbuf)
+    reps = 3 if shared else 10
+
+    def probe(active, mode, peers):
+        ts = []
+        for _ in range(reps):
+            e0, e1 = ev(), ev()
+            S.stragglar_barrier()
+            e0.record()
+            if active:
+                S.stragglar_probe_copy(kbuf, pb, mode, peers)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(gmax(e0.elapsed_time(e1) * 1e-3))
+        return min(ts)          # best of reps, max over ranks
+
+    others = [p for p in range(world) if p != rank]
+    k0 = {"bytes_per_peer": pb, "what": "device-initiated copies through the library's probe kernel; GB/s per "
+                                        "GPU port and direction (1e9 B/s), max over ranks, best of reps"}
+    t = probe(rank == 0, S.PROBE_TMA | S.PROBE_PUSH, [1])
+    k0["uni_push_tma_gbs"] = round(pb / t / 1e9, 1)
+    t = probe(rank == 0, S.PROBE_TMA | S.PROBE_PULL, [1])
+    k0["uni_pull_tma_gbs"] = round(pb / t / 1e9, 1)
+    t = probe(True, S.PROBE_TMA | S.PROBE_PUSH, [rank ^ 1] if (rank ^ 1) < world else [others[0]])
+    k0["pair_bidir_push_tma_gbs"] = round(pb / t / 1e9, 1)
+    for name, mode in (("tma", S.PROBE_TMA), ("lsu", 0)):
+        t = probe(True, mode | S.PROBE_PUSH, others)
+        k0[f"all_peers_push_{name}_gbs"] = round((world - 1) * pb / t / 1e9, 1)
+        t = probe(True, mode | S.PROBE_PULL, others)
+        k0[f"all_peers_pull_{name}_gbs"] = round((world - 1) * pb / t / 1e9, 1)
+    iters = 20 if shared else 2000
+    if rank in (0, 1):
+        S.stragglar_barrier()
+        S.stragglar_probe_pingpong(1 - rank, iters)
+        pp = S.stragglar_probe_pingpong_result()
+    else:
+        S.stragglar_barrier()
+        pp = 0.0
+    pp = gmax(pp)
+    k0["pingpong_iters"] = iters
+    k0["alpha_us"] = round(pp / (2 * iters), 3)           # one flag hop, system scope
+    comm.deregister(kbuf)
+    del kbuf
+    nvlink_pair = k0["pair_bidir_push_tma_gbs"]
+    nvlink_ingress = max(k0["all_peers_pull_tma_gbs"], k0["all_peers_pull_lsu_gbs"])
+    # the selection model consumes the measured constants (P:449-451)
+    S.stragglar_set_cost_model(k0["alpha_us"] * 1e-6, 1.0 / (nvlink_pair * 1e9))
+    if rank == 0 and os.path.isdir(os.path.join(ROOT, "gpurun_out")):
+        json.dump(dict(k0, world=world, shared=shared, mps=mps),
+                  open(os.path.join(ROOT, "gpurun_out", f"k0_n{world}.json"), "w"), indent=1)
+
+    # ---------------- buffers
     buf = to_tensor(make_input(count, dtype, rank, config=2), dtype).cuda()
     ring = buf.clone()
     nccl_buf = buf.clone()
-    rhd_buf, bc_buf = buf.clone(), buf.clone()
-    comm.register(buf)
-    comm.register(ring)
-    comm.register(rhd_buf)
-    comm.register(bc_buf)
+    rhd_buf, bc_buf, dir_buf = buf.clone(), buf.clone(), buf.clone()
+    for t_ in (buf, ring, rhd_buf, bc_buf, dir_buf):
+        comm.register(t_)
     C = chunk_bytes(count, world - 1, esize)
-    T_A_model = (world - 2) * C / (NVLINK_PEER_MEASURED * 1e9) * 1e6
-    D_ns = int((1.5 * T_A_model + 20.0) * 1e3) if args.delay_us is None else int(args.delay_us * 1e3)
-    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    R = S.stragglar_schedule_rounds(world)
 
-    def timed(fn, K):
+    def timed(fn, K, D_ns):
         res = []
         for _ in range(K):
             e0, ea, e1 = ev(), ev(), ev()
             S.stragglar_barrier()
             e0.record()
-            if rank == sigma:
+            if rank == sigma and D_ns:
                 S.stragglar_inject_delay(D_ns)
             ea.record()
             fn()
@@ -505,34 +657,75 @@ def bench_multi(args):
             res.append((e0, ea, e1))
         return res
 
+    # ---------------- delay calibrated from the MEASURED Phase A (D = 1.25 T_A + 20 us)
+    def phase_a_measured(D_ns, K):
+        tas = []
+        for _ in range(K):
+            timed(lambda: comm.allreduce(buf), 1, D_ns)
+            torch.cuda.synchronize()
+            ta, _tk = S.stragglar_phase_times()
+            tas.append(gmax(ta if rank != sigma else 0.0))
+        return statistics.median(tas)
+
+    timed(lambda: comm.allreduce(buf), args.warmup, 0)
+    torch.cuda.synchronize()
+    T_A0 = phase_a_measured(int(5e6), 3)                 # Phase A alone: straggler 5 ms late
+    D_ns = int((1.25 * T_A0 + 20.0) * 1e3) if args.delay_us is None else int(args.delay_us * 1e3)
+
     algos = {"stragglar": lambda: comm.allreduce(buf), "ring": lambda: comm.allreduce_ring(ring),
-             "bcast": lambda: comm.allreduce_bcast(bc_buf)}     # NEXT N3
+             "direct": lambda: S.stragglar_allreduce_direct(dir_buf),      # NEXT N1(ii)
+             "bcast": lambda: comm.allreduce_bcast(bc_buf)}                # NEXT N3
     if world & (world - 1) == 0:
-        algos["rhd"] = lambda: comm.allreduce_rhd(rhd_buf)   # NEXT N3
+        algos["rhd"] = lambda: comm.allreduce_rhd(rhd_buf)                 # NEXT N3
+    nccl_groups = {}
     if not shared:
-        algos["nccl"] = lambda: dist.all_reduce(nccl_buf)
-    results = {}
+        nccl_groups["nccl_default"] = None
+        for algo_env in ("Ring", "NVLS"):
+            old = os.environ.get("NCCL_ALGO")
+            os.environ["NCCL_ALGO"] = algo_env
+            try:
+                g = dist.new_group(backend="nccl")
+                tt = torch.ones(16, device="cuda")
+                dist.all_reduce(tt, group=g)          # communicator created now, with this NCCL_ALGO
+                torch.cuda.synchronize()
+                nccl_groups[f"nccl_{algo_env.lower()}"] = g
+            except Exception as e:  # noqa: BLE001  (NVLS may be unavailable)
+                nccl_groups[f"nccl_{algo_env.lower()}"] = repr(e)[:200]
+            finally:
+                if old is None:
+                    os.environ.pop("NCCL_ALGO", None)
+                else:
+                    os.environ["NCCL_ALGO"] = old
+        for name, g in nccl_groups.items():
+            if g is None or not isinstance(g, str):
+                algos[name] = (lambda g=g: dist.all_reduce(nccl_buf, group=g))
+    results, launches_total = {}, 0
+    clk_sum = None
     for name, fn in algos.items():
-        timed(fn, args.warmup)
+        timed(fn, args.warmup, D_ns)
         torch.cuda.synchronize()
         dist.barrier()
         l0 = S.stragglar_launch_count()
         with ClockSampler(local) as clk:
-            evs = timed(fn, args.steps)
+            evs = timed(fn, args.steps, D_ns)
             torch.cuda.synchronize()
-        launches = S.stragglar_launch_count() - l0
-        dev = "cpu" if shared else "cuda"
-        tot = torch.tensor([statistics.mean(e0.elapsed_time(e1) for e0, _, e1 in evs) * 1e3], device=dev)
-        dly = torch.tensor([statistics.mean(e0.elapsed_time(ea) for e0, ea, _ in evs) * 1e3], device=dev)
-        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-        dist.all_reduce(dly, op=dist.ReduceOp.MAX)
-        results[name] = (tot.item(), dly.item(), launches, clk.summary())
         if name == "stragglar":
-            # in-kernel stamps of the last call: Phase A on the non-stragglers, whole kernel per rank
-            ta, tk = S.stragglar_phase_times()
-            ph = torch.tensor([ta if rank != sigma else 0.0, tk], device="cpu" if shared else "cuda")
-            dist.all_reduce(ph, op=dist.ReduceOp.MAX)
-            phase_times = {"T_phaseA_us_max_NS": round(ph[0].item(), 2), "T_kernel_us_max": round(ph[1].item(), 2)}
+            launches_total = S.stragglar_launch_count() - l0
+            clk_sum = clk.summary()
+        tots = [e0.elapsed_time(e1) * 1e3 for e0, _, e1 in evs]
+        dlys = [e0.elapsed_time(ea) * 1e3 for e0, ea, _ in evs]
+        tot, dly = gmax(statistics.mean(tots)), gmax(statistics.mean(dlys))
+        posts = [a - b for a, b in zip(tots, dlys)]
+        results[name] = {"T_total_us": round(tot, 2), "D_meas_us": round(dly, 2), "T_post_us": round(tot - dly, 2),
+                         "T_post_min_us": round(gmax(min(posts)), 2)}
+    # phase times of the delayed StragglAR call (in-kernel stamps, each rank's GPU clock)
+    T_A = phase_a_measured(D_ns, min(5, args.steps))
+    # start-line skew: the barrier's release time compared across ranks (globaltimer)
+    skews = []
+    for _ in range(5):
+        S.stragglar_barrier()
+        tb = S.stragglar_last_barrier_ns()
+        skews.append((gmax_i(tb) + gmax_i(-tb)) * 1e-3)      # max - min over ranks
     # end to end through the public host-buffer entry point: every step copies this rank's
     # input from pinned host memory, runs StragglAR and copies the result back (pipelined pieces)
     hin = buf.cpu().pin_memory()
@@ -543,67 +736,95 @@ def bench_multi(args):
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         comm.allreduce_host(hin, hout, buf)        # synchronous per rank
-    e2e_rank = (time.perf_counter() - t0) * 1e6 / e2e_steps
-    e2e_t = torch.tensor([e2e_rank], device="cpu" if shared else "cuda")
-    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e = gmax((time.perf_counter() - t0) * 1e6 / e2e_steps)
     code, where = S.stragglar_check_error_where(False)
     if code:
         raise RuntimeError(f"device watchdog fired (where=0x{where:x})")
-    if rank == 0:
-        T_tot, D_meas, launches, clocks = results["stragglar"]
-        T_post = T_tot - D_meas
-        R = world + (world.bit_length() - 1) - 2
-        port_bytes = R * C
-        achieved = port_bytes / (T_post * 1e-6) / 1e9
-        if shared:
-            # every rank on one GPU: the links are HBM; Phase B moves 2n(n-1)C bytes in total
-            hbm, hsrc = hbm_peak()
-            hb = 2 * world * (world - 1) * C / (T_post * 1e-6) / 1e9
-            roof = {"bound": "hbm", "kernel": "k_phase<..., KIND=4> (Phase A + B), ranks sharing one GPU",
-                    "achieved": round(hb, 1), "peak": hbm, "unit": "GB/s", "frac": round(hb / hbm, 3),
-                    "traffic": None, "peak_source": hsrc}
-        else:
-            roof = {"bound": "nvlink", "kernel": "k_phase<..., KIND=4> (Phase A + B)", "achieved": round(achieved, 1),
-                    "peak": NVLINK_PEER_MEASURED, "unit": "GB/s", "frac": round(achieved / NVLINK_PEER_MEASURED, 3),
-                    "traffic": None, "peak_source": "B200_PROFILING.md measured peer copy 770 GB/s/direction"}
-        out = {
-            "metric": METRIC, "value": round(T_post, 2), "unit": "us", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(T_tot / 1e3, 4), "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None,
-            "dtype": {"float32": "f32", "bfloat16": "bf16", "int32": "i32"}[dtype],
-            "data": "synthetic (seeded N(0,1))",
-            "config": {"workload": f"{args.workload} per-rank buffer ({count} {dtype}, SUM), {world} ranks, straggler "
-                                   f"rank {sigma}; one process per GPU, CUDA IPC over NVLink/NVSwitch",
-                       "world": world, "straggler_rank": sigma, "count": count, "delay_us": D_ns / 1e3,
-                       "parallelism": f"allreduce{world}"},
-            "T_total_us": round(T_tot, 2), "D_meas_us": round(D_meas, 2), "phase_times_in_kernel": phase_times,
-            "algbw_GBps": round(S_bytes / (T_post * 1e-6) / 1e9, 1),
-            "busbw_GBps": round(S_bytes / (T_post * 1e-6) / 1e9 * 2 * (world - 1) / world, 1),
-            "ring_us": round(results["ring"][0] - results["ring"][1], 2),
-            "nccl_us": round(results["nccl"][0] - results["nccl"][1], 2) if "nccl" in results else None,
-            "speedup_vs_ring_post": round((results["ring"][0] - results["ring"][1]) / T_post, 3),
-            "speedup_vs_nccl_post": round((results["nccl"][0] - results["nccl"][1]) / T_post, 3) if "nccl" in results else None,
-            "rhd_us": round(results["rhd"][0] - results["rhd"][1], 2) if "rhd" in results else None,
-            "bcast_us": round(results["bcast"][0] - results["bcast"][1], 2),
-            "speedup_vs_rhd_post": round((results["rhd"][0] - results["rhd"][1]) / T_post, 3) if "rhd" in results else None,
-            "speedup_vs_bcast_post": round((results["bcast"][0] - results["bcast"][1]) / T_post, 3),
-            "shared_device_test": shared,
-            "roofline": roof,
-            "cpu_baseline": None,
-            "e2e": {"value": round(e2e_t.item(), 1), "unit": "us", "h2d_bytes_per_step": world * S_bytes,
-                    "d2h_bytes_per_step": world * S_bytes,
-                    "what": "stragglar_allreduce_host per rank: pinned host -> HBM, StragglAR (no injected delay), "
-                            "HBM -> host, pipelined over 8 MiB pieces; max over ranks, mean of the steps"},
-            "gpu_launches": launches,
-            "clocks": clocks,
-        }
-        print(json.dumps(out))
+    nccl_logs = _nccl_log_summary(os.path.join(logdir, f"nccl_bench_r{rank}.*.log")) if not shared else None
     comm.close()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    sar = results["stragglar"]
+    T_post, T_tot, D_meas = sar["T_post_us"], sar["T_total_us"], sar["D_meas_us"]
+    T_B = T_tot - max(D_meas, T_A)
+    # per-phase roofline: algorithmic bytes on the busiest port over the phase time
+    bytes_A, bytes_B = (world - 2) * C, R * C
+    if shared:
+        hbm, hsrc = hbm_peak()
+        roof = {"bound": "hbm", "kernel": "k_phase<..., KIND=4> (Phase A + B), ranks sharing one GPU",
+                "achieved": round(2 * world * (world - 1) * C / (T_post * 1e-6) / 1e9, 1), "peak": hbm,
+                "unit": "GB/s", "frac": None, "traffic": None, "peak_source": hsrc,
+                "note": "ranks share a GPU: every 'link' is that GPU's HBM (Phase B moves 2n(n-1)C bytes "
+                        "in total) and its SMs are split between ranks; no NVLink fraction exists"}
+        roof["frac"] = round(roof["achieved"] / hbm, 3)
+    else:
+        aA = bytes_A / (T_A * 1e-6) / 1e9 if T_A > 0 else None
+        aB = bytes_B / (T_post * 1e-6) / 1e9
+        roof = {"bound": "nvlink", "kernel": "k_phase<..., KIND=4> (Phase A + Phase B, one launch)",
+                "achieved": round(aB, 1), "peak": nvlink_pair, "unit": "GB/s", "frac": round(aB / nvlink_pair, 3),
+                "traffic": None, "peak_source": "K0 measured pair bidirectional TMA push (this run)",
+                "phase_A": {"bytes_per_port": bytes_A, "T_us": round(T_A, 2),
+                            "achieved": round(aA, 1) if aA else None, "peak_k0_ingress": nvlink_ingress,
+                            "frac_k0": round(aA / nvlink_ingress, 3) if aA else None,
+                            "frac_nominal_900": round(aA / NVLINK_NOMINAL, 3) if aA else None},
+                "phase_B": {"bytes_per_port": bytes_B, "T_us": round(T_post, 2), "achieved": round(aB, 1),
+                            "peak_k0_pair": nvlink_pair, "frac_k0": round(aB / nvlink_pair, 3),
+                            "frac_nominal_900": round(aB / NVLINK_NOMINAL, 3)}}
+    sp = {}
+    for name, r_ in results.items():
+        if name != "stragglar":
+            sp[name] = {"post": round(r_["T_post_us"] / T_post, 3), "total": round(r_["T_total_us"] / T_tot, 3)}
+    os.environ["OMP_NUM_THREADS"] = "1"
+    cpu = None if args.no_cpu else oracle_cpu_baseline(world, sigma, dtype, count)
+    out = {
+        "metric": METRIC, "value": round(T_post, 2), "unit": "us", "n_gpus": min(world, ndev), "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(T_tot / 1e3, 4), "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None,
+        "dtype": {"float32": "f32", "bfloat16": "bf16", "int32": "i32"}[dtype],
+        "data": "synthetic (seeded N(0,1), recipe in DESIGN.md §4)",
+        "config": {"workload": f"{args.workload} per-rank buffer ({count} {dtype}, SUM), {world} ranks, straggler "
+                               f"rank {sigma}; " + (f"{world} processes sharing {ndev} GPU(s)"
+                                                    + (" under MPS" if mps else " (time-sliced: functional check, "
+                                                       "not a performance number)") if shared else
+                                                    "one process per GPU, CUDA IPC over NVLink/NVSwitch"),
+                   "world": world, "straggler_rank": sigma, "count": count, "delay_us": D_ns / 1e3,
+                   "delay_rule": "1.25 x measured Phase A + 20 us" if args.delay_us is None else "--delay-us",
+                   "l2": "buffers reduced in place step after step; 256 MiB per rank exceeds the 126 MB L2",
+                   "parallelism": f"allreduce{world}"},
+        "shared_device": {"ranks_per_gpu": ranks_per_gpu, "ctas_per_rank": ctas, "mps": mps} if shared else None,
+        "T_total_us": T_tot, "D_meas_us": D_meas, "T_phaseA_us": round(T_A, 2), "T_phaseA_nodelay_us": round(T_A0, 2),
+        "T_phaseB_us": round(T_B, 2), "start_skew_us": round(statistics.median(skews), 3),
+        "algbw_GBps": round(S_bytes / (T_post * 1e-6) / 1e9, 1),
+        "busbw_GBps": round(S_bytes / (T_post * 1e-6) / 1e9 * 2 * (world - 1) / world, 1),
+        "algorithms": results, "speedup_vs": sp,
+        "ring_us": results["ring"]["T_post_us"],
+        "nccl_us": results["nccl_default"]["T_post_us"] if "nccl_default" in results else None,
+        "speedup_vs_ring_post": sp["ring"]["post"],
+        "speedup_vs_nccl_post": sp["nccl_default"]["post"] if "nccl_default" in sp else None,
+        "nccl": ({"torch_nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+                  "groups": {k: (v if isinstance(v, str) else "ok") for k, v in nccl_groups.items()},
+                  "log_rank0": nccl_logs} if not shared else
+                 {"value": None, "why": "NCCL cannot place two ranks on one GPU; the shared-device run has no NCCL arm"}),
+        "k0": k0,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e, 1), "unit": "us", "h2d_bytes_per_step": S_bytes, "d2h_bytes_per_step": S_bytes,
+                "what": "stragglar_allreduce_host per rank: pinned host -> HBM, StragglAR (no injected delay), "
+                        "HBM -> host, pipelined over 8 MiB pieces; max over ranks, mean of the steps; bytes per rank"},
+        "gpu_launches": launches_total,
+        "clocks": clk_sum,
+    }
+    print(json.dumps(out))
     dist.destroy_process_group()
 
 
 # ------------------------------------------------------------------ reference arm: the oracle
 def bench_reference(args):
+    """The CPU oracle as it stands (single thread), timed on the FULL workload
+    of our arm (same config, no sampling or scaling): one step = Algorithm 1
+    schedule generation + Phase A + the Phase-B replay; value = the Phase-B
+    replay (the analogue of T_post)."""
     world_env = int(os.environ.get("WORLD_SIZE", "1"))
     if int(os.environ.get("RANK", "0")) != 0:
         return
@@ -612,19 +833,18 @@ def bench_reference(args):
         # our arm at N GPUs runs N ranks (one per GPU) on the same per-rank buffer and straggler
         world, sigma = world_env, (sigma if sigma < world_env else 0)
         desc = f"{world} ranks, straggler rank {sigma}, {count} {dtype} per rank SUM"
-    sample = min(count, 1 << 22)
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ["OMP_NUM_THREADS"] = "1"
     from oracle import numerics as N
     from oracle import schedule as OS
     from paper_2505_23523_b200.inputs import make_inputs
 
-    xs = make_inputs(world, sample, dtype, config=2)
+    xs = make_inputs(world, count, dtype, config=2)
     phys = N.logical_to_physical(world, sigma)
-    bounds = N.chunk_bounds(sample, world - 1, dtype)
+    bounds = N.chunk_bounds(count, world - 1, dtype)
 
     def step():
         t0 = time.perf_counter()
-        sched = OS.generate_stragglar(world)
+        sched = OS.generate_stragglar(world) if world & (world - 1) == 0 else OS.generate(world)
         bufs = [x.copy() for x in xs]
         N.phase_a_reduce_scatter(bufs, sigma, dtype)
         t1 = time.perf_counter()
@@ -635,17 +855,18 @@ def bench_reference(args):
     for _ in range(args.warmup):
         step()
     res = [step() for _ in range(args.steps)]
-    scale = count / sample
-    post = statistics.mean(r[1] for r in res) * 1e6 * scale
-    tot = statistics.mean(r[0] + r[1] for r in res) * 1e6 * scale
+    post = statistics.mean(r[1] for r in res) * 1e6
+    tot = statistics.mean(r[0] + r[1] for r in res) * 1e6
     cpu = {"value": round(post, 1), "unit": "us", "cores": 1, "kind": "oracle",
-           "sample": f"{world} ranks x {sample} {dtype} elements per step (1/{scale:g} of the workload, scaled "
-                     "linearly); single-threaded numpy; value = Phase B replay", "host": host_cpu()}
+           "sample": f"the full workload every step: {world} ranks x {count} {dtype} elements (no sampling, no "
+                     "scaling); single-threaded numpy; value = Phase B replay, ms_per_step = schedule + Phase A + "
+                     "Phase B", "host": host_cpu()}
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(post, 1), "unit": "us", "n_gpus": world_env,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot / 1e3, 3), "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": {"float32": "f32", "bfloat16": "bf16"}.get(dtype, dtype),
-        "data": "synthetic", "config": {"workload": f"{args.workload}: {desc}; CPU oracle"},
+        "data": "synthetic (seeded N(0,1), the same inputs as our arm)",
+        "config": {"workload": f"{args.workload}: {desc}; CPU oracle"},
         "cpu_baseline": cpu,
         "e2e": {"value": round(post, 1), "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
@@ -660,15 +881,22 @@ def main():
     ap.add_argument("--workload", default="config2", choices=sorted(WORKLOADS))
     ap.add_argument("--delay-us", type=float, default=None)
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle cpu_baseline leg")
-    ap.add_argument("--mover", choices=["lsu", "tma"], default=None, help="Phase-B data mover (default: library's)")
+    ap.add_argument("--mover", choices=["lsu", "tma"], default=None, help="data mover (default: library's)")
+    ap.add_argument("--mps", action="store_true", help="N > GPUs: run the sharing ranks concurrently under MPS")
+    ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.mover:
         os.environ["STRAGGLAR_MOVER"] = args.mover
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    in_torchrun = "RANK" in os.environ and "WORLD_SIZE" in os.environ
+    if args.gpus > 1 and not in_torchrun:
+        sys.exit(self_launch(args))
+    if args.launch_check:
+        launch_check()
+    elif args.impl == "reference":
         bench_reference(args)
-    elif args.gpus > 1 or int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
         bench_multi(args)
     else:
         bench_team(args)

@@ -67,11 +67,13 @@ typedef enum { STRAGGLAR_SUM = 0 } stragglar_op_t;
 typedef enum {
   STRAGGLAR_OK = 0,
   STRAGGLAR_ERR_INVALID_ARG = 1,     /* NULL/unaligned buffer, bad rank, ... */
-  STRAGGLAR_ERR_UNSUPPORTED = 2,     /* world not in {2,4,8}, unknown dtype/op */
+  STRAGGLAR_ERR_UNSUPPORTED = 2,     /* world not in {2,4,6,8}, unknown dtype/op */
   STRAGGLAR_ERR_NOT_INITIALIZED = 3, /* no communicator / handles not imported */
   STRAGGLAR_ERR_NOT_REGISTERED = 4,  /* buf not inside a registered buffer */
   STRAGGLAR_ERR_CUDA = 5,            /* a CUDA runtime/driver call failed */
-  STRAGGLAR_ERR_TIMEOUT = 6,         /* a device spin-wait exceeded the watchdog */
+  STRAGGLAR_ERR_TIMEOUT = 6,         /* a device spin-wait exceeded the watchdog; sticky:
+                                        every later call on that communicator returns it
+                                        until the communicator is re-initialized */
   STRAGGLAR_ERR_INTERNAL = 7
 } stragglar_status_t;
 
@@ -92,23 +94,42 @@ int stragglar_schedule_round(int world, int round, int* out, int max_transfers, 
 
 /* ---- per-process communicator (one process per GPU) ----------------------
  * stragglar_init(rank, world, straggler_rank): rank and straggler_rank in
- * [0, world), world in {2,4,8}; uses the calling thread's current CUDA
- * device; allocates the flag array and builds this rank's round table.
- * The straggler is fixed for the communicator's lifetime. */
+ * [0, world), world in {2,4,8} (Algorithm 1) or 6 (the even
+ * non-power-of-two schedule of Appendix B); uses the calling
+ * thread's current CUDA device; allocates the flag array and builds this
+ * rank's round table.  The straggler is fixed for the communicator's lifetime
+ * (P:457-459). */
 int stragglar_init(int rank, int world, int straggler_rank);
 /* Size of the opaque per-rank blob that carries IPC handles. */
 int stragglar_handle_size(size_t* bytes);
-/* Writes this rank's flag-array IPC handle into blob (handle_size bytes). */
+/* Writes this rank's flag-array IPC handle into blob (handle_size bytes),
+ * with the rank, its GPU's UUID and co-resident CTA capacity, and the
+ * communicator's layout knobs (straggler, CTAs, slice sizes, mover, scope). */
 int stragglar_export_handle(void* blob);
 /* blobs: world * handle_size bytes, rank order (exchanged by the caller, e.g.
- * torch.distributed all_gather); opens every peer's flag array. */
+ * torch.distributed all_gather); opens every peer's flag array.
+ * INVALID_ARG if a blob sits at the wrong index or any rank's layout knobs
+ * differ from this rank's (the environment knobs below must agree across
+ * ranks: a flag covers the same bytes everywhere only then).  Ranks that
+ * share a GPU (several processes per device, e.g. under MPS) split its
+ * co-resident CTA capacity: the CTAs per rank become
+ * min over GPUs of capacity / (ranks on that GPU), the same on every rank;
+ * UNSUPPORTED if that is 0. */
 int stragglar_import_handles(const void* blobs, int world);
+/* After import: how many ranks of this communicator share this rank's GPU
+ * and the CTAs per rank a launch uses. */
+int stragglar_shared_device_ranks(int* ranks_on_my_gpu, int* ctas_per_rank);
 /* Registers [buf, buf+bytes) (device memory of this process) for peer access
  * and writes its IPC blob (handle_size bytes) into blob_out.  Collective in
  * effect: every rank registers its corresponding buffer, then all ranks call
  * stragglar_import_buffer with everyone's blobs. */
 int stragglar_register_buffer(void* buf, size_t bytes, void* blob_out);
+/* INVALID_ARG if the ranks registered different byte counts. */
 int stragglar_import_buffer(void* buf, const void* blobs, int world);
+/* Closes this process's mappings of the peers' copies of the registration
+ * that starts at buf (synchronizes the device first).  Local, but every rank
+ * should deregister its copy before freeing it; NOT_REGISTERED if none. */
+int stragglar_deregister_buffer(void* buf);
 /* StragglAR AllReduce in place ("similar functionality to
  * ncclAllReduce()").  buf must lie in a registered buffer at the same offset
  * on every rank.  Non-stragglers enqueue Phase A then Phase B; the straggler
@@ -130,9 +151,11 @@ int stragglar_allreduce_direct(void* buf, size_t count, int dtype, int op, void*
  * in-house on the same transport, in place, collective, same argument rules
  * and errors as stragglar_allreduce.
  * RHD — recursive halving/doubling ("Butterfly"): n chunks (the
- *   Ring's partition); log2 n ReduceScatter steps in which rank j pairs with
- *   j XOR n/2^(t+1) and adds the partner's copy of the half it keeps, then
- *   log2 n mirror-image AllGather steps; bf16 partials rounded per step.
+ *   Ring's partition); log2 n ReduceScatter steps in which, at step t, rank j
+ *   pairs with j XOR 2^t (round k pairs ranks differing in bit k)
+ *   and adds the partner's copy of the half of the shared block it keeps (the
+ *   lower half if bit t of j is 0), then log2 n mirror-image AllGather steps;
+ *   bf16 partials rounded per step.
  *   UNSUPPORTED unless world is a power of two.
  * Broadcast — straggler-aware: the non-stragglers AllReduce
  *   among themselves (canonical order of Phase A, then every non-straggler
@@ -160,11 +183,41 @@ int stragglar_allreduce_host(const void* host_in, void* host_out, void* buf, siz
                              void* stream);
 /* Device-side barrier among all ranks of the communicator (bench start line). */
 int stragglar_barrier(void* stream);
+/* %globaltimer (ns, this GPU's clock) at which this rank left its last
+ * stragglar_barrier; compared across ranks it bounds the start-line skew.
+ * Synchronizes the device. */
+int stragglar_last_barrier_ns(uint64_t* ns);
+/* ---- K0 probes: the measured ceilings of the transport (
+ * the paper's link bandwidths P:386-388 and model constants P:449-451) -------
+ * stragglar_probe_copy: device-initiated copies between this rank and every
+ * peer p with bit p of peer_mask set, all at once.  buf lies in a registered
+ * buffer of >= world * bytes_per_peer bytes (bytes_per_peer a multiple of
+ * 16); segment q of every rank's copy is [q*bytes_per_peer, (q+1)*...).
+ * mode bit 0: 0 = push (read own segment `rank` locally, store it into
+ * segment `rank` of each peer), 1 = pull (load segment p of peer p, store it
+ * into own segment p); mode bit 1: 0 = 16-byte ld/st by every thread, 1 =
+ * cp.async.bulk (TMA) through shared memory, the data kernels' default mover.
+ * ctas: CTAs (0 = the communicator's per-rank count), rounded up to a
+ * multiple of the number of peers.  Not collective: the caller decides which
+ * ranks probe at once (uni- vs bidirectional) and times the call with events
+ * after stragglar_barrier. */
+int stragglar_probe_copy(void* buf, size_t bytes_per_peer, int mode, uint32_t peer_mask, int ctas, void* stream);
+/* Collective between this rank and `peer` (both call it, each naming the
+ * other, with the same iters): `iters` flag round trips with the data
+ * kernels' system-scope signalling (fence.acq_rel.sys + st.relaxed.sys to the
+ * peer's flag, ld.acquire.sys on the own); the lower rank starts each trip.
+ * stragglar_probe_pingpong_result (synchronizes) returns the last ping-pong's
+ * device time in us (divide by 2*iters for one hop, the model's alpha). */
+int stragglar_probe_pingpong(int peer, int iters, void* stream);
+int stragglar_probe_pingpong_result(double* us);
 /* Bench only: a one-thread kernel that spins on %globaltimer for `ns`
  * nanoseconds from its own start (the paper's idle kernel). */
 int stragglar_inject_delay(uint64_t ns, void* stream);
-/* Reads and clears the device error word (watchdog timeouts, bad arguments
- * seen on the device).  *code = 0 if none.  Synchronizes the device. */
+/* Reads the device error word (watchdog timeouts) and clears the device copy.
+ * *code = 0 if none.  Synchronizes the device.  A timeout leaves the ranks'
+ * flags out of step, so the communicator stays failed: later calls return
+ * STRAGGLAR_ERR_TIMEOUT (from a pinned host copy of the word, no sync) until
+ * *_finalize and a new *_init. */
 int stragglar_check_error(int* code);
 /* Same, for the team (team != 0) or the per-process communicator, also
  * returning where the first failing spin-wait was: (kind << 8) | index with
@@ -189,7 +242,7 @@ int stragglar_team_allreduce(void* const* bufs, size_t count, int dtype, int op,
 /* The two phases separately (the allreduce is exactly phase A then phase B):
  * reduce_scatter = Phase A over the n-1 non-stragglers;
  * complete       = Phase B over all n ranks (requires Phase A on the same
- *                  buffers first). */
+ *                  buffers, count and dtype first: INVALID_ARG otherwise). */
 int stragglar_team_reduce_scatter(void* const* bufs, size_t count, int dtype, int op, void* stream);
 int stragglar_team_complete(void* const* bufs, size_t count, int dtype, int op, void* stream);
 int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, int op, void* stream);
@@ -248,7 +301,8 @@ int stragglar_team_finalize(void);
  *     T_SAR  = R alpha + R/(n-1) * bytes * beta        (R = n + log2 n - 2)
  *     T_Ring = 2(n-1) alpha + 2(n-1)/n * bytes * beta
  * Outputs the critical delay (s, >= 0) and use_stragglar = (delay_s >= critical).
- * Host only; world must be 2, 4 or 8 (or any power of two up to 64). */
+ * Host only; world even in [2, 64]: powers of two use Algorithm 1, other even
+ * world sizes the Appendix-B schedule (built for 6..14; UNSUPPORTED beyond). */
 int stragglar_select(int world, double bytes, double delay_s, double alpha_s, double beta_s_per_byte,
                      int* use_stragglar, double* critical_delay_s);
 /* Algorithm codes of stragglar_select_algorithm / stragglar_allreduce_auto. */
@@ -283,10 +337,7 @@ int stragglar_allreduce_auto(void* buf, size_t count, int dtype, int op, void* s
  * STRAGGLAR_SUBSLICE_BYTES (their target size on large messages, 131072: each
  * hop hands over ~128 KB pieces, so a forwarded slice is still in L2 when
  * the next hop reads it),
- * STRAGGLAR_TIMEOUT_MS (watchdog, 10000), STRAGGLAR_LL_MAX_CHUNK (chunks up
- * to this many bytes use the low-latency word protocol in Phase B; 0 = off,
- * the default — measured slower than the flag protocol on one B200),
- * STRAGGLAR_SYS_SCOPE (team mode: system-scope flags, 0), and for the host
+ * STRAGGLAR_TIMEOUT_MS (watchdog, 10000), STRAGGLAR_SYS_SCOPE (team mode: system-scope flags, 0), and for the host
  * entry point STRAGGLAR_E2E_PIECE_BYTES (8 MiB) / STRAGGLAR_E2E_STREAMS (1). */
 
 /* Number of kernel launches the library enqueued since load (bench evidence). */

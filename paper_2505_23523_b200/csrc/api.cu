@@ -23,6 +23,9 @@ cudaError_t launch_plan_kernel(int which, int dtype, const LaunchPlan& P, int nb
 cudaError_t launch_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st, cudaStream_t stream);
 cudaError_t launch_barrier(const LaunchPlan& P, cudaStream_t stream);
 cudaError_t occupancy_blocks_per_sm(int which, int dtype, int world, int mover, int* blocks);
+cudaError_t launch_probe_copy(const ProbeArgs& A, int mover, int nblocks, cudaStream_t stream);
+cudaError_t launch_probe_pingpong(uint32_t* mine, uint32_t* theirs, int initiator, int iters, DevState* st,
+                                  uint64_t timeout_ns, uint32_t* host_err, cudaStream_t stream);
 }  // namespace stragglar
 
 using namespace stragglar;
@@ -35,16 +38,30 @@ constexpr int kDefaultMover = MOVER_TMA;   // measured faster (profiles/r01)
 
 std::atomic<uint64_t> g_launches{0};
 
+// The communicator's layout knobs.  Every rank must use the same values (a
+// flag index covers the same byte range on every rank only if they agree), so
+// they travel in the flag-array blob and stragglar_import_handles rejects a
+// mismatch instead of running with silently different slice layouts.
+struct Layout {
+  int32_t world, sigma, G_alloc, sub_max, mover, sys_scope, lanes_max, pad;
+  uint64_t slice_bytes, sub_bytes;
+};
+
 struct IpcBlob {          // what travels between processes, per rank
   cudaIpcMemHandle_t handle;
   uint64_t offset;        // of the registered pointer inside its allocation
   uint64_t bytes;
+  Layout layout;          // flag-array blob only (zero in buffer blobs)
+  int32_t rank;           // the exporting rank
+  int32_t resident_ctas;  // co-resident CTA capacity of the exporter's GPU (flag blob only)
+  char uuid[16];          // the exporter's GPU (ranks sharing a GPU share its SMs)
 };
 
 struct Registration {
   char* local = nullptr;
   size_t bytes = 0;
   char* peer[kMaxWorld] = {nullptr};
+  void* mapped[kMaxWorld] = {nullptr};   // cudaIpcOpenMemHandle results (closed by deregister / finalize)
 };
 
 struct Comm {
@@ -52,15 +69,22 @@ struct Comm {
   bool team = false;
   int world = 0, rank = -1, sigma = -1, device = -1;
   int G = 0;                   // CTAs per rank (the launch's co-residency budget)
+  int G_alloc = 0;             // CTAs per rank the flag array was sized for (fixes the flag stride)
   int sub = 1;                 // slices per CTA at most (STRAGGLAR_SUBSLICES)
   uint64_t sub_bytes = 0;      // target slice size on large messages (STRAGGLAR_SUBSLICE_BYTES)
+  int lanes_max = kMaxOps;     // Phase-B op lanes per slice at most (STRAGGLAR_OP_LANES; 1 = off)
   bool rs_pending = false;     // team: a Phase A awaits its Phase B (same call epoch)
+  const void* rs_buf0 = nullptr;  // team: the pending Phase A's first buffer, count and dtype
+  size_t rs_count = 0;
+  int rs_dtype = -1;
   bool bc_pending = false;     // team: a Broadcast-baseline precondition awaits its completion
-  uint32_t* flags = nullptr;   // own flag array(s) + LL area(s); team: world of them back to back
+  uint32_t* flags = nullptr;   // own flag array(s); team: world of them back to back
   uint32_t* peer_flags[kMaxWorld] = {nullptr};
-  uint64_t* peer_ll[kMaxWorld] = {nullptr};
-  size_t flags_bytes = 0;      // per rank, before its LL area
-  size_t rank_bytes = 0;       // per rank: flags + LL
+  size_t rank_bytes = 0;       // flag bytes per rank
+  int resident = 0;            // co-resident CTAs of all kernels on this GPU (occupancy x SMs)
+  int share = 1;               // ranks of this communicator on this rank's GPU (from the blobs)
+  uint32_t* host_err = nullptr;// pinned, device-mapped copy of the error word (sticky; read without sync)
+  uint32_t* host_err_dev = nullptr;
   bool imported = false;
   DevState* state = nullptr;
   RankPrograms progs;
@@ -69,16 +93,10 @@ struct Comm {
   uint64_t* trace = nullptr;            // Phase-B op trace (optional)
   // tuning knobs, read from the environment once at init (include/stragglar.h)
   uint64_t slice_bytes = 16384;         // STRAGGLAR_SLICE_BYTES
-  uint64_t ll_max_chunk = 0;            // STRAGGLAR_LL_MAX_CHUNK (0: LL off)
   int sys_scope = 1;                    // STRAGGLAR_SYS_SCOPE (team mode only; default 0 there)
   uint64_t e2e_piece_bytes = 8ull << 20;// STRAGGLAR_E2E_PIECE_BYTES (8 MiB measured best)
   int e2e_streams = 1;                  // STRAGGLAR_E2E_STREAMS (1 measured best)
   int last_slices = 0;                  // slices per chunk of the last Phase-B call (trace layout)
-  // LL layout of the previous call if it ran Phase B through the LL areas
-  // (count, element size, CTAs per rank); see LaunchPlan::ll_gate
-  bool ll_last = false;
-  uint64_t ll_count = 0;
-  int ll_esize = 0, ll_G = 0;
   double alpha_s = 3e-6;               // P:450 per-message latency used in the paper's model
   double beta_s_per_byte = 1.0 / 770e9; // measured B200 peer copy per direction (B200_PROFILING.md)
   std::vector<Registration> regs;
@@ -165,6 +183,8 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   if (G > kMaxSlices) G = kMaxSlices;
   if (G < 1 || (team && G * world > cap)) return STRAGGLAR_ERR_UNSUPPORTED;
   c.G = G;
+  c.G_alloc = G;
+  c.resident = cap;
   c.world = world;
   c.rank = team ? -1 : rank;
   c.sigma = sigma;
@@ -175,25 +195,25 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   c.slice_bytes = env_u64("STRAGGLAR_SLICE_BYTES", 16384);
   c.sys_scope = team ? (int)env_u64("STRAGGLAR_SYS_SCOPE", 0) : 1;
   // Sub-slices (finer hand-offs) pay with gpu-scope flags (team: Phase B -3.7 %)
-  // but not with system-scope ones: every extra flag costs a fence.acq_rel.sys
-  // (team mode at sys scope: 693 vs 690 us; per-process under MPS, n = 2/4/8:
-  // 275/554/1082 us with them, 187/431/1027 without).
+  // but not with system-scope ones, where every extra flag costs a system-scope
+  // fence.
   c.sub = (int)env_u64("STRAGGLAR_SUBSLICES", c.sys_scope ? 1 : kMaxSub);
   c.sub_bytes = env_u64("STRAGGLAR_SUBSLICE_BYTES", 128 * 1024);
   if (c.sub < 1) c.sub = 1;
   if (c.sub > kMaxSub) c.sub = kMaxSub;
-  c.ll_max_chunk = env_u64("STRAGGLAR_LL_MAX_CHUNK", 0);       // off by default: slower on one GPU
-  if (c.ll_max_chunk > kLLChunkBytes) c.ll_max_chunk = kLLChunkBytes;
+  c.lanes_max = (int)env_u64("STRAGGLAR_OP_LANES", kMaxOps);
+  if (c.lanes_max < 1) c.lanes_max = 1;
   c.e2e_piece_bytes = env_u64("STRAGGLAR_E2E_PIECE_BYTES", 8ull << 20);
   c.e2e_streams = (int)env_u64("STRAGGLAR_E2E_STREAMS", 1);
-  c.flags_bytes = ((size_t)kSlots * G * kMaxSub * sizeof(uint32_t) + 255) / 256 * 256;
-  c.rank_bytes = c.flags_bytes + (size_t)(kMaxWorld - 1) * kLLChunkWords * sizeof(uint64_t);
+  c.rank_bytes = ((size_t)kSlots * G * kMaxSub * sizeof(uint32_t) + 255) / 256 * 256;
   const size_t nbytes = team ? c.rank_bytes * world : c.rank_bytes;
   auto fail_free = [&]() {
     if (c.flags) cudaFree(c.flags);
     if (c.state) cudaFree(c.state);
+    if (c.host_err) cudaFreeHost(c.host_err);
     c.flags = nullptr;
     c.state = nullptr;
+    c.host_err = nullptr;
     return STRAGGLAR_ERR_CUDA;
   };
   DevState init;
@@ -202,37 +222,58 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   if (cudaMalloc(&c.flags, nbytes) != cudaSuccess || cudaMemset(c.flags, 0, nbytes) != cudaSuccess ||
       cudaMalloc(&c.state, sizeof(DevState)) != cudaSuccess ||
       cudaMemcpy(c.state, &init, sizeof(DevState), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaHostAlloc(&c.host_err, sizeof(uint32_t), cudaHostAllocMapped) != cudaSuccess ||
+      cudaHostGetDevicePointer(&c.host_err_dev, c.host_err, 0) != cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess)
     return fail_free();
-  for (int p = 0; p < kMaxWorld; ++p) {
-    c.peer_flags[p] = nullptr;
-    c.peer_ll[p] = nullptr;
-  }
-  auto ll_of = [&](uint32_t* f) { return reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(f) + c.flags_bytes); };
+  *(volatile uint32_t*)c.host_err = 0;
+  for (int p = 0; p < kMaxWorld; ++p) c.peer_flags[p] = nullptr;
   if (team) {
-    for (int p = 0; p < world; ++p) {
+    for (int p = 0; p < world; ++p)
       c.peer_flags[p] = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(c.flags) + (size_t)p * c.rank_bytes);
-      c.peer_ll[p] = ll_of(c.peer_flags[p]);
-    }
     c.imported = true;
   } else {
     c.peer_flags[rank] = c.flags;
-    c.peer_ll[rank] = ll_of(c.flags);
     c.imported = (world == 1);
   }
   c.active = true;
   return STRAGGLAR_OK;
 }
 
+Layout layout_of(const Comm& c) {
+  Layout l;
+  std::memset(&l, 0, sizeof(l));
+  l.world = c.world;
+  l.sigma = c.sigma;
+  l.G_alloc = c.G_alloc;
+  l.sub_max = c.sub;
+  l.mover = c.mover;
+  l.sys_scope = c.sys_scope;
+  l.lanes_max = c.lanes_max;
+  l.slice_bytes = c.slice_bytes;
+  l.sub_bytes = c.sub_bytes;
+  return l;
+}
+
+// A watchdog timeout (or another device-side error) is sticky: the kernel that
+// records it also writes the pinned host copy, and every later call returns
+// STRAGGLAR_ERR_TIMEOUT without launching until stragglar_check_error clears
+// it — the flags are then out of step, so the caller must re-initialize.
+bool sticky_error(const Comm& c) { return c.host_err && *(volatile const uint32_t*)c.host_err != 0; }
+
 void common_finalize(Comm& c) {
   if (!c.active) return;
   cudaDeviceSynchronize();
   for (void* p : c.opened) cudaIpcCloseMemHandle(p);
   c.opened.clear();
+  for (auto& r : c.regs)
+    for (int p = 0; p < c.world; ++p)
+      if (r.mapped[p]) cudaIpcCloseMemHandle(r.mapped[p]);
   c.regs.clear();
   if (c.flags) cudaFree(c.flags);
   if (c.state) cudaFree(c.state);
   if (c.trace) cudaFree(c.trace);
+  if (c.host_err) cudaFreeHost(c.host_err);
   c = Comm();
 }
 
@@ -268,7 +309,7 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
   P.world = c.world;
   P.sigma = c.sigma;
   P.G = c.G;
-  P.fstride = c.G * kMaxSub;
+  P.fstride = c.G_alloc * kMaxSub;
   P.last_kernel = last_kernel ? 1 : 0;
   P.count = count;
   P.esize = esize_of(dtype);
@@ -278,18 +319,13 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
   P.timeout_ns = c.timeout_ns;
   P.mover = c.mover;
   P.trace = c.trace;
-  {
-    // LL Phase B for small chunks (latency-bound): STRAGGLAR_LL_MAX_CHUNK bytes, 0 disables
-    const uint64_t chunk_bytes = P.ce * P.esize;
-    P.use_ll = (chunk_bytes > 0 && chunk_bytes <= c.ll_max_chunk) ? 1 : 0;
-    if (P.use_ll) P.sub = 1;   // the LL area is laid out per CTA slice
-  }
   P.sys_scope = c.sys_scope;
   P.state = c.state;
+  P.host_err = c.host_err_dev;
+  P.lanes = 1;
   P.bc_partner = c.progs.bc_partner;
   for (int p = 0; p < c.world; ++p) {
     P.flags[p] = c.peer_flags[p];
-    P.ll[p] = c.peer_ll[p];
     P.logical_of_phys[p] = c.progs.logical_of_phys[p];
     P.bc_sender[p] = c.progs.bc_sender[p];
     P.bc_round[p] = c.progs.bc_round[p];
@@ -297,6 +333,24 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
     for (int k = 0; k < c.progs.nops[p]; ++k) P.ops[p][k] = c.progs.ops[p][k];
   }
   return P;
+}
+
+// Phase-B op lanes (LaunchPlan::lanes): when a call uses few slices (small
+// messages) the idle CTA budget runs a rank's ops on separate CTAs, so an op
+// waits only for its own inputs instead of the rank's previous op (one slice
+// per CTA only; the same value on every rank: it depends on the call and the
+// agreed layout alone).
+void set_op_lanes(const Comm& c, LaunchPlan& P) {
+  int maxops = 1;
+  for (int p = 0; p < c.world; ++p) maxops = c.progs.nops[p] > maxops ? c.progs.nops[p] : maxops;
+  int lanes = 1;
+  if (P.sub == 1 && P.G > 0) {
+    lanes = c.G / P.G;
+    if (lanes > maxops) lanes = maxops;
+    if (lanes > c.lanes_max) lanes = c.lanes_max;
+    if (lanes < 1) lanes = 1;
+  }
+  P.lanes = lanes;
 }
 
 int check_args(const void* buf, size_t count, int dtype, int op) {
@@ -320,25 +374,12 @@ int team_check(void* const* bufs, size_t count, int dtype, int op) {
   return STRAGGLAR_OK;
 }
 
-int launch(int which, int dtype, const LaunchPlan& P0, int nblocks, void* stream) {
-  Comm& c = (g_team.active && P0.state == g_team.state) ? g_team : g_proc;
-  if (which == K_COMPLETE || which == K_FUSED) c.last_slices = P0.G * P0.sub;
-  // A peer is at most one call ahead (every call needs every rank's arrival to
-  // complete anywhere).  If the previous call ran LL Phase B with another
-  // layout, this call's up-front LL pushes must wait for their receivers'
-  // arrival (per-process mode only: a team launch serves every rank at once).
-  const bool runs_ll = P0.use_ll && (which == K_COMPLETE || which == K_FUSED);
-  LaunchPlan P = P0;
-  P.ll_gate = (runs_ll && !c.team && c.ll_last &&
-               (c.ll_count != P.count || c.ll_esize != P.esize || c.ll_G != P.G)) ? 1 : 0;
+int launch(int which, int dtype, const LaunchPlan& P, int nblocks, void* stream) {
+  Comm& c = (g_team.active && P.state == g_team.state) ? g_team : g_proc;
+  if (sticky_error(c)) return STRAGGLAR_ERR_TIMEOUT;   // flags out of step: re-initialize
+  if (which == K_COMPLETE || which == K_FUSED) c.last_slices = P.G * P.sub;
   cudaError_t e = launch_plan_kernel(which, dtype, P, nblocks, (cudaStream_t)stream);
   if (e != cudaSuccess) return STRAGGLAR_ERR_CUDA;
-  if (P.last_kernel) {
-    c.ll_last = runs_ll;
-    c.ll_count = P.count;
-    c.ll_esize = P.esize;
-    c.ll_G = P.G;
-  }
   g_launches.fetch_add(1);
   return STRAGGLAR_OK;
 }
@@ -358,13 +399,14 @@ int team_rs(void* const* bufs, size_t count, int dtype, void* stream) {
 int team_b(void* const* bufs, size_t count, int dtype, void* stream, int which = K_COMPLETE, uint64_t delay_ns = 0) {
   Comm& c = g_team;
   LaunchPlan P = base_plan(c, count, dtype, true);
+  if (which == K_COMPLETE || which == K_FUSED) set_op_lanes(c, P);
   P.sigma_delay_ns = delay_ns;
   for (int p = 0; p < c.world; ++p) {
     P.buf[p] = (char*)bufs[p];
     P.local_rank[p] = p;
   }
   P.nlocal = c.world;
-  return launch(which, dtype, P, c.world * P.G, stream);
+  return launch(which, dtype, P, c.world * P.G * P.lanes, stream);
 }
 
 int read_error(Comm& c, int* code, uint32_t* where = nullptr) {
@@ -375,6 +417,8 @@ int read_error(Comm& c, int* code, uint32_t* where = nullptr) {
   CK(cudaMemcpy(&h, c.state, sizeof(h), cudaMemcpyDeviceToHost));
   *code = (int)h.err;
   if (where) *where = h.err_info;
+  // reported once from the device word; the host copy stays set, so every later
+  // call on this communicator fails with TIMEOUT until it is re-initialized
   if (h.err) {
     uint32_t z[2] = {0, 0};
     CK(cudaMemcpy(c.state, z, sizeof(z), cudaMemcpyHostToDevice));
@@ -520,6 +564,13 @@ int stragglar_handle_size(size_t* bytes) {
   return STRAGGLAR_OK;
 }
 
+int device_uuid(int dev, char out[16]) {
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) return STRAGGLAR_ERR_CUDA;
+  std::memcpy(out, &prop.uuid, 16);
+  return STRAGGLAR_OK;
+}
+
 int stragglar_export_handle(void* blob) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_proc.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
@@ -529,6 +580,11 @@ int stragglar_export_handle(void* blob) {
   CK(cudaIpcGetMemHandle(&b.handle, g_proc.flags));
   b.offset = 0;
   b.bytes = g_proc.rank_bytes;
+  b.layout = layout_of(g_proc);
+  b.rank = g_proc.rank;
+  b.resident_ctas = g_proc.resident;
+  int st = device_uuid(g_proc.device, b.uuid);
+  if (st) return st;
   std::memcpy(blob, &b, sizeof(b));
   return STRAGGLAR_OK;
 }
@@ -539,16 +595,47 @@ int stragglar_import_handles(const void* blobs, int world) {
   if (!c.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
   if (!blobs || world != c.world) return STRAGGLAR_ERR_INVALID_ARG;
   const IpcBlob* b = static_cast<const IpcBlob*>(blobs);
+  // every rank must run the same layout (slices, sub-slices, mover, scope,
+  // straggler) and sit at its own index: reject before mapping anything
+  const Layout mine = layout_of(c);
+  for (int p = 0; p < world; ++p) {
+    if (b[p].rank != p || b[p].bytes != c.rank_bytes) return STRAGGLAR_ERR_INVALID_ARG;
+    if (std::memcmp(&b[p].layout, &mine, sizeof(Layout)) != 0) return STRAGGLAR_ERR_INVALID_ARG;
+  }
+  // Co-residency: ranks that share a GPU (several processes per device, e.g.
+  // under MPS) must fit their cooperative grids side by side, or one rank's
+  // CTAs cannot become resident while the others spin on its flags.  Every
+  // rank derives the same CTA budget from the same blobs: the smallest
+  // capacity / (ranks on that GPU) over the GPUs in use (the flag stride
+  // stays G_alloc, so only the launch size changes).
+  int G = c.G_alloc;
+  for (int p = 0; p < world; ++p) {
+    int share = 0;
+    for (int q = 0; q < world; ++q) share += std::memcmp(b[p].uuid, b[q].uuid, 16) == 0;
+    const int cap = b[p].resident_ctas / share;
+    if (cap < G) G = cap;
+    if (p == c.rank) c.share = share;
+  }
+  if (G < 1) return STRAGGLAR_ERR_UNSUPPORTED;
   for (int p = 0; p < world; ++p) {
     if (p == c.rank) continue;
     void* ptr = nullptr;
     CK(cudaIpcOpenMemHandle(&ptr, b[p].handle, cudaIpcMemLazyEnablePeerAccess));
     c.opened.push_back(ptr);
-    if (b[p].bytes != c.rank_bytes) return STRAGGLAR_ERR_INVALID_ARG;   // ranks disagree on G
     c.peer_flags[p] = reinterpret_cast<uint32_t*>(static_cast<char*>(ptr) + b[p].offset);
-    c.peer_ll[p] = reinterpret_cast<uint64_t*>(static_cast<char*>(ptr) + b[p].offset + c.flags_bytes);
   }
+  c.G = G;
   c.imported = true;
+  return STRAGGLAR_OK;
+}
+
+int stragglar_shared_device_ranks(int* ranks_on_my_gpu, int* ctas_per_rank) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  const Comm& c = g_proc;
+  if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (!ranks_on_my_gpu || !ctas_per_rank) return STRAGGLAR_ERR_INVALID_ARG;
+  *ranks_on_my_gpu = c.share;
+  *ctas_per_rank = c.G;
   return STRAGGLAR_OK;
 }
 
@@ -575,6 +662,7 @@ int stragglar_register_buffer(void* buf, size_t bytes, void* blob_out) {
   CK(cudaIpcGetMemHandle(&b.handle, (void*)base));
   b.offset = (uint64_t)((CUdeviceptr)buf - base);
   b.bytes = bytes;
+  b.rank = g_proc.rank;
   std::memcpy(blob_out, &b, sizeof(b));
   return STRAGGLAR_OK;
 }
@@ -588,19 +676,39 @@ int stragglar_import_buffer(void* buf, const void* blobs, int world) {
   Registration r;
   r.local = static_cast<char*>(buf);
   r.bytes = b[c.rank].bytes;
+  for (int p = 0; p < world; ++p)
+    if (b[p].bytes != r.bytes) return STRAGGLAR_ERR_INVALID_ARG;   // ranks registered different sizes
   for (int p = 0; p < world; ++p) {
     if (p == c.rank) {
       r.peer[p] = r.local;
       continue;
     }
-    if (b[p].bytes != r.bytes) return STRAGGLAR_ERR_INVALID_ARG;
     void* ptr = nullptr;
-    CK(cudaIpcOpenMemHandle(&ptr, b[p].handle, cudaIpcMemLazyEnablePeerAccess));
-    c.opened.push_back(ptr);
+    if (cudaIpcOpenMemHandle(&ptr, b[p].handle, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      for (int q = 0; q < p; ++q)
+        if (r.mapped[q]) cudaIpcCloseMemHandle(r.mapped[q]);
+      return STRAGGLAR_ERR_CUDA;
+    }
+    r.mapped[p] = ptr;
     r.peer[p] = static_cast<char*>(ptr) + b[p].offset;
   }
   c.regs.push_back(r);
   return STRAGGLAR_OK;
+}
+
+int stragglar_deregister_buffer(void* buf) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  if (!c.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  for (size_t i = c.regs.size(); i-- > 0;) {
+    if (c.regs[i].local != buf) continue;
+    CK(cudaDeviceSynchronize());   // no call of this process still uses the mappings
+    for (int p = 0; p < c.world; ++p)
+      if (c.regs[i].mapped[p]) cudaIpcCloseMemHandle(c.regs[i].mapped[p]);
+    c.regs.erase(c.regs.begin() + i);
+    return STRAGGLAR_OK;
+  }
+  return STRAGGLAR_ERR_NOT_REGISTERED;
 }
 
 static int proc_plan(void* buf, size_t count, int dtype, LaunchPlan* P) {
@@ -628,7 +736,8 @@ int stragglar_allreduce(void* buf, size_t count, int dtype, int op, void* stream
   if ((st = proc_plan(buf, count, dtype, &P))) return st;
   // one persistent launch: non-stragglers run Phase A then Phase B, the
   // straggler Phase B only (its delay is whatever precedes it on its stream)
-  return launch(K_FUSED, dtype, P, P.G, stream);
+  set_op_lanes(c, P);
+  return launch(K_FUSED, dtype, P, P.G * P.lanes, stream);
 }
 
 int stragglar_allreduce_direct(void* buf, size_t count, int dtype, int op, void* stream) {
@@ -784,6 +893,7 @@ int stragglar_barrier(void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   Comm& c = g_proc;
   if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (sticky_error(c)) return STRAGGLAR_ERR_TIMEOUT;
   LaunchPlan P = base_plan(c, 0, STRAGGLAR_INT32, true);
   P.nlocal = 1;
   P.local_rank[0] = c.rank;
@@ -792,11 +902,81 @@ int stragglar_barrier(void* stream) {
   return STRAGGLAR_OK;
 }
 
+// ---------------------------------------------------------------- K0 probes
+int stragglar_probe_copy(void* buf, size_t bytes_per_peer, int mode, uint32_t peer_mask, int ctas, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (sticky_error(c)) return STRAGGLAR_ERR_TIMEOUT;
+  if (!buf || bytes_per_peer == 0 || bytes_per_peer % 16 || (mode & ~3)) return STRAGGLAR_ERR_INVALID_ARG;
+  const size_t need = bytes_per_peer * (size_t)c.world;
+  const Registration* reg = nullptr;
+  for (const auto& r : c.regs)
+    if ((char*)buf >= r.local && (char*)buf + need <= r.local + r.bytes) reg = &r;
+  if (!reg) return STRAGGLAR_ERR_NOT_REGISTERED;
+  const size_t delta = (char*)buf - reg->local;
+  ProbeArgs A;
+  std::memset(&A, 0, sizeof(A));
+  A.local = (char*)buf;
+  A.bytes = bytes_per_peer;
+  A.me = c.rank;
+  A.pull = mode & 1;
+  for (int p = 0; p < c.world; ++p) {
+    A.peer[p] = reg->peer[p] + delta;
+    if (p != c.rank && ((peer_mask >> p) & 1u)) A.peers[A.npeers++] = p;
+  }
+  if (A.npeers == 0) return STRAGGLAR_ERR_INVALID_ARG;
+  int n = ctas > 0 ? ctas : c.G;
+  n = (n + A.npeers - 1) / A.npeers * A.npeers;   // every peer served by the same number of CTAs
+  const int mover = (mode & 2) ? MOVER_TMA : MOVER_LSU;
+  if (launch_probe_copy(A, mover, n, (cudaStream_t)stream) != cudaSuccess) return STRAGGLAR_ERR_CUDA;
+  g_launches.fetch_add(1);
+  return STRAGGLAR_OK;
+}
+
+int stragglar_probe_pingpong(int peer, int iters, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (sticky_error(c)) return STRAGGLAR_ERR_TIMEOUT;
+  if (peer < 0 || peer >= c.world || peer == c.rank || iters < 1) return STRAGGLAR_ERR_INVALID_ARG;
+  uint32_t* mine = c.peer_flags[c.rank] + (size_t)SLOT_PROBE * c.G_alloc * kMaxSub;
+  uint32_t* theirs = c.peer_flags[peer] + (size_t)SLOT_PROBE * c.G_alloc * kMaxSub;
+  if (launch_probe_pingpong(mine, theirs, c.rank < peer ? 1 : 0, iters, c.state, c.timeout_ns, c.host_err_dev,
+                            (cudaStream_t)stream) != cudaSuccess)
+    return STRAGGLAR_ERR_CUDA;
+  g_launches.fetch_add(1);
+  return STRAGGLAR_OK;
+}
+
+int stragglar_probe_pingpong_result(double* us) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!us) return STRAGGLAR_ERR_INVALID_ARG;
+  if (!g_proc.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  CK(cudaDeviceSynchronize());
+  DevState h;
+  CK(cudaMemcpy(&h, g_proc.state, sizeof(h), cudaMemcpyDeviceToHost));
+  if (h.err) return STRAGGLAR_ERR_TIMEOUT;
+  *us = h.probe_ns * 1e-3;
+  return STRAGGLAR_OK;
+}
+
 int stragglar_inject_delay(uint64_t ns, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   if (!g_proc.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
   if (launch_delay(nullptr, ns, g_proc.state, (cudaStream_t)stream) != cudaSuccess) return STRAGGLAR_ERR_CUDA;
   g_launches.fetch_add(1);
+  return STRAGGLAR_OK;
+}
+
+int stragglar_last_barrier_ns(uint64_t* ns) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!ns) return STRAGGLAR_ERR_INVALID_ARG;
+  if (!g_proc.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  CK(cudaDeviceSynchronize());
+  DevState h;
+  CK(cudaMemcpy(&h, g_proc.state, sizeof(h), cudaMemcpyDeviceToHost));
+  *ns = h.t_barrier;
   return STRAGGLAR_OK;
 }
 
@@ -844,6 +1024,25 @@ int stragglar_team_slices(int* slices) {
   return STRAGGLAR_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// The split team calls (reduce_scatter -> complete*, bcast_precondition ->
+// bcast_complete) share one call epoch: a completion must run on exactly the
+// buffers, count and dtype of its pending first half, or flags written under
+// another slice layout would satisfy its waits.
+void team_pend(Comm& c, void* const* bufs, size_t count, int dtype) {
+  c.rs_buf0 = bufs[0];
+  c.rs_count = count;
+  c.rs_dtype = dtype;
+}
+bool team_matches(const Comm& c, void* const* bufs, size_t count, int dtype) {
+  return c.rs_buf0 == bufs[0] && c.rs_count == count && c.rs_dtype == dtype;
+}
+}  // namespace
+
+extern "C" {
+
 int stragglar_team_reduce_scatter(void* const* bufs, size_t count, int dtype, int op, void* stream) {
   std::lock_guard<std::mutex> lk(g_mu);
   int st = team_check(bufs, count, dtype, op);
@@ -851,6 +1050,7 @@ int stragglar_team_reduce_scatter(void* const* bufs, size_t count, int dtype, in
   if (g_team.rs_pending || g_team.bc_pending) return STRAGGLAR_ERR_INVALID_ARG;
   if ((st = team_rs(bufs, count, dtype, stream))) return st;
   g_team.rs_pending = true;
+  team_pend(g_team, bufs, count, dtype);
   return STRAGGLAR_OK;
 }
 
@@ -858,7 +1058,8 @@ int stragglar_team_complete(void* const* bufs, size_t count, int dtype, int op, 
   std::lock_guard<std::mutex> lk(g_mu);
   int st = team_check(bufs, count, dtype, op);
   if (st || count == 0) return st;
-  if (!g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;   // Phase B needs its Phase A
+  if (!g_team.rs_pending || !team_matches(g_team, bufs, count, dtype))
+    return STRAGGLAR_ERR_INVALID_ARG;   // Phase B needs its own Phase A
   g_team.rs_pending = false;
   return team_b(bufs, count, dtype, stream);
 }
@@ -875,7 +1076,7 @@ int stragglar_team_complete_direct(void* const* bufs, size_t count, int dtype, i
   std::lock_guard<std::mutex> lk(g_mu);
   int st = team_check(bufs, count, dtype, op);
   if (st || count == 0) return st;
-  if (!g_team.rs_pending) return STRAGGLAR_ERR_INVALID_ARG;
+  if (!g_team.rs_pending || !team_matches(g_team, bufs, count, dtype)) return STRAGGLAR_ERR_INVALID_ARG;
   g_team.rs_pending = false;
   return team_b(bufs, count, dtype, stream, K_DIRECT);
 }
@@ -951,6 +1152,7 @@ int stragglar_team_bcast_precondition(void* const* bufs, size_t count, int dtype
   P.nlocal = k;
   if ((st = launch(K_BCAST_A, dtype, P, k * P.G, stream))) return st;
   c.bc_pending = true;
+  team_pend(c, bufs, count, dtype);
   return STRAGGLAR_OK;
 }
 
@@ -958,7 +1160,8 @@ int stragglar_team_bcast_complete(void* const* bufs, size_t count, int dtype, in
   std::lock_guard<std::mutex> lk(g_mu);
   int st = team_check(bufs, count, dtype, op);
   if (st || count == 0) return st;
-  if (!g_team.bc_pending) return STRAGGLAR_ERR_INVALID_ARG;   // needs its precondition
+  if (!g_team.bc_pending || !team_matches(g_team, bufs, count, dtype))
+    return STRAGGLAR_ERR_INVALID_ARG;   // needs its own precondition
   g_team.bc_pending = false;
   return team_b(bufs, count, dtype, stream, K_BCAST_B);
 }

@@ -38,22 +38,6 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
 __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
   asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// 8-byte LL words (payload | epoch << 32): one single-copy-atomic access each
-__device__ __forceinline__ uint64_t ld_ll(const uint64_t* p, bool sys) {
-  uint64_t v;
-  if (sys)
-    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  else
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_ll(uint64_t* p, uint32_t payload, uint32_t epoch, bool sys) {
-  const uint64_t v = (uint64_t)payload | ((uint64_t)epoch << 32);
-  if (sys)
-    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-  else
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 // scope-selected flag access: sys for CUDA-IPC peers on other GPUs, gpu for one device
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p, bool sys) {
   return sys ? ld_acquire_sys(p) : ld_acquire_gpu(p);

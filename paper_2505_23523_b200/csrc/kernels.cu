@@ -27,7 +27,61 @@ __global__ void k_barrier(const __grid_constant__ LaunchPlan P) {
     st_release(flag_at(P.flags[threadIdx.x], SLOT_BARRIER + me, P.fstride, 0), ep, P.sys_scope);
   if (threadIdx.x < P.world && (int)threadIdx.x != me)
     spin_wait(flag_at(P.flags[me], SLOT_BARRIER + threadIdx.x, P.fstride, 0), ep, P, 0x800 | threadIdx.x);
+  __syncwarp();
+  if (threadIdx.x == 0) P.state->t_barrier = globaltimer();
   finish_call(P);
+}
+
+// ---------------------------------------------------------------- K0 probes
+// Device-initiated copies to / from peers: the ceiling the NVLink rooflines
+// are quoted against.  MV = MOVER_LSU: 16-byte ld/st by every thread
+// (copy_vecs); MOVER_TMA: cp.async.bulk through the shared-memory stage ring
+// (tma_copy), the data kernels' own mover.
+template <int MV>
+__global__ void __launch_bounds__(kThreads) k_probe_copy(const __grid_constant__ ProbeArgs A) {
+  const int pi = blockIdx.x % A.npeers, part = blockIdx.x / A.npeers;
+  const int nparts = gridDim.x / A.npeers;
+  const int p = A.peers[pi];
+  const uint64_t nv = A.bytes / 16;
+  const uint64_t lo = nv * part / nparts * 16, hi = nv * (part + 1) / nparts * 16;
+  const char* src = A.pull ? A.peer[p] + (uint64_t)p * A.bytes : A.local + (uint64_t)A.me * A.bytes;
+  char* dst = A.pull ? A.local + (uint64_t)p * A.bytes : A.peer[p] + (uint64_t)A.me * A.bytes;
+  if constexpr (MV == MOVER_TMA) {
+    Pipe pipe = make_pipe(true);
+    tma_copy(pipe, dst + lo, src + lo, hi - lo);
+  } else {
+    copy_vecs(dst + lo, src + lo, (hi - lo) / 16);
+  }
+}
+
+// Flag ping-pong between this rank and one peer at system scope with the data
+// kernels' own signalling (fence.acq_rel.sys + st.relaxed.sys to the peer's
+// flag, ld.acquire.sys spin on the own flag): `iters` round trips, timed on
+// the device.  The initiator (lower rank) starts each round trip.
+__global__ void k_probe_pingpong(uint32_t* mine, uint32_t* theirs, int initiator, int iters, DevState* st,
+                                 uint64_t timeout_ns, uint32_t* host_err) {
+  if (threadIdx.x != 0) return;
+  const uint32_t base = st->probe_seq;
+  const uint64_t t0 = globaltimer();
+  bool ok = true;
+  for (int i = 1; i <= iters && ok; ++i) {
+    const uint32_t v = base + (uint32_t)i;
+    if (initiator) st_release_sys(theirs, v);
+    const uint64_t w0 = globaltimer();
+    while (int32_t(ld_acquire_sys(mine) - v) < 0) {
+      if (globaltimer() - w0 > timeout_ns) {
+        if (atomicCAS(&st->err, 0u, (uint32_t)ERR_TIMEOUT) == 0u) {
+          st->err_info = 0xF00;
+          if (host_err) *(volatile uint32_t*)host_err = (uint32_t)ERR_TIMEOUT;
+        }
+        ok = false;
+        break;
+      }
+    }
+    if (ok && !initiator) st_release_sys(theirs, v);
+  }
+  st->probe_ns = globaltimer() - t0;
+  st->probe_seq = base + (uint32_t)iters;
 }
 
 // ---------------------------------------------------------------- host launchers
@@ -69,6 +123,23 @@ cudaError_t launch_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st, cu
 
 cudaError_t launch_barrier(const LaunchPlan& P, cudaStream_t stream) {
   k_barrier<<<1, 32, 0, stream>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_probe_copy(const ProbeArgs& A, int mover, int nblocks, cudaStream_t stream) {
+  if (mover == MOVER_TMA) {
+    cudaError_t e = cudaFuncSetAttribute(k_probe_copy<MOVER_TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem);
+    if (e != cudaSuccess) return e;
+    k_probe_copy<MOVER_TMA><<<nblocks, kThreads, kTmaSmem, stream>>>(A);
+  } else {
+    k_probe_copy<MOVER_LSU><<<nblocks, kThreads, 0, stream>>>(A);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_probe_pingpong(uint32_t* mine, uint32_t* theirs, int initiator, int iters, DevState* st,
+                                  uint64_t timeout_ns, uint32_t* host_err, cudaStream_t stream) {
+  k_probe_pingpong<<<1, 32, 0, stream>>>(mine, theirs, initiator, iters, st, timeout_ns, host_err);
   return cudaGetLastError();
 }
 

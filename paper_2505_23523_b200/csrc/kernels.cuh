@@ -34,8 +34,8 @@ __device__ __forceinline__ bool flag_ok(uint32_t v, uint32_t epoch) { return int
 
 // Spin (one thread) until *f >= epoch.  Bounded by the watchdog; gives up
 // early if another CTA of this process already reported an error.
-static __device__ bool spin_wait(const uint32_t* f, uint32_t epoch, const LaunchPlan& P, uint32_t where) {
-  const bool sys = P.sys_scope;
+static __device__ bool spin_wait(const uint32_t* f, uint32_t epoch, const LaunchPlan& P, uint32_t where,
+                                 bool sys) {
   if (flag_ok(ld_acquire(f, sys), epoch)) return true;
   const uint64_t t0 = globaltimer();
   for (uint32_t it = 1;; ++it) {
@@ -44,17 +44,28 @@ static __device__ bool spin_wait(const uint32_t* f, uint32_t epoch, const Launch
     if ((it & 127) == 0) {
       if (*(volatile uint32_t*)&P.state->err) return false;
       if (globaltimer() - t0 > P.timeout_ns) {
-        if (atomicCAS(&P.state->err, 0u, (uint32_t)ERR_TIMEOUT) == 0u) atomicExch(&P.state->err_info, where);
+        if (atomicCAS(&P.state->err, 0u, (uint32_t)ERR_TIMEOUT) == 0u) {
+          atomicExch(&P.state->err_info, where);
+          if (P.host_err) *(volatile uint32_t*)P.host_err = (uint32_t)ERR_TIMEOUT;   // sticky, seen by the host API
+        }
         return false;
       }
     }
   }
 }
 
+// Flags written by other ranks need the communicator's scope (system scope
+// across GPUs); flags a rank writes for its own CTAs (SLOT_SELF,
+// SLOT_RS_LOCAL) only need GPU scope.
+__device__ __forceinline__ bool spin_wait(const uint32_t* f, uint32_t epoch, const LaunchPlan& P, uint32_t where) {
+  return spin_wait(f, epoch, P, where, P.sys_scope != 0);
+}
+
 // Whole-CTA wait: thread 0 spins, the barrier publishes the acquired state.
-__device__ __forceinline__ bool cta_wait(const uint32_t* f, uint32_t epoch, const LaunchPlan& P, uint32_t where) {
+__device__ __forceinline__ bool cta_wait(const uint32_t* f, uint32_t epoch, const LaunchPlan& P, uint32_t where,
+                                         bool local = false) {
   int ok = 1;
-  if (threadIdx.x == 0) ok = spin_wait(f, epoch, P, where);
+  if (threadIdx.x == 0) ok = spin_wait(f, epoch, P, where, local ? false : P.sys_scope != 0);
   return __syncthreads_and(ok);
 }
 
@@ -525,9 +536,8 @@ template <int DT, int W, int MV, bool BC = false>
 __device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
   const int NV = P.G * P.sub;   // slices per chunk (flag stride)
   if (blockIdx.x == 0 && threadIdx.x == 0) P.state->t_rs_start = globaltimer();
-  // barrier (1) among the non-stragglers, per CTA slot (with LL also
-  // announced to the straggler, which may gate its up-front pushes on it)
-  if (threadIdx.x < W && (int)threadIdx.x != me && ((int)threadIdx.x != P.sigma || P.use_ll))
+  // barrier (1) among the non-stragglers, per CTA slot
+  if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
     st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, P.fstride, s), ep, P.sys_scope);
   // one waiting thread per peer: the acquire loads overlap instead of queueing
   int ok = 1;
@@ -562,6 +572,8 @@ __device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t
     } else {
       // "partial ready" for the straggler's half of the exchange
       cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, P.fstride, v), ep, P.sys_scope);
+      // and for this rank's own exchange when another op lane runs it
+      if (P.lanes > 1 && threadIdx.x == 0) st_release(flag_at(P.flags[me], SLOT_RS_LOCAL, P.fstride, v), ep, false);
     }
   }
 }
@@ -689,222 +701,39 @@ __device__ void bcast_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint3
     }
 }
 
-// ---------------------------------------------------------------- LL Phase B (small chunks)
-// Low-latency variant of complete_body: every transfer is a stream of 8-byte
-// words (4 payload bytes | epoch << 32) stored into the receiver's LL area; the
-// receiver polls the words themselves.  No release fence, no separate flag and
-// no store-completion wait per hop, and no CTA-wide synchronisation: thread t
-// of slice s owns the same words of a chunk in every op, so each thread runs
-// its own words through the rounds (the dependency order is the schedule's
-// round order, as in complete_body).  Same arithmetic per word, same bits.
-#ifndef STRAGGLAR_LL_GENTLE
-#define STRAGGLAR_LL_GENTLE 0
-#endif
-constexpr int kLLBatch = 8;
-
-__device__ __forceinline__ uint32_t ld_word(const char* buf, uint64_t o, uint64_t end) {
-  if (o + 4 <= end) return *reinterpret_cast<const uint32_t*>(buf + o);
-  return (uint32_t)(*reinterpret_cast<const uint16_t*>(buf + o));   // bf16 tail: 2 valid bytes
-}
-__device__ __forceinline__ void st_word(char* buf, uint64_t o, uint64_t end, uint32_t v) {
-  if (o + 4 <= end)
-    *reinterpret_cast<uint32_t*>(buf + o) = v;
-  else
-    *reinterpret_cast<uint16_t*>(buf + o) = (uint16_t)v;
-}
-
-// Poll kLLBatch words (w = base + j*nthr < wend) of `ll` until they carry epoch ep.
-__device__ __forceinline__ bool ll_poll_batch(const uint64_t* ll, uint64_t base, uint64_t wend, uint32_t ep,
-                                              uint32_t (&val)[kLLBatch], const LaunchPlan& P, uint32_t where) {
-  const bool sys = P.sys_scope;
-  const uint32_t nthr = blockDim.x;
-  uint64_t v[kLLBatch];
-#pragma unroll
-  for (int j = 0; j < kLLBatch; ++j) {
-    const uint64_t w = base + (uint64_t)j * nthr;
-    v[j] = (w < wend) ? ld_ll(ll + w, sys) : ((uint64_t)ep << 32);
-  }
-  uint64_t t0 = 0;
-  for (uint32_t it = 0;; ++it) {
-    bool all = true;
-#if STRAGGLAR_LL_GENTLE
-    // poll one outstanding word at a time (words of a batch arrive together)
-#pragma unroll
-    for (int j = 0; j < kLLBatch; ++j) {
-      if (all && (uint32_t)(v[j] >> 32) != ep) {
-        all = false;
-        v[j] = ld_ll(ll + base + (uint64_t)j * nthr, sys);
-      }
-    }
-    if (!all) __nanosleep(STRAGGLAR_LL_GENTLE);
-#else
-#pragma unroll
-    for (int j = 0; j < kLLBatch; ++j) {
-      if ((uint32_t)(v[j] >> 32) != ep) {
-        all = false;
-        v[j] = ld_ll(ll + base + (uint64_t)j * nthr, sys);
-      }
-    }
-#endif
-    if (all) break;
-    if (it == 0) t0 = globaltimer();
-    if ((it & 255) == 255) {
-      if (*(volatile uint32_t*)&P.state->err) return false;
-      if (globaltimer() - t0 > P.timeout_ns) {
-        if (atomicCAS(&P.state->err, 0u, (uint32_t)ERR_TIMEOUT) == 0u) atomicExch(&P.state->err_info, where);
-        return false;
-      }
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < kLLBatch; ++j) val[j] = (uint32_t)v[j];
-  return true;
-}
-
-// word-stream modes
-enum LLMode : int { LL_PUSH = 0, LL_EXCH = 1, LL_FWD = 2, LL_FWD_UNPACK = 3, LL_UNPACK = 4 };
-
-// Words [wa, wb) of one chunk slice.  ub: user buffer, cb0: the chunk's first
-// byte in it, end: buffer byte end; mll: my LL area of the chunk, pll: the
-// peer's LL area of the chunk (unused for LL_UNPACK).
-template <int DT, int MODE>
-__device__ bool ll_words(char* ub, uint64_t cb0, uint64_t end, const uint64_t* mll, uint64_t* pll, uint64_t wa,
-                         uint64_t wb, uint32_t ep, const LaunchPlan& P, uint32_t where) {
-  const bool sys = P.sys_scope;
-  const uint32_t nthr = blockDim.x;
-  for (uint64_t base = wa + threadIdx.x; base < wb; base += (uint64_t)kLLBatch * nthr) {
-    uint32_t val[kLLBatch];
-    if constexpr (MODE != LL_PUSH) {
-      if (!ll_poll_batch(mll, base, wb, ep, val, P, where)) return false;
-    }
-#pragma unroll
-    for (int j = 0; j < kLLBatch; ++j) {
-      const uint64_t w = base + (uint64_t)j * nthr;
-      if (w >= wb) break;
-      const uint64_t o = cb0 + 4 * w;
-      if constexpr (MODE == LL_PUSH) {
-        st_ll(pll + w, ld_word(ub, o, end), ep, sys);
-      } else if constexpr (MODE == LL_EXCH) {
-        const uint32_t z = add_word<DT>(ld_word(ub, o, end), val[j]);
-        st_word(ub, o, end, z);
-        st_ll(pll + w, z, ep, sys);
-      } else if constexpr (MODE == LL_FWD) {
-        st_ll(pll + w, val[j], ep, sys);
-      } else if constexpr (MODE == LL_FWD_UNPACK) {
-        st_word(ub, o, end, val[j]);
-        st_ll(pll + w, val[j], ep, sys);
-      } else {
-        st_word(ub, o, end, val[j]);
-      }
-    }
-  }
-  return true;
-}
-
-template <int DT, int W>
-__device__ void ll_phase_b(const LaunchPlan& P, int s, int me, uint32_t ep) {
-  const int G = P.G, V = 16 / P.esize, es = P.esize;
-  const uint64_t end = P.count * es;
-  char* ub = P.buf[me];
-  const int own = (me == P.sigma) ? -1 : P.logical_of_phys[me];
-  uint32_t unpacked = 0;   // chunks whose LL words were already written to the user buffer
-  // which half of chunk c this rank computed itself in the exchange: 1 low, 2 high, 0 none
-  auto local_half = [&](int c) { return c == own ? 1 : (me == P.sigma ? 2 : 0); };
-  struct Words {
-    uint64_t cb0, wa, wm, wb;
-  };
-  auto words_of = [&](int c) {
-    const Range cr = chunk_range(P, c);
-    const Range sl = slice_of(cr.lo, cr.hi, s, G, V);
-    const uint64_t nvec = (sl.hi - sl.lo + V - 1) / V;
-    const uint64_t mid = sl.lo + (nvec / 2) * V < sl.hi ? sl.lo + (nvec / 2) * V : sl.hi;
-    Words w;
-    w.cb0 = cr.lo * es;
-    w.wa = (sl.lo * es - w.cb0) / 4;
-    w.wm = (mid * es - w.cb0) / 4;
-    w.wb = (sl.hi * es - w.cb0 + 3) / 4;
-    return w;
-  };
-  bool ok = true;
-  // Exchange operands go out first, so every exchange only waits for its
-  // partner's operand (as the flag protocol's exchange only waits for Phase A),
-  // not for the partner to reach that round: non-stragglers send the
-  // straggler their partial of its half of their chunk; the straggler sends
-  // every owner x_sigma for the owner's half.
-  // ll_gate (per-process mode, set by the host when the previous call used the
-  // LL areas with another layout): a peer may still be consuming words of that
-  // call which this call's up-front pushes would overwrite, so each push waits
-  // for the receiver's arrival in this call (it then finished the previous one).
-  if (me == P.sigma) {
-    for (int c = 0; c < P.nchunks; ++c) {
-      int owner = 0;
-#pragma unroll
-      for (int q = 0; q < W; ++q)
-        if (P.logical_of_phys[q] == c) owner = q;
-      if (P.ll_gate && !cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + owner, P.fstride, s), ep, P, 0xF00 | c)) return;
-      const Words w = words_of(c);
-      ll_words<DT, LL_PUSH>(ub, w.cb0, end, nullptr, P.ll[owner] + (size_t)c * kLLChunkWords, w.wa, w.wm, ep, P, 0);
-    }
-  } else {
-    if (P.ll_gate && !cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + P.sigma, P.fstride, s), ep, P, 0xF10)) return;
-    const Words w = words_of(own);
-    ll_words<DT, LL_PUSH>(ub, w.cb0, end, nullptr, P.ll[P.sigma] + (size_t)own * kLLChunkWords, w.wm, w.wb, ep, P,
-                          0);
-  }
-  for (int k = 0; k < P.nops[me] && ok; ++k) {
-    const Op op = P.ops[me][k];
-    const int c = op.chunk, peer = op.peer;
-    const Words w = words_of(c);
-    const uint64_t* mll = P.ll[me] + (size_t)c * kLLChunkWords;
-    uint64_t* pll = P.ll[peer] + (size_t)c * kLLChunkWords;
-    const uint32_t where = 0xB00 | k;
-    if (op.kind == OP_EXCH_LOW) {
-      // my half: x_sigma arrived (pushed up front), add, keep, send the result
-      ok = ll_words<DT, LL_EXCH>(ub, w.cb0, end, mll, pll, w.wa, w.wm, ep, P, where);
-    } else if (op.kind == OP_EXCH_HIGH) {
-      ok = ll_words<DT, LL_EXCH>(ub, w.cb0, end, mll, pll, w.wm, w.wb, ep, P, where);
-    } else {
-      const int lh = local_half(c);
-      const bool first = !((unpacked >> c) & 1u);
-      const uint64_t l0 = lh == 1 ? w.wa : w.wm, l1 = lh == 1 ? w.wm : w.wb;   // local half (if any)
-      const uint64_t r0 = lh == 1 ? w.wm : w.wa, r1 = lh == 1 ? w.wb : w.wm;   // LL half
-      if (lh) ll_words<DT, LL_PUSH>(ub, w.cb0, end, mll, pll, l0, l1, ep, P, where);
-      const uint64_t f0 = lh ? r0 : w.wa, f1 = lh ? r1 : w.wb;
-      ok = first ? ll_words<DT, LL_FWD_UNPACK>(ub, w.cb0, end, mll, pll, f0, f1, ep, P, where)
-                 : ll_words<DT, LL_FWD>(ub, w.cb0, end, mll, pll, f0, f1, ep, P, where);
-      unpacked |= 1u << c;
-    }
-  }
-  // postcondition: the LL words of every chunk not yet forwarded land in the buffer
-  for (int c = 0; c < P.nchunks && ok; ++c) {
-    if ((unpacked >> c) & 1u) continue;
-    const Words w = words_of(c);
-    const uint64_t* mll = P.ll[me] + (size_t)c * kLLChunkWords;
-    const int lh = local_half(c);
-    const uint64_t f0 = lh == 1 ? w.wm : w.wa, f1 = lh == 2 ? w.wm : w.wb;
-    ok = ll_words<DT, LL_UNPACK>(ub, w.cb0, end, mll, nullptr, f0, f1, ep, P, 0xD00 | c);
-  }
-}
-
-// Phase B body (Algorithm 1 round executor) for rank `me`, CTA slot s: walks
-// the rank's op list in round order; every op runs over the CTA's `sub`
-// slices one after the other, each handed to the partner with its own flag.
-template <int DT, int W, int MV>
-__device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
+// Phase B body (Algorithm 1 round executor) for rank `me`, CTA slot s, op
+// lane q: walks the rank's ops k with k % lanes == q in round order; every op
+// runs over the CTA's `sub` slices one after the other, each handed to the
+// partner with its own flag.  With one lane a CTA runs all of the rank's ops
+// of its slice in round order.  With several lanes (small messages, where a
+// hop's latency, not bandwidth, is the cost) each op starts as soon as its
+// own inputs have landed — the transfers, partners and bytes are Algorithm 1's,
+// only the round barrier is replaced by the data dependencies: the straggler's
+// n-1 exchanges (independent of each other) no longer queue behind one CTA.
+// Lanes hand off through local flags: an exchange's own half (SLOT_SELF, for a
+// later send of that chunk on another lane) and, in the fused call, lane 0's
+// Phase-A partial (SLOT_RS_LOCAL, for the exchange).
+template <int DT, int W, int MV, bool FUSED>
+__device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int me, uint32_t ep) {
   const int NV = P.G * P.sub;   // slices per chunk (flag stride)
   const int V = 16 / P.esize;
+  const int lanes = P.lanes;
   constexpr bool tma = MV == MOVER_TMA;
   // the straggler reaches barrier (2): announce per CTA slot to the others
-  if (me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
+  if (q == 0 && me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
     st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, P.fstride, s), ep, P.sys_scope);
-  if (P.use_ll) {
-    ll_phase_b<DT, W>(P, s, me, ep);
-    return;
-  }
   char* mine = P.buf[me];
   const int nops = P.nops[me];
+  // lane of this rank's exchange op of chunk c (-1: no exchange of c here)
+  auto exch_lane = [&](int c) {
+    for (int k = 0; k < nops; ++k) {
+      const Op o = P.ops[me][k];
+      if (o.chunk == c && (o.kind == OP_EXCH_LOW || o.kind == OP_EXCH_HIGH)) return k % lanes;
+    }
+    return -1;
+  };
   bool ok = true;
-  for (int k = 0; k < nops && ok; ++k) {
+  for (int k = q; k < nops && ok; k += lanes) {
     const Op op = P.ops[me][k];
     const int c = op.chunk, peer = op.peer;
     const Range cr = chunk_range(P, c);
@@ -918,6 +747,8 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
       const uint64_t mid = sl.lo + (nvec_total / 2) * V < sl.hi ? sl.lo + (nvec_total / 2) * V : sl.hi;
       if (op.kind == OP_EXCH_LOW) {
         // non-straggler r: [lo, mid) of c_r = partial_r (+) x_sigma, stored at both ends
+        if (FUSED && q != 0 && !(ok = cta_wait(flag_at(P.flags[me], SLOT_RS_LOCAL, P.fstride, v), ep, P, 0x210 | k, true)))
+          break;
         if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, P.fstride, s), ep, P, 0x200 | k))) break;
         if (tr) tr[1] = globaltimer();
         const uint64_t a = sl.lo * P.esize, b = mid * P.esize, body = (b - a) / 16 * 16;
@@ -939,8 +770,14 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
         add2_tail<DT>(mine + a + body, P.buf[peer] + a + body, P.buf[peer] + a + body, mine + a + body,
                       (int)((b - a) % 16) / P.esize, P.esize);
       } else {
-        // copy of a fully reduced chunk (push)
+        // copy of a fully reduced chunk (push); if this rank computed half of it
+        // in an exchange on another lane, that half must have been stored too
         if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, P.fstride, v), ep, P, 0x400 | k))) break;
+        if (lanes > 1) {
+          const int el = exch_lane(c);
+          if (el >= 0 && el != q && !(ok = cta_wait(flag_at(P.flags[me], SLOT_SELF + c, P.fstride, v), ep, P, 0x410 | k, true)))
+            break;
+        }
         if (tr) tr[1] = globaltimer();
         const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize, body = (b - a) / 16 * 16;
         if constexpr (tma)
@@ -950,14 +787,19 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int me, ui
         copy_tail(P.buf[peer] + a + body, mine + a + body, (int)((b - a) % 16));
       }
       cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, P.fstride, v), ep, P.sys_scope);
+      if (lanes > 1 && op.kind != OP_SEND && threadIdx.x == 0)
+        st_release(flag_at(P.flags[me], SLOT_SELF + c, P.fstride, v), ep, false);
       if (tr) tr[2] = globaltimer();
     }
   }
   // postcondition: every chunk has landed here (one waiting thread per
-  // (chunk, slice) flag, so the acquire loads overlap)
-  if (ok && (int)threadIdx.x < P.nchunks * P.sub) {
-    const int c = threadIdx.x / P.sub, j = threadIdx.x % P.sub;
-    spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, P.fstride, s * P.sub + j), ep, P, 0x500 | c);
+  // (chunk, slice) flag, so the acquire loads overlap; lanes split the chunks)
+  if (ok) {
+    const int nc = (P.nchunks - q + lanes - 1) / lanes;   // chunks c = q, q + lanes, ...
+    if ((int)threadIdx.x < nc * P.sub) {
+      const int c = q + (threadIdx.x / P.sub) * lanes, j = threadIdx.x % P.sub;
+      spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, P.fstride, s * P.sub + j), ep, P, 0x500 | c);
+    }
   }
   __syncthreads();
 }
@@ -1028,7 +870,9 @@ __device__ void direct_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint
 //       7 Broadcast baseline completion, 8 both in one launch.
 template <int DT, int W, int MV, int KIND>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_constant__ LaunchPlan P) {
-  const int li = blockIdx.x / P.G, s = blockIdx.x % P.G;
+  // block -> (local rank, slice slot s, op lane q); lanes > 1 only for Phase B (KIND 1 / 4)
+  const int per = P.G * P.lanes;
+  const int li = blockIdx.x / per, s = (blockIdx.x % per) % P.G, q = (blockIdx.x % per) / P.G;
   const int me = P.local_rank[li];
   const uint32_t ep = call_epoch(P);
   Pipe pipe = make_pipe(MV == MOVER_TMA);
@@ -1047,10 +891,10 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_con
     __syncthreads();
   }
   if constexpr (KIND == 0 || KIND == 4 || KIND == 5)
-    if (me != P.sigma) rs_body<DT, W, MV>(P, pipe, s, me, ep);
+    if (me != P.sigma && q == 0) rs_body<DT, W, MV>(P, pipe, s, me, ep);
   if (stamps && threadIdx.x == 0)
     atomicMax(reinterpret_cast<unsigned long long*>(&stamp[1]), (unsigned long long)globaltimer());
-  if constexpr (KIND == 1 || KIND == 4) complete_body<DT, W, MV>(P, pipe, s, me, ep);
+  if constexpr (KIND == 1 || KIND == 4) complete_body<DT, W, MV, KIND == 4>(P, pipe, s, q, me, ep);
   if constexpr (KIND == 3 || KIND == 5) direct_body<DT, W, MV>(P, pipe, s, me, ep);
   if constexpr (KIND == 6 || KIND == 8)
     if (me != P.sigma) {

@@ -26,7 +26,12 @@ enum Slot : int {
   SLOT_BC_READY = 49,    // + physical rank q: q finished the non-straggler AllReduce (at q's sender)
   SLOT_RHD_READY = 57,   // + step (0..5): the step's partner finished its previous step (step 0: arrived)
   SLOT_RHD_DONE = 63,    // + AllGather step (0..2): that step's partner finished reading my buffer
-  kSlots = 72
+  SLOT_PROBE = 66,       // K0 flag ping-pong (stragglar_probe_pingpong): the peer's latest hop
+  // op lanes (LaunchPlan::lanes > 1): a rank's ops run on several CTAs per slice,
+  // so the hand-offs between its own lanes need local flags
+  SLOT_SELF = 67,        // + chunk: my half of my exchange of the chunk is stored (local)
+  SLOT_RS_LOCAL = 75,    // my Phase-A partial of the slice is stored (local; fused call)
+  kSlots = 80
 };
 
 #ifndef STRAGGLAR_THREADS
@@ -35,11 +40,6 @@ enum Slot : int {
 constexpr int kThreads = STRAGGLAR_THREADS;   // CTA size of the data kernels
 constexpr int kMaxSlices = 1024;
 constexpr int kMaxSub = 16;                   // slices per CTA (LaunchPlan::sub) at most
-// Low-latency (LL) Phase B for small chunks: every 8-byte word carries 4
-// payload bytes and the call epoch; per rank one LL area of kLLChunkBytes of
-// payload per chunk follows the flag array in the same allocation.
-constexpr uint32_t kLLChunkBytes = 256u * 1024u;
-constexpr uint32_t kLLChunkWords = kLLChunkBytes / 4;
 
 // Device-resident per-communicator state (in the launching process's memory).
 struct DevState {
@@ -54,6 +54,12 @@ struct DevState {
   // Phase B} of call e.  The last CTA of call e re-arms [(e + 1) & 1] for the
   // next call (no host memset per call).
   uint64_t stamp[2][3];
+  // K0 probes: the ping-pong's hop counter (advanced identically on both
+  // ranks of a pair) and the duration of the last ping-pong (ns, %globaltimer)
+  uint32_t probe_seq;
+  uint32_t probe_pad;
+  uint64_t probe_ns;
+  uint64_t t_barrier;    // %globaltimer when this rank left the last device barrier (start skew)
 };
 
 enum ErrCode : uint32_t { ERR_TIMEOUT = 1, ERR_BAD_PLAN = 2 };
@@ -69,6 +75,9 @@ struct LaunchPlan {
   int sub;                   // slices per CTA: every chunk is cut into G * sub slices and CTA s
                              // handles slices s*sub .. s*sub+sub-1, one flag each (finer-grained
                              // hand-offs between ranks with the same CTAs); 1 = one slice per CTA
+  int lanes;                 // op lanes per slice (Phase B): CTA lane q runs the rank's ops k with
+                             // k % lanes == q, each as soon as its own inputs have landed (1 = one
+                             // CTA walks all ops of the slice in round order)
   int nlocal;                // ranks served by this launch (1, or world in team mode)
   int fstride;               // flags per slot (G_max * kMaxSub, fixed per communicator; see flag_at)
   int local_rank[kMaxWorld]; // physical rank of local index i (blockIdx.x / G)
@@ -84,9 +93,7 @@ struct LaunchPlan {
   int sys_scope;             // 1: flags/fences at system scope (peers on other GPUs); 0: gpu scope (team)
   uint64_t timeout_ns;
   DevState* state;
-  uint64_t* ll[kMaxWorld];   // LL area of each physical rank: [chunk][word] (payload | epoch << 32)
-  int use_ll;                // Phase B through the LL areas (small chunks)
-  int ll_gate;               // LL up-front pushes wait for the receiver's arrival (see ll_phase_b)
+  uint32_t* host_err;        // pinned host word (device-mapped): the first error, sticky (api.cu)
   uint64_t sigma_delay_ns;   // team measurement only: straggler CTAs start this late (KIND 4/5)
   uint64_t* trace;           // optional: [rank][slice][op][3] %globaltimer stamps (wait, data, done) of Phase B
   int logical_of_phys[kMaxWorld];
@@ -95,6 +102,20 @@ struct LaunchPlan {
   int bc_round[kMaxWorld];   //   and in which round
   int nops[kMaxWorld];       // by physical rank
   Op ops[kMaxWorld][kMaxOps];// by physical rank
+};
+
+// K0 copy probe (stragglar_probe_copy): this rank moves `bytes` to / from
+// each peer in `peers` at once.  Push: local[me*bytes ..] -> peer[me*bytes ..];
+// pull: peer[p*bytes ..] -> local[p*bytes ..] (disjoint segments, so every
+// rank may probe at the same time).  CTA b serves peers[b % npeers].
+struct ProbeArgs {
+  char* local;
+  char* peer[kMaxWorld];
+  uint64_t bytes;
+  int me;
+  int npeers;
+  int peers[kMaxWorld];
+  int pull;                  // 0: push (remote stores), 1: pull (remote loads)
 };
 
 }  // namespace stragglar

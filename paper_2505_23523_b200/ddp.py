@@ -7,12 +7,20 @@ persistent straggler remapped once.  Here the same glue is a DDP comm hook:
     comm = ProcessComm(straggler_rank)          # paper_2505_23523_b200.dist
     ddp.register_comm_hook(StragglarHookState(comm), stragglar_hook)
 
-Every bucket's flat gradient buffer is peer-mapped the first time it is seen
-(a collective step: DDP presents buckets in the same order on every rank) and
-reduced in place by the per-process communicator.  Like DDP's default
-allreduce hook the gradients are divided by the world size (before the sum,
-as DDP does).  The division is the only torch op in the hook; the reduction
-runs in the library's kernels.
+The library reduces peer-mapped (registered) buffers only.  DDP's bucket
+tensors are not a safe thing to register: DDP rebuilds its buckets after the
+first iteration and the caching allocator reuses freed memory, so whether a
+bucket's address is "already registered" is a per-rank fact that ranks can
+disagree on (a rank would then block in the collective registration while its
+peers spin in a kernel, or peers would write through a stale mapping).  The
+hook therefore reduces through one persistent registered staging buffer owned
+by the hook state: the bucket is scaled by 1/world into it (the division DDP's
+default hook does, so the copy-in costs no extra pass), reduced in place by
+the library's kernels, and copied back.  The staging buffer only ever grows,
+and it grows at the same bucket on every rank — bucket sizes and order are
+identical across ranks — so its (collective) registration is always entered
+by all ranks together.  Outgrown staging buffers stay registered (peers may
+still read them) until ``close()``.
 """
 
 import torch
@@ -33,29 +41,47 @@ class StragglarHookState:
         if self.mode not in ("schedule", "direct", "auto"):
             raise ValueError(f"unknown mode {self.mode}")
         self.expected_delay_ns = int(expected_delay_ns)
-        self.picks: list = []        # "auto": (bucket index, algorithm) per call, for inspection
-        self._registered: list = []  # (data_ptr, nbytes) of peer-mapped bucket buffers
+        self.picks: list = []          # "auto": (bucket index, algorithm) per call, for inspection
+        self._staging = {}             # dtype -> registered staging buffer (1-D, grows only)
+        self._retired: list = []       # outgrown staging buffers (kept mapped until close)
 
-    def _ensure_registered(self, buf: torch.Tensor) -> None:
-        p, nb = buf.data_ptr(), buf.numel() * buf.element_size()
-        for q, qb in self._registered:
-            if q <= p and p + nb <= q + qb:
-                return
-        self.comm.register(buf)                 # collective: all ranks reach it in bucket order
-        self._registered.append((p, nb))
+    def staging(self, like: torch.Tensor) -> torch.Tensor:
+        """A registered buffer with room for `like` (same dtype); growing it is
+        collective, and happens at the same bucket on every rank."""
+        cur = self._staging.get(like.dtype)
+        n = like.numel()
+        if cur is None or cur.numel() < n:
+            if cur is not None:
+                self._retired.append(cur)
+            cap = max(n, int(cur.numel() * 1.5) if cur is not None else 0)
+            cap = (cap + 127) // 128 * 128
+            cur = torch.empty(cap, dtype=like.dtype, device=like.device)
+            self.comm.register(cur)      # collective: every rank reaches it at this bucket
+            self._staging[like.dtype] = cur
+        return cur[:n]
+
+    def close(self) -> None:
+        """Unmap every staging buffer (call on every rank, before comm.close())."""
+        torch.cuda.synchronize()
+        dist.barrier(self.comm.group)
+        for t in list(self._staging.values()) + self._retired:
+            self.comm.deregister(t)
+        self._staging.clear()
+        self._retired.clear()
 
 
 def stragglar_hook(state: StragglarHookState, bucket: dist.GradBucket) -> torch.futures.Future[torch.Tensor]:
     buf = bucket.buffer()
-    state._ensure_registered(buf)
-    buf.div_(state.comm.world)
+    stage = state.staging(buf)
+    torch.div(buf.view(-1), state.comm.world, out=stage)
     if state.mode == "direct":
-        state.comm.lib.stragglar_allreduce_direct(buf)
+        state.comm.lib.stragglar_allreduce_direct(stage)
     elif state.mode == "auto":
         delay = state.expected_delay_ns if bucket.index() == 0 else 0
-        state.picks.append((bucket.index(), state.comm.lib.stragglar_allreduce_auto(buf, delay)))
+        state.picks.append((bucket.index(), state.comm.lib.stragglar_allreduce_auto(stage, delay)))
     else:
-        state.comm.allreduce(buf)
+        state.comm.allreduce(stage)
+    buf.view(-1).copy_(stage)
     fut: torch.futures.Future[torch.Tensor] = torch.futures.Future()
     fut.set_result(buf)
     return fut

@@ -48,6 +48,11 @@ class ProcessComm:
         self.lib.stragglar_import_buffer(tensor, blobs, self.world)
         self.registered.append(tensor)
 
+    def deregister(self, tensor) -> None:
+        """Unmap the peers' copies of a registered buffer (every rank, before freeing it)."""
+        self.lib.stragglar_deregister_buffer(tensor)
+        self.registered = [t for t in self.registered if t is not tensor]
+
     def allreduce(self, tensor, stream=None) -> None:
         self.lib.stragglar_allreduce(tensor, stream)
 

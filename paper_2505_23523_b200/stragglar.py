@@ -53,6 +53,11 @@ _SIGS = {
     "stragglar_import_handles": ([_vp, _c_int], _c_int),
     "stragglar_register_buffer": ([_vp, _c_size, _vp], _c_int),
     "stragglar_import_buffer": ([_vp, _vp, _c_int], _c_int),
+    "stragglar_deregister_buffer": ([_vp], _c_int),
+    "stragglar_shared_device_ranks": ([ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)], _c_int),
+    "stragglar_probe_copy": ([_vp, _c_size, _c_int, ctypes.c_uint32, _c_int, _vp], _c_int),
+    "stragglar_probe_pingpong": ([_c_int, _c_int, _vp], _c_int),
+    "stragglar_probe_pingpong_result": ([ctypes.POINTER(ctypes.c_double)], _c_int),
     "stragglar_allreduce": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_allreduce_ring": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_allreduce_direct": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
@@ -61,6 +66,7 @@ _SIGS = {
     "stragglar_allreduce_bcast": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_broadcast_tree": ([_c_int, ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)], _c_int),
     "stragglar_barrier": ([_vp], _c_int),
+    "stragglar_last_barrier_ns": ([ctypes.POINTER(_c_u64)], _c_int),
     "stragglar_inject_delay": ([_c_u64, _vp], _c_int),
     "stragglar_check_error": ([ctypes.POINTER(_c_int)], _c_int),
     "stragglar_finalize": ([], _c_int),
@@ -136,6 +142,13 @@ def _ptr_array(ts: Sequence) -> ctypes.Array:
     return arr
 
 
+def _dev_args(t):
+    """A per-process buffer: contiguous CUDA tensor of a supported dtype."""
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("buffers must be contiguous CUDA tensors")
+    return t.data_ptr(), t.numel(), _dtype_code(t)
+
+
 def _team_args(bufs: Sequence):
     if not bufs:
         raise ValueError("empty buffer list")
@@ -194,6 +207,8 @@ def stragglar_import_handles(blobs: bytes, world: int) -> None:
 
 def stragglar_register_buffer(t) -> bytes:
     buf = ctypes.create_string_buffer(stragglar_handle_size())
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("registered buffers must be contiguous CUDA tensors")
     nbytes = t.numel() * t.element_size()
     _ck("stragglar_register_buffer", _lib.stragglar_register_buffer(t.data_ptr(), nbytes, buf))
     return buf.raw
@@ -203,24 +218,60 @@ def stragglar_import_buffer(t, blobs: bytes, world: int) -> None:
     _ck("stragglar_import_buffer", _lib.stragglar_import_buffer(t.data_ptr(), ctypes.c_char_p(blobs), world))
 
 
+def stragglar_deregister_buffer(t) -> None:
+    _ck("stragglar_deregister_buffer", _lib.stragglar_deregister_buffer(t if isinstance(t, int) else t.data_ptr()))
+
+
+def stragglar_shared_device_ranks():
+    """-> (ranks of this communicator on this rank's GPU, CTAs per rank per launch)."""
+    a, b = _c_int(0), _c_int(0)
+    _ck("stragglar_shared_device_ranks", _lib.stragglar_shared_device_ranks(ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+PROBE_PUSH, PROBE_PULL, PROBE_TMA = 0, 1, 2
+
+
+def stragglar_probe_copy(t, bytes_per_peer: int, mode: int, peers, ctas: int = 0, stream=None) -> None:
+    """K0: device-initiated copies with every peer in `peers` at once (see include/stragglar.h)."""
+    mask = 0
+    for p in peers:
+        mask |= 1 << int(p)
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("probe buffer must be a contiguous CUDA tensor")
+    _ck("stragglar_probe_copy", _lib.stragglar_probe_copy(t.data_ptr(), int(bytes_per_peer), int(mode), mask,
+                                                           int(ctas), _stream_ptr(stream)))
+
+
+def stragglar_probe_pingpong(peer: int, iters: int, stream=None) -> None:
+    _ck("stragglar_probe_pingpong", _lib.stragglar_probe_pingpong(int(peer), int(iters), _stream_ptr(stream)))
+
+
+def stragglar_probe_pingpong_result() -> float:
+    """-> device time (us) of the last ping-pong (all its round trips)."""
+    v = ctypes.c_double(0.0)
+    _ck("stragglar_probe_pingpong_result", _lib.stragglar_probe_pingpong_result(ctypes.byref(v)))
+    return v.value
+
+
 def stragglar_allreduce(t, stream=None) -> None:
-    _ck("stragglar_allreduce",
-        _lib.stragglar_allreduce(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream)))
+    ptr, n, dt = _dev_args(t)
+    _ck("stragglar_allreduce", _lib.stragglar_allreduce(ptr, n, dt, SUM, _stream_ptr(stream)))
 
 
 def stragglar_allreduce_ring(t, stream=None) -> None:
-    _ck("stragglar_allreduce_ring",
-        _lib.stragglar_allreduce_ring(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream)))
+    ptr, n, dt = _dev_args(t)
+    _ck("stragglar_allreduce_ring", _lib.stragglar_allreduce_ring(ptr, n, dt, SUM, _stream_ptr(stream)))
 
 
 def stragglar_allreduce_host(host_in, host_out, t, stream=None) -> None:
     """host_in/host_out: contiguous CPU tensors (pinned for full bandwidth) shaped like t."""
+    ptr, n, dt = _dev_args(t)
     for h in (host_in, host_out):
-        if h.is_cuda or h.numel() != t.numel() or h.dtype != t.dtype or not h.is_contiguous():
+        if h.is_cuda or h.numel() != n or h.dtype != t.dtype or not h.is_contiguous():
             raise ValueError("host buffers must be contiguous CPU tensors matching the device buffer")
     _ck("stragglar_allreduce_host",
-        _lib.stragglar_allreduce_host(host_in.data_ptr(), host_out.data_ptr(), t.data_ptr(), t.numel(),
-                                      _dtype_code(t), SUM, _stream_ptr(stream)))
+        _lib.stragglar_allreduce_host(host_in.data_ptr(), host_out.data_ptr(), ptr, n, dt, SUM, _stream_ptr(stream)))
 
 
 def stragglar_select(world: int, nbytes: float, delay_s: float, alpha_s: float, beta_s_per_byte: float):
@@ -251,25 +302,25 @@ def stragglar_set_cost_model(alpha_s: float, beta_s_per_byte: float) -> None:
 def stragglar_allreduce_auto(t, expected_delay_ns: int, stream=None) -> str:
     """Runs the algorithm the cost model picks; returns its name ("stragglar", "ring" or "rhd")."""
     used = _c_int(0)
+    ptr, n, dt = _dev_args(t)
     _ck("stragglar_allreduce_auto",
-        _lib.stragglar_allreduce_auto(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream),
-                                      int(expected_delay_ns), ctypes.byref(used)))
+        _lib.stragglar_allreduce_auto(ptr, n, dt, SUM, _stream_ptr(stream), int(expected_delay_ns), ctypes.byref(used)))
     return ALGO_NAMES[used.value]
 
 
 def stragglar_allreduce_direct(t, stream=None) -> None:
-    _ck("stragglar_allreduce_direct",
-        _lib.stragglar_allreduce_direct(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream)))
+    ptr, n, dt = _dev_args(t)
+    _ck("stragglar_allreduce_direct", _lib.stragglar_allreduce_direct(ptr, n, dt, SUM, _stream_ptr(stream)))
 
 
 def stragglar_allreduce_rhd(t, stream=None) -> None:
-    _ck("stragglar_allreduce_rhd",
-        _lib.stragglar_allreduce_rhd(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream)))
+    ptr, n, dt = _dev_args(t)
+    _ck("stragglar_allreduce_rhd", _lib.stragglar_allreduce_rhd(ptr, n, dt, SUM, _stream_ptr(stream)))
 
 
 def stragglar_allreduce_bcast(t, stream=None) -> None:
-    _ck("stragglar_allreduce_bcast",
-        _lib.stragglar_allreduce_bcast(t.data_ptr(), t.numel(), _dtype_code(t), SUM, _stream_ptr(stream)))
+    ptr, n, dt = _dev_args(t)
+    _ck("stragglar_allreduce_bcast", _lib.stragglar_allreduce_bcast(ptr, n, dt, SUM, _stream_ptr(stream)))
 
 
 def stragglar_broadcast_tree(world: int):
@@ -281,6 +332,12 @@ def stragglar_broadcast_tree(world: int):
 
 def stragglar_barrier(stream=None) -> None:
     _ck("stragglar_barrier", _lib.stragglar_barrier(_stream_ptr(stream)))
+
+
+def stragglar_last_barrier_ns() -> int:
+    v = _c_u64(0)
+    _ck("stragglar_last_barrier_ns", _lib.stragglar_last_barrier_ns(ctypes.byref(v)))
+    return int(v.value)
 
 
 def stragglar_inject_delay(ns: int, stream=None) -> None:

@@ -55,6 +55,7 @@ def worker(rank, world, sigma, port, mode, q):
                 q.put((rank, f"auto picks {state.picks[:6]}"))
                 return
         code = comm.lib.stragglar_check_error()
+        state.close()
         comm.close()
         q.put((rank, "ok" if code == 0 else f"device error {code}"))
         dist.destroy_process_group()

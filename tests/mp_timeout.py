@@ -1,6 +1,8 @@
 """Watchdog check: rank 0 enters the collective, rank 1 never does.  The
 device spin-waits must give up after STRAGGLAR_TIMEOUT_MS, report
 ERR_TIMEOUT through stragglar_check_error, and the kernel must exit (no hang).
+The error is sticky: the next call on the communicator fails with TIMEOUT
+instead of launching on out-of-step flags.
 Launched by tests/test_gpu_multiproc.py.  Exit 0 = behaved as specified."""
 import os
 import sys
@@ -30,7 +32,13 @@ def worker(rank, port, q):
         t0 = time.time()
         comm.allreduce(t)
         torch.cuda.synchronize()
-        res = (S.stragglar_check_error(), time.time() - t0)
+        code, secs = S.stragglar_check_error(), time.time() - t0
+        try:
+            comm.allreduce(t)
+            sticky = "no error"
+        except S.StragglarError as e:
+            sticky = e.status
+        res = (code, secs, sticky)
     dist.barrier()
     comm.close()
     q.put((rank, res))
@@ -46,8 +54,8 @@ if __name__ == "__main__":
     out = dict(q.get(timeout=300) for _ in range(2))
     for p in ps:
         p.join(timeout=60)
-    code, secs = out[0]
-    print(f"error code {code} after {secs:.2f} s")
-    ok = code == 1 and secs < 60
+    code, secs, sticky = out[0]
+    print(f"error code {code} after {secs:.2f} s; next call: {sticky}")
+    ok = code == 1 and secs < 60 and sticky == 6
     print("OK" if ok else "FAIL")
     sys.exit(0 if ok else 1)

@@ -65,7 +65,7 @@ def worker(rank, world, sigma, count, dtype, port, q):
             comm.allreduce_rhd(base["rhd"])
         comm.allreduce_bcast(base["bcast"])
         # back-to-back StragglAR calls of different sizes on prefixes of one
-        # buffer, no host sync: a fast rank's next call (another slice / LL
+        # buffer, no host sync: a fast rank's next call (another slice
         # layout) must not disturb a slow rank's current one
         for n_el in mixed_lengths(count):
             comm.allreduce(base["mixed"][:n_el])

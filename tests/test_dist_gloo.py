@@ -97,3 +97,42 @@ def test_handle_exchange_gloo(world):
         assert calls[3] == ("allreduce", 1000 + r)
         assert calls[4:7] == [("ring", 1000 + r), ("rhd", 1000 + r), ("bcast", 1000 + r)]
         assert calls[7] == ("finalize",)
+
+
+class _FakeComm:
+    """Stands in for ProcessComm: records the collective registrations."""
+
+    def __init__(self, world=4):
+        self.world = world
+        self.group = None
+        self.registered = []
+
+    def register(self, t):
+        self.registered.append(t.numel())
+
+    def deregister(self, t):
+        pass
+
+
+def test_ddp_staging_grows_at_the_same_bucket_everywhere():
+    """the DDP hook must enter the collective registration on every
+    rank together.  The staging buffer's growth depends only on the bucket
+    sizes (identical on every rank), never on the bucket's address."""
+    import torch
+
+    from paper_2505_23523_b200.ddp import StragglarHookState
+
+    sizes = [1000, 600, 5000, 5000, 700, 9000, 100]
+    seqs = []
+    for seed in range(3):
+        comm = _FakeComm()
+        st = StragglarHookState(comm)
+        torch.manual_seed(seed)
+        for n in sizes:
+            b = torch.empty(n + int(torch.randint(0, 3, ())) * 0)   # fresh allocation every time
+            v = st.staging(b)
+            assert v.numel() == n and v.dtype == b.dtype
+        seqs.append(list(comm.registered))
+    assert seqs[0] == seqs[1] == seqs[2]
+    assert len(seqs[0]) == 3                     # grew at buckets 0, 2 and 5 only
+    assert seqs[0][0] >= 1000 and seqs[0][1] >= 5000 and seqs[0][2] >= 9000

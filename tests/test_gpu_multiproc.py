@@ -30,8 +30,8 @@ def _port():
     (4, 0, 99999, "float32", "lsu"),
     (6, 4, 123457, "bfloat16", "tma"),   # Appendix-B schedule (even non-power-of-2 n)
     (8, 3, 500001, "float32", "tma"),    # the full n = 8 schedule across 8 processes
-    (4, 1, 30001, "float32", "tma+ll"),  # LL protocol forced on, system scope
-    (8, 5, 70001, "bfloat16", "lsu+ll"), # LL protocol forced on, 8 processes
+    (4, 1, 30001, "float32", "tma"),
+    (8, 5, 70001, "bfloat16", "lsu"),    # 8 processes, 16-byte loads/stores
     (4, 3, 400003, "float32", "tma+sub"),  # several slices per CTA (sub-slices), system scope
 ])
 def test_multiprocess_ipc(world, sigma, count, dtype, mover):
@@ -41,8 +41,6 @@ def test_multiprocess_ipc(world, sigma, count, dtype, mover):
 
     __graft_entry__.build()
     env = dict(os.environ, STRAGGLAR_MOVER=mover.split("+")[0])
-    if mover.endswith("+ll"):
-        env["STRAGGLAR_LL_MAX_CHUNK"] = "262144"
     if mover.endswith("+sub"):
         env["STRAGGLAR_SLICE_BYTES"] = "1024"       # 8 CTAs per rank (mp_worker), ~4 KB slices: 16 per CTA
         env["STRAGGLAR_SUBSLICE_BYTES"] = "4096"

@@ -342,52 +342,24 @@ def test_randomized_cases(S):
         check_equal(outs, want, xs, dtype, f"case {case}: n={n} s={sigma} {dtype} {count} {pattern} {algo}")
 
 
-@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-@pytest.mark.parametrize("n", [2, 4, 6, 8])
-def test_ll_protocol_vs_regular(S, dtype, n):
-    """Small chunks use the low-latency (LL) Phase B (8-byte words = 4 payload
-    bytes + epoch); force it on and off on the same inputs: both must equal
-    the oracle bit for bit (tails, odd bf16 counts, every straggler)."""
-    old = os.environ.get("STRAGGLAR_LL_MAX_CHUNK")
-    try:
-        for sigma in range(n):
-            for count in [1, 3, 8 * (n - 1) + 5, 20001]:
-                xs = make_inputs(n, count, dtype, config=70 + sigma)
-                want = N.stragglar_allreduce(xs, sigma, dtype)
-                for ll in ("262144", "0"):
-                    os.environ["STRAGGLAR_LL_MAX_CHUNK"] = ll
-                    bufs = [to_dev(x, dtype) for x in xs]
-                    S.stragglar_team_init(n, sigma)
-                    if count % 2:
-                        S.stragglar_team_allreduce(bufs)
-                    else:
-                        S.stragglar_team_reduce_scatter(bufs)
-                        S.stragglar_team_complete(bufs)
-                    torch.cuda.synchronize()
-                    assert S.stragglar_team_check_error() == 0
-                    check_equal([to_host(b, dtype) for b in bufs], want, xs, dtype, f"ll={ll} s={sigma} c={count}")
-    finally:
-        if old is None:
-            os.environ.pop("STRAGGLAR_LL_MAX_CHUNK", None)
-        else:
-            os.environ["STRAGGLAR_LL_MAX_CHUNK"] = old
-
-
 @pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
 def test_system_scope_flags(S, dtype):
     """The per-process (NVLink) mode's memory-model scope — ld.acquire.sys /
-    fence.acq_rel.sys flags and relaxed.sys LL words — exercised in team mode
-    on every Phase-B path (schedule, direct completion, LL) and the Ring."""
-    old = {k: os.environ.get(k) for k in ("STRAGGLAR_SYS_SCOPE", "STRAGGLAR_LL_MAX_CHUNK")}
+    fence.acq_rel.sys flags — exercised in team mode on every Phase-B path
+    (schedule, direct completion) and the Ring, with one and several slices
+    per CTA."""
+    old = {k: os.environ.get(k) for k in ("STRAGGLAR_SYS_SCOPE", "STRAGGLAR_SUBSLICES", "STRAGGLAR_SUBSLICE_BYTES")}
     try:
         os.environ["STRAGGLAR_SYS_SCOPE"] = "1"
-        for n, sigma in [(4, 2), (8, 0), (6, 5)]:
-            for count in [9999, 300001]:
-                for algo, ll in [("stragglar", "0"), ("stragglar", "262144"), ("direct", "0"), ("ring", "0")]:
-                    os.environ["STRAGGLAR_LL_MAX_CHUNK"] = ll
-                    xs, outs = run_team(S, n, sigma, dtype, count, config=80, algo=algo)
-                    want = N.ring_allreduce(xs, dtype) if algo == "ring" else N.stragglar_allreduce(xs, sigma, dtype)
-                    check_equal(outs, want, xs, dtype, f"sys n={n} {algo} ll={ll}")
+        for sub in ("1", "16"):
+            os.environ["STRAGGLAR_SUBSLICES"] = sub
+            os.environ["STRAGGLAR_SUBSLICE_BYTES"] = "4096"
+            for n, sigma in [(4, 2), (8, 0), (6, 5)]:
+                for count in [9999, 300001, 3_000_017]:
+                    for algo in ("stragglar", "direct", "ring"):
+                        xs, outs = run_team(S, n, sigma, dtype, count, config=80, algo=algo)
+                        want = N.ring_allreduce(xs, dtype) if algo == "ring" else N.stragglar_allreduce(xs, sigma, dtype)
+                        check_equal(outs, want, xs, dtype, f"sys n={n} {algo} sub={sub}")
     finally:
         for k, v in old.items():
             if v is None:
