@@ -234,6 +234,48 @@ int stragglar_check_error_where(int team, int* code, uint32_t* where);
 int stragglar_phase_times(double* t_a_us, double* t_total_us);
 int stragglar_finalize(void);
 
+/* ---- NEXT N1(i): NVLink SHARP (NVLS) multicast variant ---
+ * The paper assumes a single-port fabric; an NVSwitch fabric can
+ * also reduce and replicate in the switch.  Same two phases, same straggler
+ * roles: Phase A = each owner's multimem.ld_reduce of its chunk through the
+ * non-stragglers' multicast object (the switch sums the n-1 copies: owner
+ * ingress C instead of (n-2)C); completion = the owner adds x_sigma (one
+ * unicast peer load; the exchange's single add) and writes the
+ * fully reduced chunk to every rank with one multimem.st through the all-rank
+ * multicast object.  Numerics (reading 24): the switch's summation
+ * order over the non-stragglers is unspecified (fp32 accumulation; bf16 via
+ * .acc::f32, rounded once), then x_sigma is added once: int32 results are
+ * exact, float results agree with stragglar_allreduce within the north_star
+ * tolerance, not bit for bit.
+ * Buffers must be the library's arena (VMM memory bound to the multicast
+ * objects; cudaMalloc memory cannot be bound).  Setup is collective, in two
+ * steps around an exchange of POSIX file descriptors that the caller performs
+ * (dist.py passes them over UNIX-domain sockets, SCM_RIGHTS):
+ *   nvls_begin(bytes): allocates this rank's arena (rounded up to the
+ *     multicast granularity, *bytes_out) and exports fds[0] = the all-rank
+ *     multicast object (rank 0; -1 elsewhere), fds[1] = the non-straggler
+ *     object (the lowest non-straggler rank; -1 elsewhere), fds[2] = this
+ *     rank's arena.  The fds stay owned by the library.
+ *   nvls_finish(mc_all_fd, mc_ns_fd, sigma_mem_fd, &arena): imports the
+ *     objects (rank 0 / the lowest non-straggler pass their own), joins them,
+ *     binds the arena, maps the multicast ranges and (non-stragglers) the
+ *     straggler's arena; *arena = this rank's arena (device pointer).
+ * UNSUPPORTED without multicast support (stragglar_nvls_supported) or the
+ * driver entry points; every rank must reach nvls_finish (the binds wait for
+ * the whole team).  Released by stragglar_finalize.
+ * stragglar_allreduce_nvls: in place on [buf, buf + count) inside the arena
+ * (same offset on every rank), count a multiple of 16 bytes' worth of
+ * elements (INVALID_ARG otherwise), NOT_REGISTERED outside the arena.
+ * stragglar_nvls_selftest: one-GPU check of the multicast path — a
+ * one-member multicast object on the current device; host_out = the reducing
+ * load of host_in through it (equal to host_in).  No communicator needed.
+ * MEASURED ONLY ON ONE GPU: the multi-GPU path needs >= 2 NVSwitch GPUs. */
+int stragglar_nvls_supported(int* supported);
+int stragglar_nvls_begin(size_t bytes, int* fds, size_t* bytes_out);
+int stragglar_nvls_finish(int mc_all_fd, int mc_ns_fd, int sigma_mem_fd, void** arena);
+int stragglar_allreduce_nvls(void* buf, size_t count, int dtype, int op, void* stream);
+int stragglar_nvls_selftest(int dtype, size_t count, const void* host_in, void* host_out);
+
 /* ---- single-device team (all ranks on the current device) ---------------
  * bufs: array of `world` device pointers (physical rank order), each 16-byte
  * aligned with `count` elements; they must not overlap. */

@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libstragglar.so")
-SOURCES = ["api.cu", "kernels.cu", "kernels_i32.cu", "kernels_f32.cu", "kernels_bf16.cu", "schedule.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "kernels_i32.cu", "kernels_f32.cu", "kernels_bf16.cu", "nvls.cu", "schedule.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

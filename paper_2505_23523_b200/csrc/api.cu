@@ -6,6 +6,8 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <unistd.h>
+
 #include <atomic>
 #include <cstdlib>
 #include <cstring>
@@ -24,6 +26,8 @@ cudaError_t launch_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st, cu
 cudaError_t launch_barrier(const LaunchPlan& P, cudaStream_t stream);
 cudaError_t occupancy_blocks_per_sm(int which, int dtype, int world, int mover, int* blocks);
 cudaError_t launch_probe_copy(const ProbeArgs& A, int mover, int nblocks, cudaStream_t stream);
+cudaError_t launch_nvls(int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream);
+cudaError_t launch_nvls_selftest(int dtype, char* mc, uint64_t bytes, cudaStream_t stream);
 cudaError_t launch_probe_pingpong(uint32_t* mine, uint32_t* theirs, int initiator, int iters, DevState* st,
                                   uint64_t timeout_ns, uint32_t* host_err, cudaStream_t stream);
 }  // namespace stragglar
@@ -101,6 +105,14 @@ struct Comm {
   double beta_s_per_byte = 1.0 / 770e9; // measured B200 peer copy per direction (B200_PROFILING.md)
   std::vector<Registration> regs;
   std::vector<void*> opened;   // IPC mappings to close
+  // NEXT N1(i) (nvls.cu): the library-owned arena bound to two multicast objects
+  struct Nvls {
+    int stage = 0;                                   // 0 none, 1 begun, 2 ready
+    size_t bytes = 0;                                // arena size (multicast granularity)
+    unsigned long long mem = 0, mc_all = 0, mc_ns = 0, sigma_mem = 0;   // CUmemGenericAllocationHandle
+    unsigned long long va = 0, mc_all_va = 0, mc_ns_va = 0, sigma_va = 0;
+    int fds[3] = {-1, -1, -1};
+  } nvls;
 };
 
 Comm g_proc;   // per-process communicator
@@ -261,9 +273,12 @@ Layout layout_of(const Comm& c) {
 // it — the flags are then out of step, so the caller must re-initialize.
 bool sticky_error(const Comm& c) { return c.host_err && *(volatile const uint32_t*)c.host_err != 0; }
 
+void nvls_release(Comm& c);
+
 void common_finalize(Comm& c) {
   if (!c.active) return;
   cudaDeviceSynchronize();
+  nvls_release(c);
   for (void* p : c.opened) cudaIpcCloseMemHandle(p);
   c.opened.clear();
   for (auto& r : c.regs)
@@ -493,6 +508,65 @@ int e2e_pipeline(int nbufs, const void* const* host_in, void* const* host_out, v
   CK(cudaStreamSynchronize(s));
   return st;
 }
+
+// ---------------------------------------------------------------- driver API (NVLS)
+// The library does not link libcuda: driver functions come through the runtime.
+template <class F>
+F drv(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return nullptr;
+  return reinterpret_cast<F>(fn);
+}
+#define DRV(name) static auto p_##name = drv<decltype(&name)>(#name)
+#define DCK(x)                                            \
+  do {                                                    \
+    if ((x) != CUDA_SUCCESS) return STRAGGLAR_ERR_CUDA;   \
+  } while (0)
+
+int map_va(size_t bytes, CUmemGenericAllocationHandle h, int dev, unsigned long long* va) {
+  DRV(cuMemAddressReserve);
+  DRV(cuMemMap);
+  DRV(cuMemSetAccess);
+  if (!p_cuMemAddressReserve || !p_cuMemMap || !p_cuMemSetAccess) return STRAGGLAR_ERR_CUDA;
+  CUdeviceptr p = 0;
+  DCK(p_cuMemAddressReserve(&p, bytes, 0, 0, 0));
+  DCK(p_cuMemMap(p, bytes, 0, h, 0));
+  CUmemAccessDesc acc = {};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  DCK(p_cuMemSetAccess(p, bytes, &acc, 1));
+  *va = (unsigned long long)p;
+  return STRAGGLAR_OK;
+}
+
+void unmap_va(unsigned long long& va, size_t bytes) {
+  DRV(cuMemUnmap);
+  DRV(cuMemAddressFree);
+  if (va && p_cuMemUnmap && p_cuMemAddressFree) {
+    p_cuMemUnmap((CUdeviceptr)va, bytes);
+    p_cuMemAddressFree((CUdeviceptr)va, bytes);
+  }
+  va = 0;
+}
+
+void nvls_release(Comm& c) {
+  auto& n = c.nvls;
+  if (!n.stage) return;
+  DRV(cuMemRelease);
+  unmap_va(n.mc_all_va, n.bytes);
+  unmap_va(n.mc_ns_va, n.bytes);
+  unmap_va(n.sigma_va, n.bytes);
+  unmap_va(n.va, n.bytes);
+  for (unsigned long long* h : {&n.mc_all, &n.mc_ns, &n.sigma_mem, &n.mem})
+    if (*h && p_cuMemRelease) p_cuMemRelease((CUmemGenericAllocationHandle)*h);
+  for (int& fd : n.fds)
+    if (fd >= 0) close(fd), fd = -1;
+  n = Comm::Nvls();
+}
+
+int lowest_ns(const Comm& c) { return c.sigma == 0 ? 1 : 0; }
 
 }  // namespace
 
@@ -1008,6 +1082,221 @@ int stragglar_finalize(void) {
   std::lock_guard<std::mutex> lk(g_mu);
   common_finalize(g_proc);
   return STRAGGLAR_OK;
+}
+
+// ---------------------------------------------------------------- NEXT N1(i): NVLS multicast (nvls.cu)
+int stragglar_nvls_supported(int* supported) {
+  if (!supported) return STRAGGLAR_ERR_INVALID_ARG;
+  *supported = 0;
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  DRV(cuDeviceGetAttribute);
+  if (!p_cuDeviceGetAttribute) return STRAGGLAR_ERR_CUDA;
+  int v = 0;
+  DCK(p_cuDeviceGetAttribute(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev));
+  *supported = v;
+  return STRAGGLAR_OK;
+}
+
+int stragglar_nvls_begin(size_t bytes, int* fds, size_t* bytes_out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (!fds || !bytes_out || !bytes) return STRAGGLAR_ERR_INVALID_ARG;
+  if (c.nvls.stage) return STRAGGLAR_ERR_INVALID_ARG;          // one arena per communicator
+  DRV(cuMulticastGetGranularity);
+  DRV(cuMemGetAllocationGranularity);
+  DRV(cuMemCreate);
+  DRV(cuMemExportToShareableHandle);
+  DRV(cuMulticastCreate);
+  if (!p_cuMulticastGetGranularity || !p_cuMemCreate || !p_cuMulticastCreate) return STRAGGLAR_ERR_UNSUPPORTED;
+  auto& n = c.nvls;
+  CUmulticastObjectProp mp = {};
+  mp.numDevices = (unsigned)c.world;
+  mp.size = bytes;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t g_mc = 0, g_mem = 0;
+  DCK(p_cuMulticastGetGranularity(&g_mc, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  CUmemAllocationProp ap = {};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = c.device;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  DCK(p_cuMemGetAllocationGranularity(&g_mem, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  const size_t g = g_mc > g_mem ? g_mc : g_mem;
+  n.bytes = (bytes + g - 1) / g * g;
+  mp.size = n.bytes;
+  CUmemGenericAllocationHandle h = 0;
+  n.stage = 1;
+  auto fail = [&](int st) {
+    nvls_release(c);
+    return st;
+  };
+  if (p_cuMemCreate(&h, n.bytes, &ap, 0) != CUDA_SUCCESS) return fail(STRAGGLAR_ERR_CUDA);
+  n.mem = h;
+  int st = map_va(n.bytes, h, c.device, &n.va);
+  if (st) return fail(st);
+  if (p_cuMemExportToShareableHandle(&n.fds[2], h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) != CUDA_SUCCESS)
+    return fail(STRAGGLAR_ERR_CUDA);
+  if (c.rank == 0) {   // the all-rank multicast object
+    CUmemGenericAllocationHandle m = 0;
+    if (p_cuMulticastCreate(&m, &mp) != CUDA_SUCCESS) return fail(STRAGGLAR_ERR_CUDA);
+    n.mc_all = m;
+    if (p_cuMemExportToShareableHandle(&n.fds[0], m, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) != CUDA_SUCCESS)
+      return fail(STRAGGLAR_ERR_CUDA);
+  }
+  if (c.rank == lowest_ns(c)) {   // the non-stragglers' multicast object
+    CUmulticastObjectProp mq = mp;
+    mq.numDevices = (unsigned)(c.world - 1);
+    CUmemGenericAllocationHandle m = 0;
+    if (p_cuMulticastCreate(&m, &mq) != CUDA_SUCCESS) return fail(STRAGGLAR_ERR_CUDA);
+    n.mc_ns = m;
+    if (p_cuMemExportToShareableHandle(&n.fds[1], m, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) != CUDA_SUCCESS)
+      return fail(STRAGGLAR_ERR_CUDA);
+  }
+  for (int i = 0; i < 3; ++i) fds[i] = n.fds[i];
+  *bytes_out = n.bytes;
+  return STRAGGLAR_OK;
+}
+
+int stragglar_nvls_finish(int mc_all_fd, int mc_ns_fd, int sigma_mem_fd, void** arena) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  auto& n = c.nvls;
+  if (!c.active || n.stage != 1) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (!arena) return STRAGGLAR_ERR_INVALID_ARG;
+  DRV(cuMemImportFromShareableHandle);
+  DRV(cuMulticastAddDevice);
+  DRV(cuMulticastBindMem);
+  DRV(cuDeviceGet);
+  if (!p_cuMemImportFromShareableHandle || !p_cuMulticastAddDevice || !p_cuMulticastBindMem || !p_cuDeviceGet)
+    return STRAGGLAR_ERR_UNSUPPORTED;
+  auto fail = [&](int st) {
+    nvls_release(c);
+    return st;
+  };
+  CUdevice dev;
+  if (p_cuDeviceGet(&dev, c.device) != CUDA_SUCCESS) return fail(STRAGGLAR_ERR_CUDA);
+  auto import = [&](int fd, unsigned long long* h) {
+    CUmemGenericAllocationHandle x = 0;
+    if (fd < 0) return STRAGGLAR_ERR_INVALID_ARG;
+    if (p_cuMemImportFromShareableHandle(&x, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) !=
+        CUDA_SUCCESS)
+      return STRAGGLAR_ERR_CUDA;
+    *h = x;
+    return STRAGGLAR_OK;
+  };
+  int st;
+  if (!n.mc_all && (st = import(mc_all_fd, &n.mc_all))) return fail(st);
+  const bool ns = c.rank != c.sigma;
+  if (ns && !n.mc_ns && (st = import(mc_ns_fd, &n.mc_ns))) return fail(st);
+  // every member joins before any binds (a bind waits for the whole team)
+  if (p_cuMulticastAddDevice((CUmemGenericAllocationHandle)n.mc_all, dev) != CUDA_SUCCESS) return fail(STRAGGLAR_ERR_CUDA);
+  if (ns && p_cuMulticastAddDevice((CUmemGenericAllocationHandle)n.mc_ns, dev) != CUDA_SUCCESS)
+    return fail(STRAGGLAR_ERR_CUDA);
+  if (p_cuMulticastBindMem((CUmemGenericAllocationHandle)n.mc_all, 0, (CUmemGenericAllocationHandle)n.mem, 0, n.bytes,
+                           0) != CUDA_SUCCESS)
+    return fail(STRAGGLAR_ERR_CUDA);
+  if (ns && p_cuMulticastBindMem((CUmemGenericAllocationHandle)n.mc_ns, 0, (CUmemGenericAllocationHandle)n.mem, 0,
+                                 n.bytes, 0) != CUDA_SUCCESS)
+    return fail(STRAGGLAR_ERR_CUDA);
+  if ((st = map_va(n.bytes, (CUmemGenericAllocationHandle)n.mc_all, c.device, &n.mc_all_va))) return fail(st);
+  if (ns) {
+    if ((st = map_va(n.bytes, (CUmemGenericAllocationHandle)n.mc_ns, c.device, &n.mc_ns_va))) return fail(st);
+    // owners read the straggler's input through a unicast peer mapping of its arena
+    if ((st = import(sigma_mem_fd, &n.sigma_mem))) return fail(st);
+    if ((st = map_va(n.bytes, (CUmemGenericAllocationHandle)n.sigma_mem, c.device, &n.sigma_va))) return fail(st);
+  }
+  n.stage = 2;
+  *arena = (void*)n.va;
+  return STRAGGLAR_OK;
+}
+
+int stragglar_allreduce_nvls(void* buf, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  auto& n = c.nvls;
+  if (!c.active || !c.imported || n.stage != 2) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  int st = check_args(buf, count, dtype, op);
+  if (st || count == 0) return st;
+  const int es = esize_of(dtype);
+  if (count % (16 / es)) return STRAGGLAR_ERR_INVALID_ARG;             // whole 16-byte vectors only
+  const char* lo = (const char*)n.va;
+  if ((const char*)buf < lo || (const char*)buf + count * es > lo + n.bytes) return STRAGGLAR_ERR_NOT_REGISTERED;
+  if (sticky_error(c)) return STRAGGLAR_ERR_TIMEOUT;
+  const size_t off = (const char*)buf - lo;
+  LaunchPlan P = base_plan(c, count, dtype, true);
+  P.nlocal = 1;
+  P.local_rank[0] = c.rank;
+  P.sub = 1;
+  P.G = c.G;                                   // one slice per CTA
+  {
+    const uint64_t chunk_bytes = P.ce * P.esize, per = c.slice_bytes ? c.slice_bytes : 16384;
+    uint64_t g = (chunk_bytes + per - 1) / per;
+    if (g < 1) g = 1;
+    if (g < (uint64_t)P.G) P.G = (int)g;
+  }
+  P.buf[c.rank] = (char*)buf;
+  P.mc_all = (char*)n.mc_all_va + off;
+  P.mc_ns = n.mc_ns_va ? (char*)n.mc_ns_va + off : nullptr;
+  P.sigma_uc = n.sigma_va ? (char*)n.sigma_va + off : nullptr;
+  if (launch_nvls(dtype, P, P.G, (cudaStream_t)stream) != cudaSuccess) return STRAGGLAR_ERR_CUDA;
+  g_launches.fetch_add(1);
+  return STRAGGLAR_OK;
+}
+
+int stragglar_nvls_selftest(int dtype, size_t count, const void* host_in, void* host_out) {
+  // a one-member multicast object on the current device: out = ld_reduce(in) through it
+  const int es = esize_of(dtype);
+  if (!es || !host_in || !host_out || !count || count % (16 / es)) return STRAGGLAR_ERR_INVALID_ARG;
+  int sup = 0;
+  int st = stragglar_nvls_supported(&sup);
+  if (st) return st;
+  if (!sup) return STRAGGLAR_ERR_UNSUPPORTED;
+  DRV(cuMulticastGetGranularity);
+  DRV(cuMemGetAllocationGranularity);
+  DRV(cuMemCreate);
+  DRV(cuMulticastCreate);
+  DRV(cuMulticastAddDevice);
+  DRV(cuMulticastBindMem);
+  DRV(cuMemRelease);
+  DRV(cuDeviceGet);
+  int devi = 0;
+  CK(cudaGetDevice(&devi));
+  CUdevice dev;
+  DCK(p_cuDeviceGet(&dev, devi));
+  const size_t bytes = count * es;
+  CUmulticastObjectProp mp = {};
+  mp.numDevices = 1;
+  mp.size = 2 * bytes;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_NONE;
+  size_t g_mc = 0, g_mem = 0;
+  DCK(p_cuMulticastGetGranularity(&g_mc, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+  CUmemAllocationProp ap = {};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = devi;
+  DCK(p_cuMemGetAllocationGranularity(&g_mem, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+  const size_t g = g_mc > g_mem ? g_mc : g_mem;
+  const size_t size = (2 * bytes + g - 1) / g * g;
+  mp.size = size;
+  CUmemGenericAllocationHandle mem = 0, mc = 0;
+  unsigned long long va = 0, mcva = 0;
+  st = STRAGGLAR_ERR_CUDA;
+  if (p_cuMemCreate(&mem, size, &ap, 0) == CUDA_SUCCESS && p_cuMulticastCreate(&mc, &mp) == CUDA_SUCCESS &&
+      p_cuMulticastAddDevice(mc, dev) == CUDA_SUCCESS && p_cuMulticastBindMem(mc, 0, mem, 0, size, 0) == CUDA_SUCCESS &&
+      map_va(size, mem, devi, &va) == STRAGGLAR_OK && map_va(size, mc, devi, &mcva) == STRAGGLAR_OK &&
+      cudaMemcpy((void*)va, host_in, bytes, cudaMemcpyHostToDevice) == cudaSuccess &&
+      cudaMemset((char*)va + bytes, 0, bytes) == cudaSuccess &&
+      launch_nvls_selftest(dtype, (char*)mcva, bytes, 0) == cudaSuccess &&
+      cudaDeviceSynchronize() == cudaSuccess &&
+      cudaMemcpy(host_out, (char*)va + bytes, bytes, cudaMemcpyDeviceToHost) == cudaSuccess)
+    st = STRAGGLAR_OK;
+  unmap_va(mcva, size);
+  unmap_va(va, size);
+  if (mc) p_cuMemRelease(mc);
+  if (mem) p_cuMemRelease(mem);
+  return st;
 }
 
 // ---------------------------------------------------------------- team

@@ -100,6 +100,9 @@ struct LaunchPlan {
   int bc_partner;            // Broadcast baseline: the straggler's exchange partner (physical)
   int bc_sender[kMaxWorld];  //   per physical rank: who copies the full sum to it (-1: a holder)
   int bc_round[kMaxWorld];   //   and in which round
+  char* mc_all;              // NVLS (nvls.cu): multicast mapping of every rank's arena (+ call offset)
+  char* mc_ns;               //   the non-stragglers' multicast mapping (+ call offset)
+  char* sigma_uc;            //   the straggler's arena, unicast peer mapping (+ call offset)
   int nops[kMaxWorld];       // by physical rank
   Op ops[kMaxWorld][kMaxOps];// by physical rank
 };

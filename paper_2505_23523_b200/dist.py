@@ -6,7 +6,11 @@ libstragglar.so exports; the collective itself never goes through it.
 """
 from __future__ import annotations
 
-from typing import List, Optional
+import json
+import os
+import secrets
+import socket
+from typing import Dict, List, Optional
 
 import torch.distributed as dist
 
@@ -19,6 +23,42 @@ def all_gather_bytes(blob: bytes, group=None) -> bytes:
     if any(b is None or len(b) != len(blob) for b in out):
         raise RuntimeError("handle blobs of unequal size")
     return b"".join(out)  # type: ignore[arg-type]
+
+
+def exchange_fds(fds: Dict[str, int], group=None) -> Dict[int, Dict[str, int]]:
+    """Send this rank's labelled file descriptors (values < 0 are skipped) to
+    every other rank of the node over abstract UNIX-domain sockets
+    (SCM_RIGHTS); returns {peer rank: {label: received fd}}.  The caller owns
+    (and closes) the received fds.  NVLS multicast objects and VMM arenas are
+    shared this way: their POSIX handles are file descriptors, which a
+    torch.distributed collective cannot carry."""
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    tok = [secrets.token_hex(8) if rank == 0 else None]
+    dist.broadcast_object_list(tok, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    name = lambda r: f"\0stragglar-{tok[0]}-{r}"  # noqa: E731  (abstract namespace: no file to clean up)
+    srv = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+    srv.bind(name(rank))
+    srv.listen(world)
+    dist.barrier(group)
+    labels = [k for k, v in fds.items() if v is not None and v >= 0]
+    payload = json.dumps({"from": rank, "labels": labels}).encode()
+    for p in range(world):
+        if p == rank:
+            continue
+        cl = socket.socket(socket.AF_UNIX, socket.SOCK_STREAM)
+        cl.connect(name(p))
+        socket.send_fds(cl, [payload], [fds[k] for k in labels])
+        cl.close()
+    got: Dict[int, Dict[str, int]] = {}
+    for _ in range(world - 1):
+        conn, _ = srv.accept()
+        msg, rfds, _, _ = socket.recv_fds(conn, 4096, 16)
+        info = json.loads(msg.decode())
+        got[info["from"]] = dict(zip(info["labels"], rfds))
+        conn.close()
+    srv.close()
+    dist.barrier(group)
+    return got
 
 
 class ProcessComm:
@@ -69,5 +109,28 @@ class ProcessComm:
     def allreduce_bcast(self, tensor, stream=None) -> None:
         self.lib.stragglar_allreduce_bcast(tensor, stream)
 
+    def nvls_setup(self, nbytes: int):
+        """NEXT N1(i): allocate and bind this rank's NVLS arena (collective).
+        Returns a uint8 CUDA tensor aliasing the arena; stragglar_allreduce_nvls
+        reduces views of it in place."""
+        fds, size = self.lib.stragglar_nvls_begin(nbytes)
+        got = exchange_fds({"mc_all": fds[0], "mc_ns": fds[1], "mem": fds[2]}, self.group)
+        lowest_ns = 1 if self.straggler == 0 else 0
+        mc_all = fds[0] if self.rank == 0 else got[0]["mc_all"]
+        mc_ns = fds[1] if self.rank == lowest_ns else got.get(lowest_ns, {}).get("mc_ns", -1)
+        sig_mem = got[self.straggler]["mem"] if self.rank != self.straggler else -1
+        try:
+            ptr = self.lib.stragglar_nvls_finish(mc_all, mc_ns, sig_mem)
+        finally:
+            for peer in got.values():          # the library imported what it needs
+                for fd in peer.values():
+                    os.close(fd)
+        self.arena = self.lib.device_bytes(ptr, size)
+        return self.arena
+
+    def allreduce_nvls(self, tensor, stream=None) -> None:
+        self.lib.stragglar_allreduce_nvls(tensor, stream)
+
     def close(self) -> None:
+        self.arena = None
         self.lib.stragglar_finalize()

@@ -58,6 +58,11 @@ _SIGS = {
     "stragglar_probe_copy": ([_vp, _c_size, _c_int, ctypes.c_uint32, _c_int, _vp], _c_int),
     "stragglar_probe_pingpong": ([_c_int, _c_int, _vp], _c_int),
     "stragglar_probe_pingpong_result": ([ctypes.POINTER(ctypes.c_double)], _c_int),
+    "stragglar_nvls_supported": ([ctypes.POINTER(_c_int)], _c_int),
+    "stragglar_nvls_begin": ([_c_size, ctypes.POINTER(_c_int), ctypes.POINTER(_c_size)], _c_int),
+    "stragglar_nvls_finish": ([_c_int, _c_int, _c_int, ctypes.POINTER(_vp)], _c_int),
+    "stragglar_allreduce_nvls": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
+    "stragglar_nvls_selftest": ([_c_int, _c_size, _vp, _vp], _c_int),
     "stragglar_allreduce": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_allreduce_ring": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_allreduce_direct": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
@@ -366,6 +371,59 @@ def stragglar_phase_times():
     a, t = ctypes.c_double(0), ctypes.c_double(0)
     _ck("stragglar_phase_times", _lib.stragglar_phase_times(ctypes.byref(a), ctypes.byref(t)))
     return a.value, t.value
+
+
+# ---------------------------------------------------------------- NEXT N1(i): NVLS multicast
+def stragglar_nvls_supported() -> bool:
+    v = _c_int(0)
+    _ck("stragglar_nvls_supported", _lib.stragglar_nvls_supported(ctypes.byref(v)))
+    return bool(v.value)
+
+
+def stragglar_nvls_begin(nbytes: int):
+    """-> ([mc_all_fd, mc_ns_fd, arena_fd] (-1 where this rank exports none), rounded arena bytes)."""
+    fds, out = (_c_int * 3)(), _c_size(0)
+    _ck("stragglar_nvls_begin", _lib.stragglar_nvls_begin(int(nbytes), fds, ctypes.byref(out)))
+    return list(fds), out.value
+
+
+def stragglar_nvls_finish(mc_all_fd: int, mc_ns_fd: int, sigma_mem_fd: int) -> int:
+    """-> the arena's device pointer."""
+    p = _vp(0)
+    _ck("stragglar_nvls_finish", _lib.stragglar_nvls_finish(int(mc_all_fd), int(mc_ns_fd), int(sigma_mem_fd),
+                                                            ctypes.byref(p)))
+    return int(p.value)
+
+
+def stragglar_allreduce_nvls(t, stream=None) -> None:
+    ptr, n, dt = _dev_args(t)
+    _ck("stragglar_allreduce_nvls", _lib.stragglar_allreduce_nvls(ptr, n, dt, SUM, _stream_ptr(stream)))
+
+
+def stragglar_nvls_selftest(host_in) -> "object":
+    """host_in: contiguous CPU tensor; returns its reducing load through a one-member multicast object."""
+    import torch
+
+    if host_in.is_cuda or not host_in.is_contiguous():
+        raise ValueError("host tensor expected")
+    out = torch.empty_like(host_in)
+    _ck("stragglar_nvls_selftest", _lib.stragglar_nvls_selftest(_dtype_code(host_in), host_in.numel(),
+                                                                host_in.data_ptr(), out.data_ptr()))
+    return out
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ view of library memory (torch.as_tensor wraps it without a copy)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 2}
+
+
+def device_bytes(ptr: int, nbytes: int):
+    """A uint8 torch tensor aliasing nbytes of library device memory at ptr."""
+    import torch
+
+    return torch.as_tensor(_DeviceArray(ptr, nbytes), device="cuda")
 
 
 def stragglar_finalize() -> None:

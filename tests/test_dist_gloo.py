@@ -136,3 +136,46 @@ def test_ddp_staging_grows_at_the_same_bucket_everywhere():
     assert seqs[0] == seqs[1] == seqs[2]
     assert len(seqs[0]) == 3                     # grew at buckets 0, 2 and 5 only
     assert seqs[0][0] >= 1000 and seqs[0][1] >= 5000 and seqs[0][2] >= 9000
+
+
+def _fd_worker(rank, world, port, q):
+    import tempfile
+
+    import torch.distributed as dist
+
+    from paper_2505_23523_b200.dist import exchange_fds
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    f = tempfile.TemporaryFile()
+    f.write(f"rank{rank}".encode())
+    f.flush()
+    mine = {"file": f.fileno(), "none": -1} if rank != 1 else {"none": -1}
+    got = exchange_fds(mine)
+    seen = {}
+    for peer, fds in sorted(got.items()):
+        for label, fd in fds.items():
+            seen[(peer, label)] = os.pread(fd, 16, 0).decode()   # the offset is shared by every copy
+            os.close(fd)
+    dist.destroy_process_group()
+    q.put((rank, seen))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fd_exchange_over_unix_sockets(world):
+    """The NVLS setup's descriptor exchange (SCM_RIGHTS over abstract UNIX
+    sockets): every rank receives every other rank's labelled fds — here
+    temporary files — and can read through them; -1 entries are not sent."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_fd_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=30)
+    for r in range(world):
+        want = {(p, "file"): f"rank{p}" for p in range(world) if p not in (r, 1)}
+        assert out[r] == want
