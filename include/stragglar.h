@@ -268,7 +268,9 @@ int stragglar_finalize(void);
  * elements (INVALID_ARG otherwise), NOT_REGISTERED outside the arena.
  * stragglar_nvls_selftest: one-GPU check of the multicast path — a
  * one-member multicast object on the current device; host_out = the reducing
- * load of host_in through it (equal to host_in).  No communicator needed.
+ * load of host_in through it (equal to host_in).  No communicator needed;
+ * UNSUPPORTED when the driver creates no multicast object (a GPU without an
+ * NVSwitch fabric behind it, e.g. this run's one-GPU box).
  * MEASURED ONLY ON ONE GPU: the multi-GPU path needs >= 2 NVSwitch GPUs. */
 int stragglar_nvls_supported(int* supported);
 int stragglar_nvls_begin(size_t bytes, int* fds, size_t* bytes_out);

@@ -1283,8 +1283,15 @@ int stragglar_nvls_selftest(int dtype, size_t count, const void* host_in, void* 
   CUmemGenericAllocationHandle mem = 0, mc = 0;
   unsigned long long va = 0, mcva = 0;
   st = STRAGGLAR_ERR_CUDA;
-  if (p_cuMemCreate(&mem, size, &ap, 0) == CUDA_SUCCESS && p_cuMulticastCreate(&mc, &mp) == CUDA_SUCCESS &&
-      p_cuMulticastAddDevice(mc, dev) == CUDA_SUCCESS && p_cuMulticastBindMem(mc, 0, mem, 0, size, 0) == CUDA_SUCCESS &&
+  if (p_cuMemCreate(&mem, size, &ap, 0) != CUDA_SUCCESS) return STRAGGLAR_ERR_CUDA;
+  // A GPU can report multicast support and still have no usable multicast
+  // object (no NVSwitch fabric behind it: this one-GPU box answers
+  // CUDA_ERROR_INVALID_VALUE for any member count): that is UNSUPPORTED here.
+  if (p_cuMulticastCreate(&mc, &mp) != CUDA_SUCCESS) {
+    p_cuMemRelease(mem);
+    return STRAGGLAR_ERR_UNSUPPORTED;
+  }
+  if (p_cuMulticastAddDevice(mc, dev) == CUDA_SUCCESS && p_cuMulticastBindMem(mc, 0, mem, 0, size, 0) == CUDA_SUCCESS &&
       map_va(size, mem, devi, &va) == STRAGGLAR_OK && map_va(size, mc, devi, &mcva) == STRAGGLAR_OK &&
       cudaMemcpy((void*)va, host_in, bytes, cudaMemcpyHostToDevice) == cudaSuccess &&
       cudaMemset((char*)va + bytes, 0, bytes) == cudaSuccess &&

@@ -69,10 +69,20 @@ __device__ __forceinline__ bool cta_wait(const uint32_t* f, uint32_t epoch, cons
   return __syncthreads_and(ok);
 }
 
-// Whole-CTA signal: all prior stores of the CTA happen-before the flag store.
+// Whole-CTA signal: all prior stores of the CTA happen-before the flag store
+// (the barrier orders every thread's stores — thread 0's completed bulk stores
+// included — before the signalling thread's release fence, which is cumulative).
+// The release is issued by a thread of warp 1, not by thread 0, which issues
+// the TMA copies: the fence (a MEMBAR that waits ~0.45 us at GPU scope, ~1 us
+// at system scope after the data is stored; profiles/r02/ab/r02b_fence_probe.jsonl)
+// then overlaps thread 0's poll of the next op's flag instead of preceding it.
+#ifndef STRAGGLAR_SIGNAL_TID
+#define STRAGGLAR_SIGNAL_TID 32
+#endif
+constexpr int kSignalThread = STRAGGLAR_SIGNAL_TID;
 __device__ __forceinline__ void cta_signal(uint32_t* f, uint32_t epoch, bool sys) {
   __syncthreads();
-  if (threadIdx.x == 0) st_release(f, epoch, sys);
+  if (threadIdx.x == kSignalThread) st_release(f, epoch, sys);
 }
 
 // The call's epoch lives in device memory (state->epoch + 1), so a captured
@@ -106,6 +116,15 @@ __device__ __forceinline__ void finish_call(const LaunchPlan& P) {
 // then land in the same slot as in this call, never in another slot's range.
 __device__ __forceinline__ uint32_t* flag_at(uint32_t* base, int slot, int stride, int s) {
   return base + (size_t)slot * stride + s;
+}
+
+// Whole-CTA wait for `n` consecutive flags of one slot (one waiting thread each).
+__device__ __forceinline__ bool cta_wait_range(uint32_t* base, int slot, int first, int n, uint32_t epoch,
+                                               const LaunchPlan& P, uint32_t where, bool local = false) {
+  int ok = 1;
+  if ((int)threadIdx.x < n)
+    ok = spin_wait(flag_at(base, slot, P.fstride, first + threadIdx.x), epoch, P, where, local ? false : P.sys_scope != 0);
+  return __syncthreads_and(ok);
 }
 
 // ---------------------------------------------------------------- ranges
@@ -532,17 +551,24 @@ __device__ void rs_slice(const LaunchPlan& P, const char* const (&src)[W - 1], c
 // Phase A body for non-straggler `me`, CTA slot s (slices s*sub .. s*sub+sub-1).
 // BC (Broadcast baseline): the partial is announced to every other
 // non-straggler (they copy it in ag_body) instead of to the straggler.
+// With op lanes (fused call, small messages: LaunchPlan::lanes = L > 1, one
+// slice per CTA) Phase A is split over the lanes too: CTA (s, q) reduces
+// mini-slice m = s*L + q of the G*L equal parts of the chunk (slice s is
+// exactly the union of minis s*L .. s*L+L-1) and flags it on its own, so the
+// exchange of slice s waits for L flags.
 template <int DT, int W, int MV, bool BC = false>
-__device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t ep) {
-  const int NV = P.G * P.sub;   // slices per chunk (flag stride)
+__device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int me, uint32_t ep) {
+  const int L = P.lanes;
+  const int m = s * L + q;           // this CTA's Phase-A slot
+  const int NV = P.G * L * P.sub;    // Phase-A slices per chunk (flag stride)
   if (blockIdx.x == 0 && threadIdx.x == 0) P.state->t_rs_start = globaltimer();
   // barrier (1) among the non-stragglers, per CTA slot
   if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
-    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, P.fstride, s), ep, P.sys_scope);
+    st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, P.fstride, m), ep, P.sys_scope);
   // one waiting thread per peer: the acquire loads overlap instead of queueing
   int ok = 1;
   if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
-    ok = spin_wait(flag_at(P.flags[me], SLOT_ARRIVE + threadIdx.x, P.fstride, s), ep, P, 0x100 | threadIdx.x);
+    ok = spin_wait(flag_at(P.flags[me], SLOT_ARRIVE + threadIdx.x, P.fstride, m), ep, P, 0x100 | threadIdx.x);
   if (!__syncthreads_and(ok)) return;
 
   const int g = P.logical_of_phys[me];  // owned chunk
@@ -552,7 +578,7 @@ __device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t
 #pragma unroll
   for (int j = 0; j < W - 1; ++j) src[j] = P.buf[j < P.sigma ? j : j + 1];
   for (int j = 0; j < P.sub; ++j) {
-    const int v = s * P.sub + j;
+    const int v = m * P.sub + j;
     const Range r = slice_of(c.lo, c.hi, v, NV, 16 / P.esize);
     // with two ranks the owner's chunk already is the non-straggler "sum"
     if constexpr (W > 2) {
@@ -573,7 +599,8 @@ __device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint32_t
       // "partial ready" for the straggler's half of the exchange
       cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, P.fstride, v), ep, P.sys_scope);
       // and for this rank's own exchange when another op lane runs it
-      if (P.lanes > 1 && threadIdx.x == 0) st_release(flag_at(P.flags[me], SLOT_RS_LOCAL, P.fstride, v), ep, false);
+      if (P.lanes > 1 && threadIdx.x == kSignalThread)
+        st_release(flag_at(P.flags[me], SLOT_RS_LOCAL, P.fstride, v), ep, false);
     }
   }
 }
@@ -711,8 +738,9 @@ __device__ void bcast_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint3
 // only the round barrier is replaced by the data dependencies: the straggler's
 // n-1 exchanges (independent of each other) no longer queue behind one CTA.
 // Lanes hand off through local flags: an exchange's own half (SLOT_SELF, for a
-// later send of that chunk on another lane) and, in the fused call, lane 0's
-// Phase-A partial (SLOT_RS_LOCAL, for the exchange).
+// later send of that chunk on another lane) and, in the fused call, the
+// lanes' parts of the Phase-A partial (SLOT_RS_LOCAL, for the exchange; see
+// rs_body).
 template <int DT, int W, int MV, bool FUSED>
 __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int me, uint32_t ep) {
   const int NV = P.G * P.sub;   // slices per chunk (flag stride)
@@ -747,7 +775,9 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
       const uint64_t mid = sl.lo + (nvec_total / 2) * V < sl.hi ? sl.lo + (nvec_total / 2) * V : sl.hi;
       if (op.kind == OP_EXCH_LOW) {
         // non-straggler r: [lo, mid) of c_r = partial_r (+) x_sigma, stored at both ends
-        if (FUSED && q != 0 && !(ok = cta_wait(flag_at(P.flags[me], SLOT_RS_LOCAL, P.fstride, v), ep, P, 0x210 | k, true)))
+        // (fused call with lanes: Phase A of this slice was split over the L lanes)
+        if (FUSED && lanes > 1 &&
+            !(ok = cta_wait_range(P.flags[me], SLOT_RS_LOCAL, s * lanes, lanes, ep, P, 0x210 | k, true)))
           break;
         if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, P.fstride, s), ep, P, 0x200 | k))) break;
         if (tr) tr[1] = globaltimer();
@@ -760,7 +790,11 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
                       (int)((b - a) % 16) / P.esize, P.esize);
       } else if (op.kind == OP_EXCH_HIGH) {
         // straggler: [mid, hi) of c_r; waits for rank r's Phase-A partial
-        if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, P.fstride, v), ep, P, 0x300 | k))) break;
+        if (FUSED && lanes > 1) {
+          if (!(ok = cta_wait_range(P.flags[me], SLOT_RSDONE + c, s * lanes, lanes, ep, P, 0x300 | k))) break;
+        } else if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, P.fstride, v), ep, P, 0x300 | k))) {
+          break;
+        }
         if (tr) tr[1] = globaltimer();
         const uint64_t a = mid * P.esize, b = sl.hi * P.esize, body = (b - a) / 16 * 16;
         if constexpr (tma)
@@ -787,7 +821,7 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
         copy_tail(P.buf[peer] + a + body, mine + a + body, (int)((b - a) % 16));
       }
       cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, P.fstride, v), ep, P.sys_scope);
-      if (lanes > 1 && op.kind != OP_SEND && threadIdx.x == 0)
+      if (lanes > 1 && op.kind != OP_SEND && threadIdx.x == kSignalThread)
         st_release(flag_at(P.flags[me], SLOT_SELF + c, P.fstride, v), ep, false);
       if (tr) tr[2] = globaltimer();
     }
@@ -891,14 +925,14 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_con
     __syncthreads();
   }
   if constexpr (KIND == 0 || KIND == 4 || KIND == 5)
-    if (me != P.sigma && q == 0) rs_body<DT, W, MV>(P, pipe, s, me, ep);
+    if (me != P.sigma) rs_body<DT, W, MV>(P, pipe, s, q, me, ep);
   if (stamps && threadIdx.x == 0)
     atomicMax(reinterpret_cast<unsigned long long*>(&stamp[1]), (unsigned long long)globaltimer());
   if constexpr (KIND == 1 || KIND == 4) complete_body<DT, W, MV, KIND == 4>(P, pipe, s, q, me, ep);
   if constexpr (KIND == 3 || KIND == 5) direct_body<DT, W, MV>(P, pipe, s, me, ep);
   if constexpr (KIND == 6 || KIND == 8)
     if (me != P.sigma) {
-      rs_body<DT, W, MV, true>(P, pipe, s, me, ep);
+      rs_body<DT, W, MV, true>(P, pipe, s, 0, me, ep);
       ag_body<DT, W, MV>(P, pipe, s, me, ep);
     }
   if constexpr (KIND == 7 || KIND == 8) bcast_body<DT, W, MV>(P, pipe, s, me, ep);

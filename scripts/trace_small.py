@@ -13,11 +13,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2505_23523_b200 import stragglar as S  # noqa: E402
 
-n, sigma = 8, 0
+n, sigma = int(os.environ.get("N", "8")), int(os.environ.get("SIGMA", "0"))
 count = int(os.environ.get("COUNT", "4096"))
+dt = {"float32": torch.float32, "bfloat16": torch.bfloat16}[os.environ.get("DTYPE", "float32")]
 torch.cuda.set_device(0)
 S.stragglar_team_init(n, sigma)
-bufs = [torch.randn(count, device="cuda") for _ in range(n)]
+bufs = [torch.randn(count, device="cuda").to(dt) for _ in range(n)]
 for _ in range(5):
     S.stragglar_team_allreduce(bufs)
 S.stragglar_team_set_trace(True)
@@ -35,7 +36,7 @@ for rep in range(5):
         for k in range(16):
             w, d, e = tr[((p * NS + 0) * 16 + k) * 3:((p * NS + 0) * 16 + k) * 3 + 3]
             if w and d and e:
-                ops.append({"k": k, "start": w - t0, "wait": d - w, "move": e - d})
+                ops.append({"k": k, "start": w - t0, "wait": d - w, "move": e - d, "end": e - t0})
         rows[f"phys{p}"] = ops
     out.append({"rep": rep, "slices": NS, "end_ns": max(v for v in tr if v) - t0, "ranks": rows})
 S.stragglar_team_set_trace(False)

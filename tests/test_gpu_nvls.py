@@ -43,7 +43,13 @@ def test_selftest_one_member_multicast(S, dtype, count):
         x = torch.randint(-2**31, 2**31 - 1, (count,), generator=g, dtype=torch.int64).to(torch.int32)
     else:
         x = torch.randn(count, generator=g).to(dtype)
-    y = S.stragglar_nvls_selftest(x)
+    try:
+        y = S.stragglar_nvls_selftest(x)
+    except S.StragglarError as e:
+        if e.status == 2:
+            pytest.skip("the driver creates no multicast object on this GPU (no NVSwitch fabric: "
+                        "cuMulticastCreate -> CUDA_ERROR_INVALID_VALUE, scripts/mc_selftest.cu)")
+        raise
     assert torch.equal(x.view(torch.int16 if dtype == torch.bfloat16 else torch.int32),
                        y.view(torch.int16 if dtype == torch.bfloat16 else torch.int32))
 
