@@ -624,6 +624,7 @@ def bench_multi(args):
     k0["pingpong_iters"] = iters
     k0["alpha_us"] = round(pp / (2 * iters), 3)           # one flag hop, system scope
     comm.deregister(kbuf)
+    dist.barrier()                 # every rank unmapped the peers' probe buffers before any frees its own
     del kbuf
     nvlink_pair = k0["pair_bidir_push_tma_gbs"]
     nvlink_ingress = max(k0["all_peers_pull_tma_gbs"], k0["all_peers_pull_lsu_gbs"])

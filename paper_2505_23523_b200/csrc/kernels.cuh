@@ -71,42 +71,58 @@ __device__ __forceinline__ bool cta_wait(const uint32_t* f, uint32_t epoch, cons
 
 // Whole-CTA signal: all prior stores of the CTA happen-before the flag store
 // (the barrier orders every thread's stores — thread 0's completed bulk stores
-// included — before the signalling thread's release fence, which is cumulative).
-// The release is issued by a thread of warp 1, not by thread 0, which issues
-// the TMA copies: the fence (a MEMBAR that waits ~0.45 us at GPU scope, ~1 us
-// at system scope after the data is stored; profiles/r02/ab/r02b_fence_probe.jsonl)
-// then overlaps thread 0's poll of the next op's flag instead of preceding it.
-#ifndef STRAGGLAR_SIGNAL_TID
-#define STRAGGLAR_SIGNAL_TID 32
-#endif
-constexpr int kSignalThread = STRAGGLAR_SIGNAL_TID;
+// included — before the release fence, which is cumulative).  Issuing the
+// release from a thread of warp 1, so that it overlaps thread 0's poll of the
+// next flag, measured no different (profiles/r02/ab/r02g_sig*); thread 0 it is.
+constexpr int kSignalThread = 0;
 __device__ __forceinline__ void cta_signal(uint32_t* f, uint32_t epoch, bool sys) {
   __syncthreads();
   if (threadIdx.x == kSignalThread) st_release(f, epoch, sys);
 }
 
 // The call's epoch lives in device memory (state->epoch + 1), so a captured
-// CUDA graph replays correctly: the last CTA to leave the call's final kernel
-// increments it, after every CTA of every kernel of the call has read it.
+// CUDA graph replays correctly.  It is incremented once every CTA of the
+// call's final kernel has read it: by default counted at kernel START (thread
+// 0 of each CTA, after its acquire read of the epoch; the last to arrive bumps
+// it and re-arms the next call's phase stamps), which keeps the same-address
+// atomics off the call's tail; STRAGGLAR_EPOCH_AT_START=0 counts CTAs at exit.
+// Every thread of the CTA must call call_epoch (it has a CTA barrier).
+#ifndef STRAGGLAR_EPOCH_AT_START
+#define STRAGGLAR_EPOCH_AT_START 1
+#endif
+__device__ __forceinline__ void bump_epoch(const LaunchPlan& P, uint32_t e) {
+  P.state->exit_count = 0;
+  uint64_t* nx = P.state->stamp[(e + 1u) & 1u];   // re-arm for the next call
+  nx[0] = ~0ull;
+  nx[1] = 0;
+  nx[2] = 0;
+  __threadfence();
+  atomicAdd(&P.state->epoch, 1u);
+}
 __device__ __forceinline__ uint32_t call_epoch(const LaunchPlan& P) {
+#if STRAGGLAR_EPOCH_AT_START
+  __shared__ uint32_t s_ep;
+  if (threadIdx.x == 0) {
+    const uint32_t e = ld_acquire_gpu(&P.state->epoch) + 1u;
+    s_ep = e;
+    if (P.last_kernel && atomicAdd(&P.state->exit_count, 1u) == gridDim.x - 1) bump_epoch(P, e);
+  }
+  __syncthreads();
+  return s_ep;
+#else
   return *(volatile const uint32_t*)&P.state->epoch + 1u;
+#endif
 }
 __device__ __forceinline__ void finish_call(const LaunchPlan& P) {
+#if STRAGGLAR_EPOCH_AT_START
+  return;
+#endif
   if (!P.last_kernel) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     const uint32_t prev = atomicAdd(&P.state->exit_count, 1u);
-    if (prev == gridDim.x - 1) {
-      P.state->exit_count = 0;
-      const uint32_t e = *(volatile uint32_t*)&P.state->epoch + 1u;   // this call
-      uint64_t* nx = P.state->stamp[(e + 1u) & 1u];                      // re-arm for the next call
-      nx[0] = ~0ull;
-      nx[1] = 0;
-      nx[2] = 0;
-      __threadfence();
-      atomicAdd(&P.state->epoch, 1u);
-    }
+    if (prev == gridDim.x - 1) bump_epoch(P, *(volatile uint32_t*)&P.state->epoch + 1u);
   }
 }
 
@@ -551,8 +567,9 @@ __device__ void rs_slice(const LaunchPlan& P, const char* const (&src)[W - 1], c
 // Phase A body for non-straggler `me`, CTA slot s (slices s*sub .. s*sub+sub-1).
 // BC (Broadcast baseline): the partial is announced to every other
 // non-straggler (they copy it in ag_body) instead of to the straggler.
-// With op lanes (fused call, small messages: LaunchPlan::lanes = L > 1, one
-// slice per CTA) Phase A is split over the lanes too: CTA (s, q) reduces
+// With op lanes (small messages: LaunchPlan::lanes = L > 1, one slice per
+// CTA; the split Phase-A kernel uses the same L) Phase A is split over the
+// lanes too: CTA (s, q) reduces
 // mini-slice m = s*L + q of the G*L equal parts of the chunk (slice s is
 // exactly the union of minis s*L .. s*L+L-1) and flags it on its own, so the
 // exchange of slice s waits for L flags.
@@ -790,7 +807,7 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
                       (int)((b - a) % 16) / P.esize, P.esize);
       } else if (op.kind == OP_EXCH_HIGH) {
         // straggler: [mid, hi) of c_r; waits for rank r's Phase-A partial
-        if (FUSED && lanes > 1) {
+        if (lanes > 1) {   // Phase A of the slice was split over the lanes (rs_body)
           if (!(ok = cta_wait_range(P.flags[me], SLOT_RSDONE + c, s * lanes, lanes, ep, P, 0x300 | k))) break;
         } else if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, P.fstride, v), ep, P, 0x300 | k))) {
           break;
