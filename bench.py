@@ -44,6 +44,7 @@ WORKLOADS = {
     "config4": (8, 0, "bfloat16", 13_107_200, "BASELINE configs[3]: n=8, straggler 0, 25 MiB bf16 DP bucket"),
     "config5": (8, 3, "bfloat16", 524_288, "BASELINE configs[4]: n=8, straggler 3, bf16 [64x8192] TP activation"),
     "config1": (4, 0, "float32", 1 << 20, "BASELINE configs[0]: n=4, straggler 0, 1M fp32"),
+    "config3_1GiB": (8, 0, "bfloat16", 1 << 29, "BASELINE configs[2] largest point: n=8, straggler 0, 1 GiB bf16"),
 }
 ESIZE = {"float32": 4, "int32": 4, "bfloat16": 2}
 
@@ -612,7 +613,7 @@ def bench_multi(args):
         k0[f"all_peers_push_{name}_gbs"] = round((world - 1) * pb / t / 1e9, 1)
         t = probe(True, mode | S.PROBE_PULL, others)
         k0[f"all_peers_pull_{name}_gbs"] = round((world - 1) * pb / t / 1e9, 1)
-    iters = 20 if shared else 2000
+    iters = 20 if (shared and not mps) else 2000     # time-sliced ranks: every hop waits for a time slice
     if rank in (0, 1):
         S.stragglar_barrier()
         S.stragglar_probe_pingpong(1 - rank, iters)
