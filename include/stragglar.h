@@ -91,6 +91,12 @@ const char* stragglar_status_string(int status);   /* static string, never NULL 
  * *n_transfers.  Supports power-of-two world in [2, 64]. */
 int stragglar_schedule_rounds(int world, int* rounds);
 int stragglar_schedule_round(int world, int round, int* out, int max_transfers, int* n_transfers);
+/* Host only: the layout a StragglAR call of `count` elements would use with
+ * `ctas_per_rank` CTAs per rank and the default knobs — slices per chunk
+ * (CTA slots), slices per CTA (sub) and Phase-B op lanes per slice (DESIGN.md
+ * §5).  sys_scope selects the per-process defaults (one slice per CTA). */
+int stragglar_plan_layout(int world, int straggler_rank, size_t count, int dtype, int ctas_per_rank, int sys_scope,
+                          int* slices, int* sub, int* lanes);
 
 /* ---- per-process communicator (one process per GPU) ----------------------
  * stragglar_init(rank, world, straggler_rank): rank and straggler_rank in

@@ -77,6 +77,7 @@ struct Comm {
   int sub = 1;                 // slices per CTA at most (STRAGGLAR_SUBSLICES)
   uint64_t sub_bytes = 0;      // target slice size on large messages (STRAGGLAR_SUBSLICE_BYTES)
   int lanes_max = kMaxOps;     // Phase-B op lanes per slice at most (STRAGGLAR_OP_LANES; 1 = off)
+  int rs_whole = 0;                 // Phase A over a CTA's sub slices as one range (STRAGGLAR_RS_WHOLE)
   uint64_t lane_slice_max = 32768;  // slices may grow to this size to make room for op lanes
                                     // (STRAGGLAR_LANE_SLICE_MAX; 0 = keep slice_bytes)
   bool rs_pending = false;     // team: a Phase A awaits its Phase B (same call epoch)
@@ -216,6 +217,7 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   if (c.sub < 1) c.sub = 1;
   if (c.sub > kMaxSub) c.sub = kMaxSub;
   c.lane_slice_max = env_u64("STRAGGLAR_LANE_SLICE_MAX", 32768);
+  c.rs_whole = (int)env_u64("STRAGGLAR_RS_WHOLE", 0) ? 1 : 0;
   c.lanes_max = (int)env_u64("STRAGGLAR_OP_LANES", kMaxOps);
   if (c.lanes_max < 1) c.lanes_max = 1;
   c.e2e_piece_bytes = env_u64("STRAGGLAR_E2E_PIECE_BYTES", 8ull << 20);
@@ -366,6 +368,7 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
   P.state = c.state;
   P.host_err = c.host_err_dev;
   P.lanes = 1;
+  P.rs_whole = c.rs_whole;
   P.bc_partner = c.progs.bc_partner;
   for (int p = 0; p < c.world; ++p) {
     P.flags[p] = c.peer_flags[p];
@@ -658,6 +661,34 @@ int stragglar_schedule_round(int world, int round, int* out, int max_transfers, 
   } catch (const std::exception&) {
     return STRAGGLAR_ERR_UNSUPPORTED;
   }
+  return STRAGGLAR_OK;
+}
+
+// Host-only: the slice / sub-slice / op-lane layout a StragglAR call of this
+// size would use, for a per-rank CTA budget and the default knobs (tests).
+int stragglar_plan_layout(int world, int straggler_rank, size_t count, int dtype, int ctas_per_rank, int sys_scope,
+                          int* slices, int* sub, int* lanes) {
+  if (!slices || !sub || !lanes || ctas_per_rank < 1 || ctas_per_rank > kMaxSlices) return STRAGGLAR_ERR_INVALID_ARG;
+  if (!supported_world(world)) return STRAGGLAR_ERR_UNSUPPORTED;
+  if (straggler_rank < 0 || straggler_rank >= world) return STRAGGLAR_ERR_INVALID_ARG;
+  if (!esize_of(dtype)) return STRAGGLAR_ERR_UNSUPPORTED;
+  Comm c;
+  try {
+    c.progs = build_programs(world, straggler_rank);
+  } catch (const std::exception&) {
+    return STRAGGLAR_ERR_INTERNAL;
+  }
+  c.world = world;
+  c.sigma = straggler_rank;
+  c.G = c.G_alloc = ctas_per_rank;
+  c.sys_scope = sys_scope ? 1 : 0;
+  c.sub = c.sys_scope ? 1 : kMaxSub;
+  c.sub_bytes = 128 * 1024;
+  LaunchPlan P = base_plan(c, count, dtype, true);
+  stragglar_layout(c, P);
+  *slices = P.G;
+  *sub = P.sub;
+  *lanes = P.lanes;
   return STRAGGLAR_OK;
 }
 

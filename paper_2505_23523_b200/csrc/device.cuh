@@ -38,6 +38,19 @@ __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
 __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
   asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// a release fence followed by relaxed flag stores (several flags, one fence)
+__device__ __forceinline__ void fence_release(bool sys) {
+  if (sys)
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+__device__ __forceinline__ void st_flag(uint32_t* p, uint32_t v, bool sys) {
+  if (sys)
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  else
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 // scope-selected flag access: sys for CUDA-IPC peers on other GPUs, gpu for one device
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p, bool sys) {
   return sys ? ld_acquire_sys(p) : ld_acquire_gpu(p);

@@ -594,9 +594,15 @@ __device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int me, u
   const char* src[W - 1];
 #pragma unroll
   for (int j = 0; j < W - 1; ++j) src[j] = P.buf[j < P.sigma ? j : j + 1];
-  for (int j = 0; j < P.sub; ++j) {
+  // P.rs_whole: the CTA's `sub` adjacent slices are reduced as one range (no
+  // pipeline drain between them) and flagged together after it, with one
+  // release fence for all of them; otherwise slice by slice (the next hop can
+  // start on the first slice sooner).
+  const int nseg = P.rs_whole ? 1 : P.sub;
+  for (int j = 0; j < nseg; ++j) {
     const int v = m * P.sub + j;
-    const Range r = slice_of(c.lo, c.hi, v, NV, 16 / P.esize);
+    Range r = slice_of(c.lo, c.hi, v, NV, 16 / P.esize);
+    if (P.rs_whole) r.hi = slice_of(c.lo, c.hi, m * P.sub + P.sub - 1, NV, 16 / P.esize).hi;
     // with two ranks the owner's chunk already is the non-straggler "sum"
     if constexpr (W > 2) {
       if constexpr (MV == MOVER_TMA) {
@@ -608,16 +614,21 @@ __device__ void rs_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int me, u
         rs_slice<DT, W>(P, src, P.buf[me], r.lo * P.esize, r.hi * P.esize);
       }
     }
+    const int v1 = P.rs_whole ? m * P.sub + P.sub : v + 1;   // slices [v, v1) are done
+    __syncthreads();
     if constexpr (BC) {
-      __syncthreads();
-      if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma)
-        st_release(flag_at(P.flags[threadIdx.x], SLOT_RSDONE + g, P.fstride, v), ep, P.sys_scope);
-    } else {
-      // "partial ready" for the straggler's half of the exchange
-      cta_signal(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, P.fstride, v), ep, P.sys_scope);
-      // and for this rank's own exchange when another op lane runs it
-      if (P.lanes > 1 && threadIdx.x == kSignalThread)
-        st_release(flag_at(P.flags[me], SLOT_RS_LOCAL, P.fstride, v), ep, false);
+      if (threadIdx.x < W && (int)threadIdx.x != me && (int)threadIdx.x != P.sigma) {
+        fence_release(P.sys_scope);
+        for (int u = v; u < v1; ++u) st_flag(flag_at(P.flags[threadIdx.x], SLOT_RSDONE + g, P.fstride, u), ep, P.sys_scope);
+      }
+    } else if (threadIdx.x == kSignalThread) {
+      // "partial ready" for the straggler's half of the exchange, and for this
+      // rank's own exchange when another op lane runs it
+      fence_release(P.sys_scope);
+      for (int u = v; u < v1; ++u) {
+        st_flag(flag_at(P.flags[P.sigma], SLOT_RSDONE + g, P.fstride, u), ep, P.sys_scope);
+        if (P.lanes > 1) st_flag(flag_at(P.flags[me], SLOT_RS_LOCAL, P.fstride, u), ep, false);
+      }
     }
   }
 }

@@ -78,6 +78,7 @@ struct LaunchPlan {
   int lanes;                 // op lanes per slice (Phase B): CTA lane q runs the rank's ops k with
                              // k % lanes == q, each as soon as its own inputs have landed (1 = one
                              // CTA walks all ops of the slice in round order)
+  int rs_whole;              // Phase A: a CTA's sub slices as one range, flagged together (kernels.cuh rs_body)
   int nlocal;                // ranks served by this launch (1, or world in team mode)
   int fstride;               // flags per slot (G_max * kMaxSub, fixed per communicator; see flag_at)
   int local_rank[kMaxWorld]; // physical rank of local index i (blockIdx.x / G)

@@ -47,6 +47,8 @@ _SIGS = {
     "stragglar_launch_count": ([ctypes.POINTER(_c_u64)], _c_int),
     "stragglar_schedule_rounds": ([_c_int, ctypes.POINTER(_c_int)], _c_int),
     "stragglar_schedule_round": ([_c_int, _c_int, ctypes.POINTER(_c_int), _c_int, ctypes.POINTER(_c_int)], _c_int),
+    "stragglar_plan_layout": ([_c_int, _c_int, _c_size, _c_int, _c_int, _c_int, ctypes.POINTER(_c_int),
+                               ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)], _c_int),
     "stragglar_init": ([_c_int, _c_int, _c_int], _c_int),
     "stragglar_handle_size": ([ctypes.POINTER(_c_size)], _c_int),
     "stragglar_export_handle": ([_vp], _c_int),
@@ -187,6 +189,16 @@ def stragglar_schedule_round(world: int, rnd: int) -> List[Tuple[int, int, int, 
     k = _c_int(0)
     _ck("stragglar_schedule_round", _lib.stragglar_schedule_round(world, rnd, out, cap, ctypes.byref(k)))
     return [tuple(out[4 * i:4 * i + 4]) for i in range(k.value)]
+
+
+def stragglar_plan_layout(world: int, straggler_rank: int, count: int, dtype_code: int, ctas_per_rank: int,
+                          sys_scope: bool = False):
+    """-> (slices per chunk, slices per CTA, op lanes) of a StragglAR call (host only)."""
+    g, sub, lanes = _c_int(0), _c_int(0), _c_int(0)
+    _ck("stragglar_plan_layout", _lib.stragglar_plan_layout(world, straggler_rank, int(count), dtype_code, ctas_per_rank,
+                                                            1 if sys_scope else 0, ctypes.byref(g), ctypes.byref(sub),
+                                                            ctypes.byref(lanes)))
+    return g.value, sub.value, lanes.value
 
 
 # ---------------------------------------------------------------- per-process communicator

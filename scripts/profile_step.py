@@ -13,7 +13,7 @@ import __graft_entry__  # noqa: E402
 __graft_entry__.build()
 from paper_2505_23523_b200 import stragglar as S  # noqa: E402
 
-world, sigma = 8, 0
+world, sigma = 8, int(os.environ.get("PROFILE_SIGMA", "0"))
 count = int(os.environ.get("PROFILE_COUNT", str(1 << 26)))
 dt = {"f32": torch.float32, "bf16": torch.bfloat16}[os.environ.get("PROFILE_DTYPE", "f32")]
 steps = int(os.environ.get("PROFILE_STEPS", "3"))
