@@ -381,12 +381,14 @@ int stragglar_allreduce_auto(void* buf, size_t count, int dtype, int op, void* s
 /* Environment knobs, read once by stragglar_init / stragglar_team_init:
  * STRAGGLAR_MOVER=tma|lsu (data mover), STRAGGLAR_SLICE_BYTES (target bytes
  * per slice, 16384), STRAGGLAR_SLICES (per-process CTA cap, 2 x SMs),
- * STRAGGLAR_SUBSLICES (slices per CTA at most, 1..16; default 16 with
- * gpu-scope flags (team mode), 1 with system-scope flags (per-process mode,
- * where each extra flag costs a system-scope fence)) and
+ * STRAGGLAR_SUBSLICES (slices per CTA at most, 1..16; default 16) and
  * STRAGGLAR_SUBSLICE_BYTES (their target size on large messages, 131072: each
  * hop hands over ~128 KB pieces, so a forwarded slice is still in L2 when
  * the next hop reads it),
+ * STRAGGLAR_OP_LANES (Phase-B op lanes per slice at most, 16; 1 = off),
+ * STRAGGLAR_LANE_SLICE_MAX (slices may grow to this many bytes to make room
+ * for op lanes on small messages, 32768; 0 = off), STRAGGLAR_RS_WHOLE (Phase A
+ * reduces a CTA's sub-slices as one range and flags them together, 1),
  * STRAGGLAR_TIMEOUT_MS (watchdog, 10000), STRAGGLAR_SYS_SCOPE (team mode: system-scope flags, 0), and for the host
  * entry point STRAGGLAR_E2E_PIECE_BYTES (8 MiB) / STRAGGLAR_E2E_STREAMS (1). */
 

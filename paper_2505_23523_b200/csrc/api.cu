@@ -77,7 +77,7 @@ struct Comm {
   int sub = 1;                 // slices per CTA at most (STRAGGLAR_SUBSLICES)
   uint64_t sub_bytes = 0;      // target slice size on large messages (STRAGGLAR_SUBSLICE_BYTES)
   int lanes_max = kMaxOps;     // Phase-B op lanes per slice at most (STRAGGLAR_OP_LANES; 1 = off)
-  int rs_whole = 0;                 // Phase A over a CTA's sub slices as one range (STRAGGLAR_RS_WHOLE)
+  int rs_whole = 1;                 // Phase A over a CTA's sub slices as one range (STRAGGLAR_RS_WHOLE)
   uint64_t lane_slice_max = 32768;  // slices may grow to this size to make room for op lanes
                                     // (STRAGGLAR_LANE_SLICE_MAX; 0 = keep slice_bytes)
   bool rs_pending = false;     // team: a Phase A awaits its Phase B (same call epoch)
@@ -184,8 +184,19 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
     c.mover = (m && std::strcmp(m, "lsu") == 0) ? MOVER_LSU : (m && std::strcmp(m, "tma") == 0) ? MOVER_TMA : kDefaultMover;
   }
   int sms = 0;
-  const int cap = resident_ctas(world, c.mover, &sms);
+  int cap = resident_ctas(world, c.mover, &sms);
   if (cap <= 0) return STRAGGLAR_ERR_CUDA;
+  const int device_cap = cap;   // the whole GPU's (what ranks sharing it divide, stragglar_import_handles)
+  {
+    // an MPS client capped to a share of the SMs can keep only that share resident
+    const uint64_t pct = env_u64("CUDA_MPS_ACTIVE_THREAD_PERCENTAGE", 100);
+    if (pct >= 1 && pct < 100) {
+      cap = (int)(cap * pct / 100);
+      sms = (int)(sms * pct / 100);
+      if (sms < 1) sms = 1;
+      if (cap < 1) cap = 1;
+    }
+  }
   int G;
   if (team) {
     G = cap / world;                                   // every rank's CTAs co-resident
@@ -199,7 +210,7 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   if (G < 1 || (team && G * world > cap)) return STRAGGLAR_ERR_UNSUPPORTED;
   c.G = G;
   c.G_alloc = G;
-  c.resident = cap;
+  c.resident = device_cap;
   c.world = world;
   c.rank = team ? -1 : rank;
   c.sigma = sigma;
@@ -209,15 +220,17 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   c.timeout_ns = env_u64("STRAGGLAR_TIMEOUT_MS", 10000) * 1000000ull;
   c.slice_bytes = env_u64("STRAGGLAR_SLICE_BYTES", 16384);
   c.sys_scope = team ? (int)env_u64("STRAGGLAR_SYS_SCOPE", 0) : 1;
-  // Sub-slices (finer hand-offs) pay with gpu-scope flags (team: Phase B -3.7 %)
-  // but not with system-scope ones, where every extra flag costs a system-scope
-  // fence.
-  c.sub = (int)env_u64("STRAGGLAR_SUBSLICES", c.sys_scope ? 1 : kMaxSub);
+  // Sub-slices (finer hand-offs): team Phase B -3.7 % at gpu scope; at system
+  // scope (per process, MPS-shared GPU, round 2) equal or better for T_post
+  // (config 2 n = 8: 667-708 vs 715-716 us) and 10 % better for the Ring, once
+  // Phase A no longer pays a drain and a fence per sub-slice (rs_whole;
+  // DESIGN.md §10).  Round 1 chose 1 at system scope under a 12 % MPS thread cap.
+  c.sub = (int)env_u64("STRAGGLAR_SUBSLICES", kMaxSub);
   c.sub_bytes = env_u64("STRAGGLAR_SUBSLICE_BYTES", 128 * 1024);
   if (c.sub < 1) c.sub = 1;
   if (c.sub > kMaxSub) c.sub = kMaxSub;
   c.lane_slice_max = env_u64("STRAGGLAR_LANE_SLICE_MAX", 32768);
-  c.rs_whole = (int)env_u64("STRAGGLAR_RS_WHOLE", 0) ? 1 : 0;
+  c.rs_whole = (int)env_u64("STRAGGLAR_RS_WHOLE", 1) ? 1 : 0;
   c.lanes_max = (int)env_u64("STRAGGLAR_OP_LANES", kMaxOps);
   if (c.lanes_max < 1) c.lanes_max = 1;
   c.e2e_piece_bytes = env_u64("STRAGGLAR_E2E_PIECE_BYTES", 8ull << 20);
@@ -682,7 +695,7 @@ int stragglar_plan_layout(int world, int straggler_rank, size_t count, int dtype
   c.sigma = straggler_rank;
   c.G = c.G_alloc = ctas_per_rank;
   c.sys_scope = sys_scope ? 1 : 0;
-  c.sub = c.sys_scope ? 1 : kMaxSub;
+  c.sub = kMaxSub;
   c.sub_bytes = 128 * 1024;
   LaunchPlan P = base_plan(c, count, dtype, true);
   stragglar_layout(c, P);

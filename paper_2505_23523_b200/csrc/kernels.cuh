@@ -913,9 +913,11 @@ __device__ void direct_body(const LaunchPlan& P, Pipe& pipe, int s, int me, uint
         }
       }
       __syncthreads();
-      for (int j = 0; j < P.sub; ++j)
-        if (threadIdx.x < W && (int)threadIdx.x != me)
-          st_release(flag_at(P.flags[threadIdx.x], SLOT_HAVE + own, P.fstride, s * P.sub + j), ep, P.sys_scope);
+      if (threadIdx.x < W && (int)threadIdx.x != me) {   // one release fence per peer for all its flags
+        fence_release(P.sys_scope);
+        for (int j = 0; j < P.sub; ++j)
+          st_flag(flag_at(P.flags[threadIdx.x], SLOT_HAVE + own, P.fstride, s * P.sub + j), ep, P.sys_scope);
+      }
     }
   }
   // postcondition: every other chunk has landed here (one waiting thread per flag)

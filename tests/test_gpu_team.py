@@ -663,3 +663,43 @@ def test_sweep_max_size_bf16_sampled(S):
         assert np.array_equal(got, want), algo
         del bufs
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("knobs", [
+    {"STRAGGLAR_OP_LANES": "1"},                                   # one CTA walks a slice's ops in round order
+    {"STRAGGLAR_OP_LANES": "16", "STRAGGLAR_LANE_SLICE_MAX": "0"},  # lanes, plain 16 KB slices
+    {"STRAGGLAR_LANE_SLICE_MAX": "65536"},                         # lanes with up to 64 KB slices
+    {"STRAGGLAR_RS_WHOLE": "1", "STRAGGLAR_SUBSLICES": "16", "STRAGGLAR_SUBSLICE_BYTES": "4096"},
+    {"STRAGGLAR_SYS_SCOPE": "1", "STRAGGLAR_OP_LANES": "16"},
+])
+def test_layout_knobs_same_bits(S, knobs):
+    """Round-2 layout choices (op lanes, lane-aware slices, whole-range Phase A
+    with batched flags) change who moves which bytes when, never the result:
+    split and fused calls stay bit-exact vs the oracle."""
+    old = {k: os.environ.get(k) for k in knobs}
+    try:
+        os.environ.update(knobs)
+        for n, sigma in [(4, 1), (6, 5), (8, 3)]:
+            for dtype in ("float32", "bfloat16"):
+                for count in [5003, 200_003, 1_500_001]:
+                    xs = make_inputs(n, count, dtype, config=33)
+                    want = N.stragglar_allreduce(xs, sigma, dtype)
+                    for split in (False, True):
+                        bufs = [to_dev(x, dtype) for x in xs]
+                        S.stragglar_team_init(n, sigma)
+                        if split:
+                            S.stragglar_team_reduce_scatter(bufs)
+                            S.stragglar_team_inject_delay(20_000)
+                            S.stragglar_team_complete(bufs)
+                        else:
+                            S.stragglar_team_allreduce(bufs)
+                        torch.cuda.synchronize()
+                        assert S.stragglar_team_check_error() == 0
+                        check_equal([to_host(b, dtype) for b in bufs], want, xs, dtype,
+                                    f"{knobs} n={n} {dtype} count={count} split={split}")
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v

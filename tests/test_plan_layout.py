@@ -50,7 +50,7 @@ def test_layout_invariants(S, world, budget, sys_scope):
             G, sub, lanes = S.stragglar_plan_layout(world, world - 1, count, dtype, budget, sys_scope)
             cb = chunk_bytes(count, world, ESZ[dtype])
             assert 1 <= G <= budget
-            assert 1 <= sub <= 16 and (sub == 1 or not sys_scope)
+            assert 1 <= sub <= 16
             assert 1 <= lanes <= rounds                      # at most one op per rank per round (Thm 1 rounds)
             assert G * lanes <= budget                        # co-resident within the CTA budget
             if lanes > 1:
@@ -75,6 +75,8 @@ def test_named_configurations(S):
     assert S.stragglar_plan_layout(8, 0, 1 << 26, 1, 74) == (74, 4, 1)
     # the same per process (2 x 148 SMs, system scope): one ~130 KB slice per CTA
     assert S.stragglar_plan_layout(8, 0, 1 << 26, 1, 296, True) == (296, 1, 1)
+    # 1 GiB bf16 per process: ~128 KB sub-slices, 4 per CTA
+    assert S.stragglar_plan_layout(8, 0, 1 << 29, 2, 296, True) == (296, 4, 1)
     # 2 MiB bf16: 32 KB slices make room for 7 lanes
     assert S.stragglar_plan_layout(8, 0, 1 << 20, 2, 74) == (10, 1, 7)
 
