@@ -526,6 +526,11 @@ def _nccl_log_summary(path_glob):
     return out
 
 
+def _nccl_version(torch):
+    v = torch.cuda.nccl.version()
+    return ".".join(map(str, v)) if isinstance(v, (tuple, list)) else str(v)
+
+
 def bench_multi(args):
     import torch
     import torch.distributed as dist
@@ -804,7 +809,7 @@ def bench_multi(args):
         "nccl_us": results["nccl_default"]["T_post_us"] if "nccl_default" in results else None,
         "speedup_vs_ring_post": sp["ring"]["post"],
         "speedup_vs_nccl_post": sp["nccl_default"]["post"] if "nccl_default" in sp else None,
-        "nccl": ({"torch_nccl_version": ".".join(map(str, torch.cuda.nccl.version())),
+        "nccl": ({"torch_nccl_version": _nccl_version(torch),
                   "groups": {k: (v if isinstance(v, str) else "ok") for k, v in nccl_groups.items()},
                   "log_rank0": nccl_logs} if not shared else
                  {"value": None, "why": "NCCL cannot place two ranks on one GPU; the shared-device run has no NCCL arm"}),
