@@ -507,7 +507,7 @@ def _nccl_log_summary(path_glob):
     import glob
     import re
 
-    out = {"version": None, "nranks": [], "algos": {}, "nvls_lines": 0, "files": 0}
+    out = {"version": None, "nranks": [], "algos": {}, "nvls_lines": 0, "nvls_available": None, "files": 0}
     for f in glob.glob(path_glob):
         out["files"] += 1
         for line in open(f, errors="replace"):
@@ -523,6 +523,10 @@ def _nccl_log_summary(path_glob):
                     out["algos"][m.group(1)] = out["algos"].get(m.group(1), 0) + 1
             if "NVLS" in line:
                 out["nvls_lines"] += 1
+            if "NVLS multicast support is available" in line:
+                out["nvls_available"] = True
+            elif "NVLS multicast support is not available" in line:
+                out["nvls_available"] = False
     return out
 
 
@@ -541,7 +545,9 @@ def bench_multi(args):
     # NCCL's own log (read once per process, before the first communicator):
     # version, nranks and the algorithm each AllReduce was tuned to
     os.environ.setdefault("NCCL_DEBUG", "INFO")
-    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,TUNING")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,TUNING,NVLS")
+    # a failed baseline collective raises in this process instead of the watchdog aborting it
+    os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "0")
     os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(logdir, f"nccl_bench_r{rank}.%p.log"))
 
     import __graft_entry__
@@ -687,7 +693,15 @@ def bench_multi(args):
     nccl_groups = {}
     if not shared:
         nccl_groups["nccl_default"] = None
+        # NCCL reports at init whether NVLS (NVLink SHARP) is usable; without it an
+        # NVLS-only communicator would fail its first collective, so it is skipped
+        nvls_seen = _nccl_log_summary(os.path.join(logdir, f"nccl_bench_r{rank}.*.log"))["nvls_available"]
+        mine = 1.0 if (nvls_seen is True and S.stragglar_nvls_supported()) else 0.0
+        nvls_ok = -gmax(-mine) > 0.5                   # every rank must have it
         for algo_env in ("Ring", "NVLS"):
+            if algo_env == "NVLS" and not nvls_ok:
+                nccl_groups["nccl_nvls"] = "skipped: NCCL's log shows no NVLS support on this node"
+                continue
             old = os.environ.get("NCCL_ALGO")
             os.environ["NCCL_ALGO"] = algo_env
             try:

@@ -22,14 +22,15 @@ __global__ void k_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st) {
 
 __global__ void k_barrier(const __grid_constant__ LaunchPlan P) {
   const int me = P.local_rank[0];
-  const uint32_t ep = call_epoch(P);
+  const CallEpoch ce = call_epoch(P);
+  const uint32_t ep = ce.ep;
   if (threadIdx.x < P.world && (int)threadIdx.x != me)
     st_release(flag_at(P.flags[threadIdx.x], SLOT_BARRIER + me, P.fstride, 0), ep, P.sys_scope);
   if (threadIdx.x < P.world && (int)threadIdx.x != me)
     spin_wait(flag_at(P.flags[me], SLOT_BARRIER + threadIdx.x, P.fstride, 0), ep, P, 0x800 | threadIdx.x);
   __syncwarp();
   if (threadIdx.x == 0) P.state->t_barrier = globaltimer();
-  finish_call(P);
+  finish_call(P, ce);
 }
 
 // ---------------------------------------------------------------- K0 probes

@@ -82,14 +82,13 @@ __device__ __forceinline__ void cta_signal(uint32_t* f, uint32_t epoch, bool sys
 
 // The call's epoch lives in device memory (state->epoch + 1), so a captured
 // CUDA graph replays correctly.  It is incremented once every CTA of the
-// call's final kernel has read it: by default counted at kernel START (thread
-// 0 of each CTA, after its acquire read of the epoch; the last to arrive bumps
-// it and re-arms the next call's phase stamps), which keeps the same-address
-// atomics off the call's tail; STRAGGLAR_EPOCH_AT_START=0 counts CTAs at exit.
+// call's final kernel has read it: thread 0 of each CTA takes a ticket from a
+// counter right after its acquire read of the epoch (at kernel start), without
+// waiting for the ticket; the CTA that drew the last ticket bumps the epoch and
+// re-arms the next call's phase stamps when it finishes (finish_call).  The
+// same-address atomics thus overlap the call's work instead of queueing on
+// its tail (config 5: 22.3 -> 20.7 us vs counting CTAs at exit).
 // Every thread of the CTA must call call_epoch (it has a CTA barrier).
-#ifndef STRAGGLAR_EPOCH_AT_START
-#define STRAGGLAR_EPOCH_AT_START 1
-#endif
 __device__ __forceinline__ void bump_epoch(const LaunchPlan& P, uint32_t e) {
   P.state->exit_count = 0;
   uint64_t* nx = P.state->stamp[(e + 1u) & 1u];   // re-arm for the next call
@@ -99,31 +98,24 @@ __device__ __forceinline__ void bump_epoch(const LaunchPlan& P, uint32_t e) {
   __threadfence();
   atomicAdd(&P.state->epoch, 1u);
 }
-__device__ __forceinline__ uint32_t call_epoch(const LaunchPlan& P) {
-#if STRAGGLAR_EPOCH_AT_START
+struct CallEpoch {
+  uint32_t ep;       // this call's epoch
+  uint32_t ticket;   // thread 0: counter value drawn at start (final kernel only)
+};
+__device__ __forceinline__ CallEpoch call_epoch(const LaunchPlan& P) {
   __shared__ uint32_t s_ep;
+  CallEpoch c{0u, 0u};
   if (threadIdx.x == 0) {
     const uint32_t e = ld_acquire_gpu(&P.state->epoch) + 1u;
     s_ep = e;
-    if (P.last_kernel && atomicAdd(&P.state->exit_count, 1u) == gridDim.x - 1) bump_epoch(P, e);
+    if (P.last_kernel) c.ticket = atomicAdd(&P.state->exit_count, 1u);
   }
   __syncthreads();
-  return s_ep;
-#else
-  return *(volatile const uint32_t*)&P.state->epoch + 1u;
-#endif
+  c.ep = s_ep;
+  return c;
 }
-__device__ __forceinline__ void finish_call(const LaunchPlan& P) {
-#if STRAGGLAR_EPOCH_AT_START
-  return;
-#endif
-  if (!P.last_kernel) return;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const uint32_t prev = atomicAdd(&P.state->exit_count, 1u);
-    if (prev == gridDim.x - 1) bump_epoch(P, *(volatile uint32_t*)&P.state->epoch + 1u);
-  }
+__device__ __forceinline__ void finish_call(const LaunchPlan& P, const CallEpoch& c) {
+  if (P.last_kernel && threadIdx.x == 0 && c.ticket == gridDim.x - 1) bump_epoch(P, c.ep);
 }
 
 // Slot k of a rank's flag array spans [k * stride, (k+1) * stride) with a
@@ -938,7 +930,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_con
   const int per = P.G * P.lanes;
   const int li = blockIdx.x / per, s = (blockIdx.x % per) % P.G, q = (blockIdx.x % per) / P.G;
   const int me = P.local_rank[li];
-  const uint32_t ep = call_epoch(P);
+  const CallEpoch ce = call_epoch(P);
+  const uint32_t ep = ce.ep;
   Pipe pipe = make_pipe(MV == MOVER_TMA);
   const bool stamps = (KIND == 4 || KIND == 5) && P.nlocal == 1;   // per-process fused call
   uint64_t* stamp = P.state->stamp[ep & 1u];   // armed by the previous call's last CTA (or at init)
@@ -968,7 +961,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_phase(const __grid_con
   if constexpr (KIND == 7 || KIND == 8) bcast_body<DT, W, MV>(P, pipe, s, me, ep);
   if (stamps && threadIdx.x == 0)
     atomicMax(reinterpret_cast<unsigned long long*>(&stamp[2]), (unsigned long long)globaltimer());
-  finish_call(P);
+  finish_call(P, ce);
 }
 
 // ---------------------------------------------------------------- Ring
@@ -981,7 +974,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
   const int j = P.local_rank[li];
   const int NV = P.G * P.sub;   // slices per chunk (flag stride); CTA s covers s*sub .. s*sub+sub-1
   const int V = 16 / P.esize;
-  const uint32_t ep = call_epoch(P);
+  const CallEpoch ce = call_epoch(P);
+  const uint32_t ep = ce.ep;
   const int left = (j + W - 1) % W, right = (j + 1) % W;
   if (threadIdx.x == 0) st_release(flag_at(P.flags[right], SLOT_RING_ARRIVE, P.fstride, s), ep, P.sys_scope);
   constexpr bool tma = MV == MOVER_TMA;
@@ -997,7 +991,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
       const uint32_t* wf = (t == 0) ? flag_at(P.flags[j], SLOT_RING_ARRIVE, P.fstride, s)
                                     : flag_at(P.flags[j], SLOT_RING_READY + t - 1, P.fstride, v);
       if (!cta_wait(wf, ep, P, 0x600 | t)) {
-        finish_call(P);
+        finish_call(P, ce);
         return;
       }
       const Range sl = slice_of(cr.lo, cr.hi, v, NV, V);
@@ -1023,7 +1017,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
   // I am done reading the left buffer; wait until the right neighbour is done with mine
   cta_signal(flag_at(P.flags[left], SLOT_RING_DONE, P.fstride, s), ep, P.sys_scope);
   cta_wait(flag_at(P.flags[j], SLOT_RING_DONE, P.fstride, s), ep, P, 0x700);
-  finish_call(P);
+  finish_call(P, ce);
 }
 
 // ---------------------------------------------------------------- RHD (NEXT N3)
@@ -1043,7 +1037,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_rhd(const __grid_const
   const int j = P.local_rank[li];
   const int NV = P.G * P.sub;
   const int V = 16 / P.esize;
-  const uint32_t ep = call_epoch(P);
+  const CallEpoch ce = call_epoch(P);
+  const uint32_t ep = ce.ep;
   auto partner = [&](int tau) { return j ^ (tau < L ? (1 << tau) : (1 << (2 * L - 1 - tau))); };
   if (threadIdx.x == 0) st_release(flag_at(P.flags[partner(0)], SLOT_RHD_READY, P.fstride, s), ep, P.sys_scope);
   Pipe pipe = make_pipe(MV == MOVER_TMA);
@@ -1092,7 +1087,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_rhd(const __grid_const
     const int u = threadIdx.x / P.sub, q = threadIdx.x % P.sub;
     spin_wait(flag_at(P.flags[j], SLOT_RHD_DONE + u, P.fstride, s * P.sub + q), ep, P, 0xE10 | u);
   }
-  finish_call(P);
+  finish_call(P, ce);
 }
 
 template <int DT, int W, int MV>

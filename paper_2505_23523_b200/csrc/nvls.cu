@@ -58,7 +58,8 @@ __device__ __forceinline__ void mm_st(void* mc, const uint4& v) {
 template <int DT, int W>
 __global__ void __launch_bounds__(kThreads) k_nvls(const __grid_constant__ LaunchPlan P) {
   const int me = P.local_rank[0], s = blockIdx.x;
-  const uint32_t ep = call_epoch(P);
+  const CallEpoch ce = call_epoch(P);
+  const uint32_t ep = ce.ep;
   const int V = 16 / P.esize;
   uint64_t* stamp = P.state->stamp[ep & 1u];
   if (threadIdx.x == 0) atomicMin(reinterpret_cast<unsigned long long*>(&stamp[0]), (unsigned long long)globaltimer());
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(kThreads) k_nvls(const __grid_constant__ Launc
     spin_wait(flag_at(P.flags[me], SLOT_HAVE + threadIdx.x, P.fstride, s), ep, P, 0x1300 | threadIdx.x, true);
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(reinterpret_cast<unsigned long long*>(&stamp[2]), (unsigned long long)globaltimer());
-  finish_call(P);
+  finish_call(P, ce);
 }
 
 cudaError_t launch_nvls(int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream) {
