@@ -37,3 +37,30 @@ def test_reference_arm_runs_full_workload_unscaled():
     assert "no sampling" in out["cpu_baseline"]["sample"]
     assert out["value"] == out["cpu_baseline"]["value"] == out["e2e"]["value"]
     assert out["ms_per_step"] * 1e3 >= out["value"]
+
+
+def test_nccl_log_summary_parses_version_nranks_algos_and_nvls(tmp_path):
+    """bench.py's NCCL_DEBUG=INFO reader (the N>1 line's `nccl.log_rank0`): version,
+    communicator sizes, the algorithms the tuner logged, and whether NCCL found
+    NVLS usable (which gates the NCCL_ALGO=NVLS arm)."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    log = tmp_path / "nccl_bench_r0.123.log"
+    log.write_text(
+        "host:123:123 [0] NCCL INFO NCCL version 2.28.9+cuda12.9\n"
+        "host:123:200 [0] NCCL INFO NVLS multicast support is available on dev 0\n"
+        "host:123:200 [0] NCCL INFO ncclCommInitRankConfig comm 0x1 rank 0 nRanks 8 nNodes 1 localRanks 8 localRank 0 MNNVL 0\n"
+        "host:123:200 [0] NCCL INFO ncclCommInitRankConfig comm 0x1 rank 0 nranks 8 cudaDev 0 nvmlDev 0 busId 1000 commId 0x2 - Init COMPLETE\n"
+        "host:123:200 [0] NCCL INFO AllReduce: opCount 0 sendbuff 0x1 recvbuff 0x1 count 16 datatype 7 op 0 root 0 comm 0x1 [nranks=8] stream 0x3\n"
+        "host:123:200 [0] NCCL INFO AllReduce: 268435456 Bytes -> Algo NVLS proto SIMPLE channel{Lo..Hi}={0..15}\n"
+        "host:123:200 [0] NCCL INFO AllReduce: 268435456 Bytes -> Algo RING proto SIMPLE channel{Lo..Hi}={0..31}\n")
+    out = bench._nccl_log_summary(str(tmp_path / "nccl_bench_r0.*.log"))
+    assert out["version"] == "2.28.9+cuda12.9"
+    assert out["nranks"] == [8]
+    assert out["algos"] == {"NVLS": 1, "RING": 1}
+    assert out["nvls_available"] is True and out["files"] == 1
+    log.write_text("x NCCL INFO NVLS multicast support is not available on dev 0\n")
+    assert bench._nccl_log_summary(str(tmp_path / "nccl_bench_r0.*.log"))["nvls_available"] is False
