@@ -737,8 +737,11 @@ def bench_multi(args):
         dlys = [e0.elapsed_time(ea) * 1e3 for e0, ea, _ in evs]
         tot, dly = gmax(statistics.mean(tots)), gmax(statistics.mean(dlys))
         posts = [a - b for a, b in zip(tots, dlys)]
+        sem = statistics.stdev(posts) / len(posts) ** 0.5 if len(posts) > 1 else 0.0
         results[name] = {"T_total_us": round(tot, 2), "D_meas_us": round(dly, 2), "T_post_us": round(tot - dly, 2),
-                         "T_post_min_us": round(gmax(min(posts)), 2)}
+                         "T_post_median_us": round(gmax(statistics.median(posts)), 2),
+                         "T_post_min_us": round(gmax(min(posts)), 2), "T_post_sem_us": round(gmax(sem), 2),
+                         "stats": "per rank over the timed steps, then the max over ranks (P:395: mean, SEM)"}
     # phase times of the delayed StragglAR call (in-kernel stamps, each rank's GPU clock)
     T_A = phase_a_measured(D_ns, min(5, args.steps))
     # start-line skew: the barrier's release time compared across ranks (globaltimer)

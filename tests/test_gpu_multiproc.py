@@ -76,3 +76,16 @@ def test_ddp_comm_hook(world, sigma, mode):
     r = subprocess.run([sys.executable, os.path.join(HERE, "mp_ddp.py"), str(world), str(sigma), str(_port()), mode],
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+
+
+def test_layout_mismatch_rejected_at_import():
+    """Ranks with different layout knobs fail at stragglar_import_handles
+    (INVALID_ARG) instead of running with different slice layouts."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    r = subprocess.run([sys.executable, os.path.join(HERE, "mp_layout_mismatch.py"), str(_port())],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
