@@ -530,6 +530,24 @@ def _nccl_log_summary(path_glob):
     return out
 
 
+def nvlink_roofline(bytes_A, bytes_B, T_A, T_post, ingress_gbs, pair_gbs):
+    """per-phase fraction of the NVLink roofline — algorithmic bytes
+    on the busiest port over the phase time, against K0's measured ceilings
+    (Phase A: all-peer ingress; Phase B: pairwise bidirectional) and 900 GB/s."""
+    aA = bytes_A / (T_A * 1e-6) / 1e9 if T_A > 0 else None
+    aB = bytes_B / (T_post * 1e-6) / 1e9
+    return {"bound": "nvlink", "kernel": "k_phase<..., KIND=4> (Phase A + Phase B, one launch)",
+            "achieved": round(aB, 1), "peak": pair_gbs, "unit": "GB/s", "frac": round(aB / pair_gbs, 3),
+            "traffic": None, "peak_source": "K0 measured pair bidirectional TMA push (this run)",
+            "phase_A": {"bytes_per_port": bytes_A, "T_us": round(T_A, 2),
+                        "achieved": round(aA, 1) if aA else None, "peak_k0_ingress": ingress_gbs,
+                        "frac_k0": round(aA / ingress_gbs, 3) if aA else None,
+                        "frac_nominal_900": round(aA / NVLINK_NOMINAL, 3) if aA else None},
+            "phase_B": {"bytes_per_port": bytes_B, "T_us": round(T_post, 2), "achieved": round(aB, 1),
+                        "peak_k0_pair": pair_gbs, "frac_k0": round(aB / pair_gbs, 3),
+                        "frac_nominal_900": round(aB / NVLINK_NOMINAL, 3)}}
+
+
 def _nccl_version(torch):
     v = torch.cuda.nccl.version()
     return ".".join(map(str, v)) if isinstance(v, (tuple, list)) else str(v)
@@ -783,18 +801,7 @@ def bench_multi(args):
                         "in total) and its SMs are split between ranks; no NVLink fraction exists"}
         roof["frac"] = round(roof["achieved"] / hbm, 3)
     else:
-        aA = bytes_A / (T_A * 1e-6) / 1e9 if T_A > 0 else None
-        aB = bytes_B / (T_post * 1e-6) / 1e9
-        roof = {"bound": "nvlink", "kernel": "k_phase<..., KIND=4> (Phase A + Phase B, one launch)",
-                "achieved": round(aB, 1), "peak": nvlink_pair, "unit": "GB/s", "frac": round(aB / nvlink_pair, 3),
-                "traffic": None, "peak_source": "K0 measured pair bidirectional TMA push (this run)",
-                "phase_A": {"bytes_per_port": bytes_A, "T_us": round(T_A, 2),
-                            "achieved": round(aA, 1) if aA else None, "peak_k0_ingress": nvlink_ingress,
-                            "frac_k0": round(aA / nvlink_ingress, 3) if aA else None,
-                            "frac_nominal_900": round(aA / NVLINK_NOMINAL, 3) if aA else None},
-                "phase_B": {"bytes_per_port": bytes_B, "T_us": round(T_post, 2), "achieved": round(aB, 1),
-                            "peak_k0_pair": nvlink_pair, "frac_k0": round(aB / nvlink_pair, 3),
-                            "frac_nominal_900": round(aB / NVLINK_NOMINAL, 3)}}
+        roof = nvlink_roofline(bytes_A, bytes_B, T_A, T_post, nvlink_ingress, nvlink_pair)
     sp = {}
     for name, r_ in results.items():
         if name != "stragglar":

@@ -64,3 +64,21 @@ def test_nccl_log_summary_parses_version_nranks_algos_and_nvls(tmp_path):
     assert out["nvls_available"] is True and out["files"] == 1
     log.write_text("x NCCL INFO NVLS multicast support is not available on dev 0\n")
     assert bench._nccl_log_summary(str(tmp_path / "nccl_bench_r0.*.log"))["nvls_available"] is False
+
+
+def test_nvlink_roofline_per_phase():
+    """The N>1 line's roofline at config 2, n = 8, with made-up K0 ceilings:
+    Phase A (n-2)C per port over T_A, Phase B R*C over T_post."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod2", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    C = bench.chunk_bytes(1 << 26, 7, 4)
+    assert C == 38_347_936                                   # SURVEY §8(a) sizes table
+    r = bench.nvlink_roofline(6 * C, 9 * C, 300.0, 450.0, 800.0, 700.0)
+    assert r["bound"] == "nvlink" and r["unit"] == "GB/s"
+    assert abs(r["phase_A"]["achieved"] - 6 * C / 300e-6 / 1e9) < 0.1
+    assert abs(r["phase_B"]["achieved"] - 9 * C / 450e-6 / 1e9) < 0.1
+    assert r["frac"] == r["phase_B"]["frac_k0"] == round(9 * C / 450e-6 / 1e9 / 700.0, 3)
+    assert r["phase_A"]["frac_nominal_900"] == round(6 * C / 300e-6 / 1e9 / 900.0, 3)
