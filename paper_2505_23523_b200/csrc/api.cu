@@ -356,7 +356,7 @@ void lane_slices(const Comm& c, uint64_t chunk_bytes, int* G, int sub) {
   const int64_t gmin = (int64_t)((chunk_bytes + c.lane_slice_max - 1) / c.lane_slice_max);
   if (g < gmin) g = gmin;
   if (g < 1) g = 1;
-  if (g < *G) *G = (int)g;
+  if (g < *G && c.G / g >= 2) *G = (int)g;   // only when it buys at least two lanes
 }
 
 // The call's epoch is not a launch parameter: kernels read state->epoch + 1 and
@@ -830,8 +830,8 @@ int stragglar_import_buffer(void* buf, const void* blobs, int world) {
   Registration r;
   r.local = static_cast<char*>(buf);
   r.bytes = b[c.rank].bytes;
-  for (int p = 0; p < world; ++p)
-    if (b[p].bytes != r.bytes) return STRAGGLAR_ERR_INVALID_ARG;   // ranks registered different sizes
+  for (int p = 0; p < world; ++p)   // ranks registered different sizes, or blobs out of rank order
+    if (b[p].bytes != r.bytes || b[p].rank != p) return STRAGGLAR_ERR_INVALID_ARG;
   for (int p = 0; p < world; ++p) {
     if (p == c.rank) {
       r.peer[p] = r.local;

@@ -58,6 +58,8 @@ def test_layout_invariants(S, world, budget, sys_scope):
                 assert G >= math.ceil(cb / 32768) or G == budget // lanes   # slices stay <= 32 KB
             if sub > 1:
                 assert G == budget and lanes == 1
+            if lanes == 1 and sub == 1:                       # slices never shrink without buying lanes
+                assert G == min(budget, max(1, math.ceil(cb / 16384)))
 
 
 @pytest.mark.parametrize("world", [4, 6, 8])
@@ -79,6 +81,8 @@ def test_named_configurations(S):
     assert S.stragglar_plan_layout(8, 0, 1 << 29, 2, 296, True) == (296, 4, 1)
     # 2 MiB bf16: 32 KB slices make room for 7 lanes
     assert S.stragglar_plan_layout(8, 0, 1 << 20, 2, 74) == (10, 1, 7)
+    # config 1 (n 4, 4 MiB fp32): 43 slices would buy no second lane, so all 74 CTAs keep 1 slice each
+    assert S.stragglar_plan_layout(4, 0, 1 << 20, 1, 74) == (74, 1, 1)
 
 
 def test_layout_rejects_bad_arguments(S):
