@@ -89,3 +89,16 @@ def test_layout_mismatch_rejected_at_import():
     r = subprocess.run([sys.executable, os.path.join(HERE, "mp_layout_mismatch.py"), str(_port())],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_k0_probes_move_the_right_bytes():
+    """K0: the probe copies land every byte in the right peer
+    segment (push / pull, LSU / TMA) and the flag ping-pong completes."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    r = subprocess.run([sys.executable, os.path.join(HERE, "mp_probe.py"), str(_port())],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
