@@ -283,6 +283,14 @@ int stragglar_nvls_begin(size_t bytes, int* fds, size_t* bytes_out);
 int stragglar_nvls_finish(int mc_all_fd, int mc_ns_fd, int sigma_mem_fd, void** arena);
 int stragglar_allreduce_nvls(void* buf, size_t count, int dtype, int op, void* stream);
 int stragglar_nvls_selftest(int dtype, size_t count, const void* host_in, void* host_out);
+/* Test only: the NVLS kernel with its two multicast operations emulated
+ * through IPC peer pointers (the reducing load as the canonical non-straggler
+ * sum, the multicast store as one store per rank) on a REGISTERED buffer of
+ * the per-process communicator — validates the variant's flags, epochs and
+ * hand-offs where no multicast object exists.  Same arguments and errors as
+ * stragglar_allreduce_nvls (count a multiple of 16 bytes' worth); the result
+ * equals stragglar_allreduce's bit for bit. */
+int stragglar_allreduce_nvls_emulated(void* buf, size_t count, int dtype, int op, void* stream);
 
 /* ---- single-device team (all ranks on the current device) ---------------
  * bufs: array of `world` device pointers (physical rank order), each 16-byte

@@ -26,7 +26,7 @@ cudaError_t launch_delay(const uint64_t* base_ptr, uint64_t ns, DevState* st, cu
 cudaError_t launch_barrier(const LaunchPlan& P, cudaStream_t stream);
 cudaError_t occupancy_blocks_per_sm(int which, int dtype, int world, int mover, int* blocks);
 cudaError_t launch_probe_copy(const ProbeArgs& A, int mover, int nblocks, cudaStream_t stream);
-cudaError_t launch_nvls(int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream);
+cudaError_t launch_nvls(int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream, bool emulated);
 cudaError_t launch_nvls_selftest(int dtype, char* mc, uint64_t bytes, cudaStream_t stream);
 cudaError_t launch_probe_pingpong(uint32_t* mine, uint32_t* theirs, int initiator, int iters, DevState* st,
                                   uint64_t timeout_ns, uint32_t* host_err, cudaStream_t stream);
@@ -619,6 +619,14 @@ void nvls_release(Comm& c) {
 }
 
 int lowest_ns(const Comm& c) { return c.sigma == 0 ? 1 : 0; }
+
+// NVLS variant: one slice per CTA, about one per slice_bytes of a chunk
+int nvls_slices(const Comm& c, const LaunchPlan& P) {
+  const uint64_t chunk_bytes = P.ce * P.esize, per = c.slice_bytes ? c.slice_bytes : 16384;
+  uint64_t g = (chunk_bytes + per - 1) / per;
+  if (g < 1) g = 1;
+  return g < (uint64_t)c.G ? (int)g : c.G;
+}
 
 }  // namespace
 
@@ -1309,18 +1317,29 @@ int stragglar_allreduce_nvls(void* buf, size_t count, int dtype, int op, void* s
   P.nlocal = 1;
   P.local_rank[0] = c.rank;
   P.sub = 1;
-  P.G = c.G;                                   // one slice per CTA
-  {
-    const uint64_t chunk_bytes = P.ce * P.esize, per = c.slice_bytes ? c.slice_bytes : 16384;
-    uint64_t g = (chunk_bytes + per - 1) / per;
-    if (g < 1) g = 1;
-    if (g < (uint64_t)P.G) P.G = (int)g;
-  }
+  P.G = nvls_slices(c, P);                     // one slice per CTA
   P.buf[c.rank] = (char*)buf;
   P.mc_all = (char*)n.mc_all_va + off;
   P.mc_ns = n.mc_ns_va ? (char*)n.mc_ns_va + off : nullptr;
   P.sigma_uc = n.sigma_va ? (char*)n.sigma_va + off : nullptr;
-  if (launch_nvls(dtype, P, P.G, (cudaStream_t)stream) != cudaSuccess) return STRAGGLAR_ERR_CUDA;
+  if (launch_nvls(dtype, P, P.G, (cudaStream_t)stream, false) != cudaSuccess) return STRAGGLAR_ERR_CUDA;
+  g_launches.fetch_add(1);
+  return STRAGGLAR_OK;
+}
+
+int stragglar_allreduce_nvls_emulated(void* buf, size_t count, int dtype, int op, void* stream) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  if (!c.active || !c.imported) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  int st = check_args(buf, count, dtype, op);
+  if (st || count == 0) return st;
+  if (count % (16 / esize_of(dtype))) return STRAGGLAR_ERR_INVALID_ARG;
+  if (sticky_error(c)) return STRAGGLAR_ERR_TIMEOUT;
+  LaunchPlan P;
+  if ((st = proc_plan(buf, count, dtype, &P))) return st;   // registered: P.buf[p] = every rank's copy
+  P.sub = 1;
+  P.G = nvls_slices(c, P);
+  if (launch_nvls(dtype, P, P.G, (cudaStream_t)stream, true) != cudaSuccess) return STRAGGLAR_ERR_CUDA;
   g_launches.fetch_add(1);
   return STRAGGLAR_OK;
 }

@@ -55,7 +55,15 @@ __device__ __forceinline__ void mm_st(void* mc, const uint4& v) {
 // P.buf[me] = this rank's arena (+ call offset), P.mc_ns / P.mc_all = the two
 // multicast mappings, P.sigma_uc = the straggler's arena (unicast peer mapping).
 // count must be a multiple of 16 bytes' worth of elements (host-checked).
-template <int DT, int W>
+//
+// EMU (test only, stragglar_allreduce_nvls_emulated): the same kernel — flags,
+// epochs, arrivals, slices, hand-offs — with the two multicast operations
+// replaced by what they do, through IPC peer pointers (P.buf[p], registered
+// cudaMalloc buffers): the reducing load becomes the canonical non-straggler
+// sum (ascending rank, fp32 accumulation, so the result is bit-exact to the
+// oracle) and the multicast store one store per rank.  It validates the
+// variant's synchronisation where no multicast object can be created (one GPU).
+template <int DT, int W, bool EMU>
 __global__ void __launch_bounds__(kThreads) k_nvls(const __grid_constant__ LaunchPlan P) {
   const int me = P.local_rank[0], s = blockIdx.x;
   const CallEpoch ce = call_epoch(P);
@@ -80,8 +88,15 @@ __global__ void __launch_bounds__(kThreads) k_nvls(const __grid_constant__ Launc
     const uint64_t a = sl.lo * P.esize, nv = (sl.hi - sl.lo) / V;
     if (ok) {
       // Phase A in the switch: partial of the slice = sum over the non-stragglers' copies
-      for (uint64_t i = threadIdx.x; i < nv; i += blockDim.x)
-        st_vec(P.buf[me] + a + i * 16, mm_ld_reduce<DT>(P.mc_ns + a + i * 16));
+      if constexpr (EMU) {
+        const char* src[W - 1];
+#pragma unroll
+        for (int j = 0; j < W - 1; ++j) src[j] = P.buf[j < P.sigma ? j : j + 1];
+        if constexpr (W > 2) rs_slice<DT, W>(P, src, P.buf[me], a, a + nv * 16);
+      } else {
+        for (uint64_t i = threadIdx.x; i < nv; i += blockDim.x)
+          st_vec(P.buf[me] + a + i * 16, mm_ld_reduce<DT>(P.mc_ns + a + i * 16));
+      }
       __syncthreads();
       if (threadIdx.x == 0)
         atomicMax(reinterpret_cast<unsigned long long*>(&stamp[1]), (unsigned long long)globaltimer());
@@ -91,8 +106,14 @@ __global__ void __launch_bounds__(kThreads) k_nvls(const __grid_constant__ Launc
     if (ok) {
       // completion: full = partial (+) x_sigma, one multicast store to every rank's arena
       for (uint64_t i = threadIdx.x; i < nv; i += blockDim.x) {
-        const uint4 z = add_vec<DT>(ld_vec(P.buf[me] + a + i * 16), ld_vec(P.sigma_uc + a + i * 16));
-        mm_st(P.mc_all + a + i * 16, z);
+        if constexpr (EMU) {
+          const uint4 z = add_vec<DT>(ld_vec(P.buf[me] + a + i * 16), ld_vec(P.buf[P.sigma] + a + i * 16));
+#pragma unroll
+          for (int d = 0; d < W; ++d) st_vec(P.buf[d] + a + i * 16, z);
+        } else {
+          const uint4 z = add_vec<DT>(ld_vec(P.buf[me] + a + i * 16), ld_vec(P.sigma_uc + a + i * 16));
+          mm_st(P.mc_all + a + i * 16, z);
+        }
       }
       __syncthreads();
       // hand-off: the multicast stores happen-before every rank's HAVE flag
@@ -108,10 +129,10 @@ __global__ void __launch_bounds__(kThreads) k_nvls(const __grid_constant__ Launc
   finish_call(P, ce);
 }
 
-cudaError_t launch_nvls(int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream) {
+cudaError_t launch_nvls(int dtype, const LaunchPlan& P, int nblocks, cudaStream_t stream, bool emulated) {
   void* fn = nullptr;
 #define STRAGGLAR_NVLS_CASE(DTV, WV) \
-  if (dtype == DTV && P.world == WV) fn = (void*)k_nvls<DTV, WV>;
+  if (dtype == DTV && P.world == WV) fn = emulated ? (void*)k_nvls<DTV, WV, true> : (void*)k_nvls<DTV, WV, false>;
   STRAGGLAR_NVLS_CASE(DT_I32, 2) STRAGGLAR_NVLS_CASE(DT_I32, 4) STRAGGLAR_NVLS_CASE(DT_I32, 6) STRAGGLAR_NVLS_CASE(DT_I32, 8)
   STRAGGLAR_NVLS_CASE(DT_F32, 2) STRAGGLAR_NVLS_CASE(DT_F32, 4) STRAGGLAR_NVLS_CASE(DT_F32, 6) STRAGGLAR_NVLS_CASE(DT_F32, 8)
   STRAGGLAR_NVLS_CASE(DT_BF16, 2) STRAGGLAR_NVLS_CASE(DT_BF16, 4) STRAGGLAR_NVLS_CASE(DT_BF16, 6)

@@ -65,6 +65,7 @@ _SIGS = {
     "stragglar_nvls_finish": ([_c_int, _c_int, _c_int, ctypes.POINTER(_vp)], _c_int),
     "stragglar_allreduce_nvls": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_nvls_selftest": ([_c_int, _c_size, _vp, _vp], _c_int),
+    "stragglar_allreduce_nvls_emulated": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_allreduce": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_allreduce_ring": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_allreduce_direct": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
@@ -410,6 +411,13 @@ def stragglar_nvls_finish(mc_all_fd: int, mc_ns_fd: int, sigma_mem_fd: int) -> i
 def stragglar_allreduce_nvls(t, stream=None) -> None:
     ptr, n, dt = _dev_args(t)
     _ck("stragglar_allreduce_nvls", _lib.stragglar_allreduce_nvls(ptr, n, dt, SUM, _stream_ptr(stream)))
+
+
+def stragglar_allreduce_nvls_emulated(t, stream=None) -> None:
+    """Test only: the NVLS kernel with its multicast operations emulated on a registered buffer."""
+    ptr, n, dt = _dev_args(t)
+    _ck("stragglar_allreduce_nvls_emulated",
+        _lib.stragglar_allreduce_nvls_emulated(ptr, n, dt, SUM, _stream_ptr(stream)))
 
 
 def stragglar_nvls_selftest(host_in) -> "object":

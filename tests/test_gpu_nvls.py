@@ -3,6 +3,8 @@
 * One GPU: the multicast instructions and the VMM/multicast plumbing through a
   one-member multicast object (stragglar_nvls_selftest): a reducing load
   through it returns the member's own data, bit for bit, for every dtype.
+* One GPU, several processes: the kernel's synchronisation with the multicast
+  operations emulated through IPC peer pointers (tests/mp_nvls_emu.py), bit-exact.
 * Two or more GPUs: the whole variant (tests/mp_nvls.py), one process per GPU,
   against the plain definition within the north_star tolerance (int32 exact;
   the switch's summation order is unspecified), ranks bitwise identical.
@@ -72,3 +74,18 @@ def test_nvls_allreduce_multi_gpu(S, dtype):
                         str(_port())], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "OK" in r.stdout
+
+
+@pytest.mark.parametrize("world,sigma,count,dtype", [
+    (2, 1, 40_000, "float32"),
+    (4, 2, 250_000, "bfloat16"),
+    (6, 5, 123_456, "int32"),
+    (8, 3, 524_288, "bfloat16"),      # config 5's shape
+])
+def test_nvls_protocol_emulated(S, world, sigma, count, dtype):
+    """The NVLS kernel's flags / epochs / hand-offs with the multicast operations
+    emulated through IPC peer pointers (processes sharing this GPU): bit-exact vs
+    the oracle's StragglAR result on every rank, three calls back to back."""
+    r = subprocess.run([sys.executable, os.path.join(HERE, "mp_nvls_emu.py"), str(world), str(sigma), str(count), dtype,
+                        str(_port())], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
