@@ -262,13 +262,16 @@ int stragglar_finalize(void);
  *     multicast object (rank 0; -1 elsewhere), fds[1] = the non-straggler
  *     object (the lowest non-straggler rank; -1 elsewhere), fds[2] = this
  *     rank's arena.  The fds stay owned by the library.
- *   nvls_finish(mc_all_fd, mc_ns_fd, sigma_mem_fd, &arena): imports the
- *     objects (rank 0 / the lowest non-straggler pass their own), joins them,
- *     binds the arena, maps the multicast ranges and (non-stragglers) the
- *     straggler's arena; *arena = this rank's arena (device pointer).
+ *   nvls_import(mc_all_fd, mc_ns_fd, sigma_mem_fd): imports the objects (rank
+ *     0 / the lowest non-straggler pass their own) and, on non-stragglers, the
+ *     straggler's arena.  The caller checks that EVERY rank imported before
+ *     any binds: a bind waits until the whole team joined, so a rank that
+ *     failed here would leave the others waiting (stragglar_nvls_release
+ *     undoes a begun / imported arena).
+ *   nvls_bind(&arena): joins both objects, binds the arena, maps the multicast
+ *     ranges and the straggler's arena; *arena = this rank's arena.
  * UNSUPPORTED without multicast support (stragglar_nvls_supported) or the
- * driver entry points; every rank must reach nvls_finish (the binds wait for
- * the whole team).  Released by stragglar_finalize.
+ * driver entry points.  Released by stragglar_nvls_release / _finalize.
  * stragglar_allreduce_nvls: in place on [buf, buf + count) inside the arena
  * (same offset on every rank), count a multiple of 16 bytes' worth of
  * elements (INVALID_ARG otherwise), NOT_REGISTERED outside the arena.
@@ -280,7 +283,9 @@ int stragglar_finalize(void);
  * MEASURED ONLY ON ONE GPU: the multi-GPU path needs >= 2 NVSwitch GPUs. */
 int stragglar_nvls_supported(int* supported);
 int stragglar_nvls_begin(size_t bytes, int* fds, size_t* bytes_out);
-int stragglar_nvls_finish(int mc_all_fd, int mc_ns_fd, int sigma_mem_fd, void** arena);
+int stragglar_nvls_import(int mc_all_fd, int mc_ns_fd, int sigma_mem_fd);
+int stragglar_nvls_bind(void** arena);
+int stragglar_nvls_release(void);
 int stragglar_allreduce_nvls(void* buf, size_t count, int dtype, int op, void* stream);
 int stragglar_nvls_selftest(int dtype, size_t count, const void* host_in, void* host_out);
 /* Test only: the NVLS kernel with its two multicast operations emulated

@@ -110,7 +110,7 @@ struct Comm {
   std::vector<void*> opened;   // IPC mappings to close
   // NEXT N1(i) (nvls.cu): the library-owned arena bound to two multicast objects
   struct Nvls {
-    int stage = 0;                                   // 0 none, 1 begun, 2 ready
+    int stage = 0;                                   // 0 none, 1 begun, 2 imported, 3 bound (ready)
     size_t bytes = 0;                                // arena size (multicast granularity)
     unsigned long long mem = 0, mc_all = 0, mc_ns = 0, sigma_mem = 0;   // CUmemGenericAllocationHandle
     unsigned long long va = 0, mc_all_va = 0, mc_ns_va = 0, sigma_va = 0;
@@ -1247,24 +1247,13 @@ int stragglar_nvls_begin(size_t bytes, int* fds, size_t* bytes_out) {
   return STRAGGLAR_OK;
 }
 
-int stragglar_nvls_finish(int mc_all_fd, int mc_ns_fd, int sigma_mem_fd, void** arena) {
+int stragglar_nvls_import(int mc_all_fd, int mc_ns_fd, int sigma_mem_fd) {
   std::lock_guard<std::mutex> lk(g_mu);
   Comm& c = g_proc;
   auto& n = c.nvls;
   if (!c.active || n.stage != 1) return STRAGGLAR_ERR_NOT_INITIALIZED;
-  if (!arena) return STRAGGLAR_ERR_INVALID_ARG;
   DRV(cuMemImportFromShareableHandle);
-  DRV(cuMulticastAddDevice);
-  DRV(cuMulticastBindMem);
-  DRV(cuDeviceGet);
-  if (!p_cuMemImportFromShareableHandle || !p_cuMulticastAddDevice || !p_cuMulticastBindMem || !p_cuDeviceGet)
-    return STRAGGLAR_ERR_UNSUPPORTED;
-  auto fail = [&](int st) {
-    nvls_release(c);
-    return st;
-  };
-  CUdevice dev;
-  if (p_cuDeviceGet(&dev, c.device) != CUDA_SUCCESS) return fail(STRAGGLAR_ERR_CUDA);
+  if (!p_cuMemImportFromShareableHandle) return STRAGGLAR_ERR_UNSUPPORTED;
   auto import = [&](int fd, unsigned long long* h) {
     CUmemGenericAllocationHandle x = 0;
     if (fd < 0) return STRAGGLAR_ERR_INVALID_ARG;
@@ -1275,9 +1264,33 @@ int stragglar_nvls_finish(int mc_all_fd, int mc_ns_fd, int sigma_mem_fd, void** 
     return STRAGGLAR_OK;
   };
   int st;
-  if (!n.mc_all && (st = import(mc_all_fd, &n.mc_all))) return fail(st);
   const bool ns = c.rank != c.sigma;
-  if (ns && !n.mc_ns && (st = import(mc_ns_fd, &n.mc_ns))) return fail(st);
+  if ((!n.mc_all && (st = import(mc_all_fd, &n.mc_all))) || (ns && !n.mc_ns && (st = import(mc_ns_fd, &n.mc_ns))) ||
+      (ns && (st = import(sigma_mem_fd, &n.sigma_mem)))) {
+    nvls_release(c);
+    return st;
+  }
+  n.stage = 2;
+  return STRAGGLAR_OK;
+}
+
+int stragglar_nvls_bind(void** arena) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Comm& c = g_proc;
+  auto& n = c.nvls;
+  if (!c.active || n.stage != 2) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (!arena) return STRAGGLAR_ERR_INVALID_ARG;
+  DRV(cuMulticastAddDevice);
+  DRV(cuMulticastBindMem);
+  DRV(cuDeviceGet);
+  if (!p_cuMulticastAddDevice || !p_cuMulticastBindMem || !p_cuDeviceGet) return STRAGGLAR_ERR_UNSUPPORTED;
+  auto fail = [&](int st) {
+    nvls_release(c);
+    return st;
+  };
+  CUdevice dev;
+  if (p_cuDeviceGet(&dev, c.device) != CUDA_SUCCESS) return fail(STRAGGLAR_ERR_CUDA);
+  const bool ns = c.rank != c.sigma;
   // every member joins before any binds (a bind waits for the whole team)
   if (p_cuMulticastAddDevice((CUmemGenericAllocationHandle)n.mc_all, dev) != CUDA_SUCCESS) return fail(STRAGGLAR_ERR_CUDA);
   if (ns && p_cuMulticastAddDevice((CUmemGenericAllocationHandle)n.mc_ns, dev) != CUDA_SUCCESS)
@@ -1288,15 +1301,23 @@ int stragglar_nvls_finish(int mc_all_fd, int mc_ns_fd, int sigma_mem_fd, void** 
   if (ns && p_cuMulticastBindMem((CUmemGenericAllocationHandle)n.mc_ns, 0, (CUmemGenericAllocationHandle)n.mem, 0,
                                  n.bytes, 0) != CUDA_SUCCESS)
     return fail(STRAGGLAR_ERR_CUDA);
+  int st;
   if ((st = map_va(n.bytes, (CUmemGenericAllocationHandle)n.mc_all, c.device, &n.mc_all_va))) return fail(st);
   if (ns) {
     if ((st = map_va(n.bytes, (CUmemGenericAllocationHandle)n.mc_ns, c.device, &n.mc_ns_va))) return fail(st);
     // owners read the straggler's input through a unicast peer mapping of its arena
-    if ((st = import(sigma_mem_fd, &n.sigma_mem))) return fail(st);
     if ((st = map_va(n.bytes, (CUmemGenericAllocationHandle)n.sigma_mem, c.device, &n.sigma_va))) return fail(st);
   }
-  n.stage = 2;
+  n.stage = 3;
   *arena = (void*)n.va;
+  return STRAGGLAR_OK;
+}
+
+int stragglar_nvls_release(void) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_proc.active) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  cudaDeviceSynchronize();
+  nvls_release(g_proc);
   return STRAGGLAR_OK;
 }
 
@@ -1304,7 +1325,7 @@ int stragglar_allreduce_nvls(void* buf, size_t count, int dtype, int op, void* s
   std::lock_guard<std::mutex> lk(g_mu);
   Comm& c = g_proc;
   auto& n = c.nvls;
-  if (!c.active || !c.imported || n.stage != 2) return STRAGGLAR_ERR_NOT_INITIALIZED;
+  if (!c.active || !c.imported || n.stage != 3) return STRAGGLAR_ERR_NOT_INITIALIZED;
   int st = check_args(buf, count, dtype, op);
   if (st || count == 0) return st;
   const int es = esize_of(dtype);

@@ -113,18 +113,38 @@ class ProcessComm:
         """NEXT N1(i): allocate and bind this rank's NVLS arena (collective).
         Returns a uint8 CUDA tensor aliasing the arena; stragglar_allreduce_nvls
         reduces views of it in place."""
-        fds, size = self.lib.stragglar_nvls_begin(nbytes)
+        try:
+            fds, size = self.lib.stragglar_nvls_begin(nbytes)
+            began = True
+        except Exception as e:  # noqa: BLE001  (e.g. no multicast support): every rank must learn it
+            began, err = False, e
+        every = [None] * self.world
+        dist.all_gather_object(every, began, group=self.group)
+        if not all(every):
+            if began:
+                self.lib.stragglar_nvls_release()
+            raise RuntimeError(f"NVLS arena setup failed on ranks {[r for r, v in enumerate(every) if not v]}"
+                               + ("" if began else f": {err}"))
         got = exchange_fds({"mc_all": fds[0], "mc_ns": fds[1], "mem": fds[2]}, self.group)
         lowest_ns = 1 if self.straggler == 0 else 0
         mc_all = fds[0] if self.rank == 0 else got[0]["mc_all"]
         mc_ns = fds[1] if self.rank == lowest_ns else got.get(lowest_ns, {}).get("mc_ns", -1)
         sig_mem = got[self.straggler]["mem"] if self.rank != self.straggler else -1
         try:
-            ptr = self.lib.stragglar_nvls_finish(mc_all, mc_ns, sig_mem)
+            st = self.lib.stragglar_nvls_import(mc_all, mc_ns, sig_mem)
         finally:
             for peer in got.values():          # the library imported what it needs
                 for fd in peer.values():
                     os.close(fd)
+        # a bind waits for the whole team: bind only if every rank imported
+        ok = [st == 0]
+        every = [None] * self.world
+        dist.all_gather_object(every, ok[0], group=self.group)
+        if not all(every):
+            if st == 0:
+                self.lib.stragglar_nvls_release()
+            raise RuntimeError(f"NVLS import failed on ranks {[r for r, v in enumerate(every) if not v]} (status {st})")
+        ptr = self.lib.stragglar_nvls_bind()
         self.arena = self.lib.device_bytes(ptr, size)
         return self.arena
 

@@ -62,7 +62,9 @@ _SIGS = {
     "stragglar_probe_pingpong_result": ([ctypes.POINTER(ctypes.c_double)], _c_int),
     "stragglar_nvls_supported": ([ctypes.POINTER(_c_int)], _c_int),
     "stragglar_nvls_begin": ([_c_size, ctypes.POINTER(_c_int), ctypes.POINTER(_c_size)], _c_int),
-    "stragglar_nvls_finish": ([_c_int, _c_int, _c_int, ctypes.POINTER(_vp)], _c_int),
+    "stragglar_nvls_import": ([_c_int, _c_int, _c_int], _c_int),
+    "stragglar_nvls_bind": ([ctypes.POINTER(_vp)], _c_int),
+    "stragglar_nvls_release": ([], _c_int),
     "stragglar_allreduce_nvls": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
     "stragglar_nvls_selftest": ([_c_int, _c_size, _vp, _vp], _c_int),
     "stragglar_allreduce_nvls_emulated": ([_vp, _c_size, _c_int, _c_int, _vp], _c_int),
@@ -400,12 +402,20 @@ def stragglar_nvls_begin(nbytes: int):
     return list(fds), out.value
 
 
-def stragglar_nvls_finish(mc_all_fd: int, mc_ns_fd: int, sigma_mem_fd: int) -> int:
+def stragglar_nvls_import(mc_all_fd: int, mc_ns_fd: int, sigma_mem_fd: int) -> int:
+    """-> status (0 = imported); the caller agrees across ranks before binding."""
+    return int(_lib.stragglar_nvls_import(int(mc_all_fd), int(mc_ns_fd), int(sigma_mem_fd)))
+
+
+def stragglar_nvls_bind() -> int:
     """-> the arena's device pointer."""
     p = _vp(0)
-    _ck("stragglar_nvls_finish", _lib.stragglar_nvls_finish(int(mc_all_fd), int(mc_ns_fd), int(sigma_mem_fd),
-                                                            ctypes.byref(p)))
+    _ck("stragglar_nvls_bind", _lib.stragglar_nvls_bind(ctypes.byref(p)))
     return int(p.value)
+
+
+def stragglar_nvls_release() -> None:
+    _ck("stragglar_nvls_release", _lib.stragglar_nvls_release())
 
 
 def stragglar_allreduce_nvls(t, stream=None) -> None:
