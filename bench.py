@@ -530,6 +530,30 @@ def _nccl_log_summary(path_glob):
     return out
 
 
+def nvlink_counters(gpu_index):
+    """(tx, rx) bytes summed over this GPU's NVLink links from `nvidia-smi nvlink
+    -gt d` (data throughput counters, KiB), or None where the driver reports N/A
+    (NVLink TX/RX bytes for multi-GPU runs, where ncu cannot go)."""
+    import re
+
+    try:
+        r = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(gpu_index)], capture_output=True, text=True,
+                           timeout=20)
+    except Exception:  # noqa: BLE001
+        return None
+    return parse_nvlink_counters(r.stdout)
+
+
+def parse_nvlink_counters(text):
+    import re
+
+    tx = [float(v) for v in re.findall(r"Data Tx:\s*([0-9.]+)\s*KiB", text)]
+    rx = [float(v) for v in re.findall(r"Data Rx:\s*([0-9.]+)\s*KiB", text)]
+    if not tx and not rx:
+        return None
+    return sum(tx) * 1024.0, sum(rx) * 1024.0
+
+
 def nvlink_roofline(bytes_A, bytes_B, T_A, T_post, ingress_gbs, pair_gbs):
     """per-phase fraction of the NVLink roofline — algorithmic bytes
     on the busiest port over the phase time, against K0's measured ceilings
@@ -740,17 +764,30 @@ def bench_multi(args):
                 algos[name] = (lambda g=g: dist.all_reduce(nccl_buf, group=g))
     results, launches_total = {}, 0
     clk_sum = None
+    nvlink_traffic = None
     for name, fn in algos.items():
         timed(fn, args.warmup, D_ns)
         torch.cuda.synchronize()
         dist.barrier()
         l0 = S.stragglar_launch_count()
+        nv0 = nvlink_counters(local) if (name == "stragglar" and not shared) else None
         with ClockSampler(local) as clk:
             evs = timed(fn, args.steps, D_ns)
             torch.cuda.synchronize()
         if name == "stragglar":
             launches_total = S.stragglar_launch_count() - l0
             clk_sum = clk.summary()
+            if not shared:      # collective on every rank, whatever nvidia-smi answered
+                nv1 = nvlink_counters(local)
+                have = nv0 is not None and nv1 is not None
+                tx = gmax((nv1[0] - nv0[0]) / args.steps if have else -1.0)
+                rx = gmax((nv1[1] - nv0[1]) / args.steps if have else -1.0)
+                if -gmax(-(1.0 if have else 0.0)) > 0.5:
+                    nvlink_traffic = {"tx_bytes_per_step": tx, "rx_bytes_per_step": rx,
+                                      "source": "nvidia-smi nvlink -gt d before/after the timed StragglAR steps, "
+                                                "max over ranks (includes the barrier, delay and flag traffic)"}
+                else:
+                    nvlink_traffic = {"value": None, "why": "nvidia-smi reports no NVLink data counters (N/A)"}
         tots = [e0.elapsed_time(e1) * 1e3 for e0, _, e1 in evs]
         dlys = [e0.elapsed_time(ea) * 1e3 for e0, ea, _ in evs]
         tot, dly = gmax(statistics.mean(tots)), gmax(statistics.mean(dlys))
@@ -838,6 +875,7 @@ def bench_multi(args):
                   "log_rank0": nccl_logs} if not shared else
                  {"value": None, "why": "NCCL cannot place two ranks on one GPU; the shared-device run has no NCCL arm"}),
         "k0": k0,
+        "nvlink_counters": nvlink_traffic if not shared else {"value": None, "why": "ranks share one GPU: no NVLink traffic"},
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e, 1), "unit": "us", "h2d_bytes_per_step": S_bytes, "d2h_bytes_per_step": S_bytes,

@@ -82,3 +82,16 @@ def test_nvlink_roofline_per_phase():
     assert abs(r["phase_B"]["achieved"] - 9 * C / 450e-6 / 1e9) < 0.1
     assert r["frac"] == r["phase_B"]["frac_k0"] == round(9 * C / 450e-6 / 1e9 / 700.0, 3)
     assert r["phase_A"]["frac_nominal_900"] == round(6 * C / 300e-6 / 1e9 / 900.0, 3)
+
+
+def test_nvlink_counter_parser():
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("bench_mod3", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    txt = ("GPU 0: NVIDIA B200 (UUID: GPU-x)\n\t Link 0: Data Tx: 1024 KiB\n\t Link 0: Data Rx: 2048 KiB\n"
+           "\t Link 1: Data Tx: 3 KiB\n\t Link 1: Data Rx: 0 KiB\n")
+    assert bench.parse_nvlink_counters(txt) == (1027 * 1024.0, 2048 * 1024.0)
+    # what this round's one-GPU box prints (profiles/r02/nvlink_gt.txt): no numbers
+    assert bench.parse_nvlink_counters("GPU 0: NVIDIA B200\n\t Link 0: Data Tx: N/A\n\t Link 0: Data Rx: N/A\n") is None
