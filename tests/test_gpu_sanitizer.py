@@ -12,14 +12,24 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
-@pytest.mark.parametrize("mover", ["tma", "lsu"])
-def test_sanitizer_clean(tool, mover):
+def _sanitizer():
+    """The compute-sanitizer binary, or skip: not installed, or closed by the
+    GPU pool (its wrapper then refuses every run, exit code 86)."""
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
     if not os.path.exists(cs):
         pytest.skip("compute-sanitizer not installed")
+    r = subprocess.run([cs, "--version"], capture_output=True, text=True, timeout=120)
+    if r.returncode != 0 or "closed" in (r.stdout + r.stderr):
+        pytest.skip("compute-sanitizer unavailable on this pool: " + (r.stdout + r.stderr).strip()[:200])
+    return cs
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck"])
+@pytest.mark.parametrize("mover", ["tma", "lsu"])
+def test_sanitizer_clean(tool, mover):
+    cs = _sanitizer()
     import __graft_entry__
 
     __graft_entry__.build()
@@ -37,11 +47,7 @@ def test_sanitizer_clean_ipc_ranks(tool):
     """The per-process mode: two ranks (torchrun, each under its own
     compute-sanitizer) exchanging CUDA-IPC peer mappings; every algorithm runs
     once and is checked against the oracle inside tests/mp_rank_sanitize.py."""
-    if not torch.cuda.is_available():
-        pytest.skip("no GPU")
-    cs = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
-    if not os.path.exists(cs):
-        pytest.skip("compute-sanitizer not installed")
+    cs = _sanitizer()
     import __graft_entry__
 
     __graft_entry__.build()
