@@ -626,6 +626,11 @@ def bench_multi(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.item()
 
+    def gmax_vec(xs):   # elementwise max over ranks of a per-step list
+        t = torch.tensor([float(x) for x in xs], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
     def gmax_i(x):   # exact for %globaltimer stamps (~1.7e18 ns: beyond float64's integer range)
         t = torch.tensor([int(x)], dtype=torch.int64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -788,15 +793,18 @@ def bench_multi(args):
                                                 "max over ranks (includes the barrier, delay and flag traffic)"}
                 else:
                     nvlink_traffic = {"value": None, "why": "nvidia-smi reports no NVLink data counters (N/A)"}
-        tots = [e0.elapsed_time(e1) * 1e3 for e0, _, e1 in evs]
-        dlys = [e0.elapsed_time(ea) * 1e3 for e0, ea, _ in evs]
-        tot, dly = gmax(statistics.mean(tots)), gmax(statistics.mean(dlys))
+        # per step: completion = max over ranks of the step's total (each rank from its own
+        # barrier release), delay = the straggler's injected idle time; T_post = their difference
+        tots = gmax_vec([e0.elapsed_time(e1) * 1e3 for e0, _, e1 in evs])
+        dlys = gmax_vec([e0.elapsed_time(ea) * 1e3 for e0, ea, _ in evs])
         posts = [a - b for a, b in zip(tots, dlys)]
         sem = statistics.stdev(posts) / len(posts) ** 0.5 if len(posts) > 1 else 0.0
-        results[name] = {"T_total_us": round(tot, 2), "D_meas_us": round(dly, 2), "T_post_us": round(tot - dly, 2),
-                         "T_post_median_us": round(gmax(statistics.median(posts)), 2),
-                         "T_post_min_us": round(gmax(min(posts)), 2), "T_post_sem_us": round(gmax(sem), 2),
-                         "stats": "per rank over the timed steps, then the max over ranks (P:395: mean, SEM)"}
+        results[name] = {"T_total_us": round(statistics.mean(tots), 2), "D_meas_us": round(statistics.mean(dlys), 2),
+                         "T_post_us": round(statistics.mean(posts), 2),
+                         "T_post_median_us": round(statistics.median(posts), 2),
+                         "T_post_min_us": round(min(posts), 2), "T_post_sem_us": round(sem, 2),
+                         "stats": "per timed step the max over ranks (total) minus the straggler's delay; "
+                                  "mean / median / min / SEM over the steps (P:395)"}
     # phase times of the delayed StragglAR call (in-kernel stamps, each rank's GPU clock)
     T_A = phase_a_measured(D_ns, min(5, args.steps))
     # start-line skew: the barrier's release time compared across ranks (globaltimer)

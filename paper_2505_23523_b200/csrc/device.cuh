@@ -23,11 +23,29 @@ __device__ __forceinline__ void st_vec(void* p, const uint4& v) {
 }
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
+#if STRAGGLAR_DIAG_ACQ_GPU
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+#else
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+#endif
   return v;
 }
+// Diagnostic A/B knobs (never on in a product build; NOT valid across GPUs):
+// STRAGGLAR_DIAG_FENCE_GPU=1 issues the system-scope release fence at GPU
+// scope, STRAGGLAR_DIAG_ACQ_GPU=1 the system-scope acquire polls at GPU scope
+// -- to find which half of a system-scope hand-off costs (team mode only).
+#ifndef STRAGGLAR_DIAG_FENCE_GPU
+#define STRAGGLAR_DIAG_FENCE_GPU 0
+#endif
+#ifndef STRAGGLAR_DIAG_ACQ_GPU
+#define STRAGGLAR_DIAG_ACQ_GPU 0
+#endif
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+#if STRAGGLAR_DIAG_FENCE_GPU
+  asm volatile("fence.acq_rel.gpu;\n\tst.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#else
   asm volatile("fence.acq_rel.sys;\n\tst.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#endif
 }
 // GPU-scope variants: enough when every rank lives on this device (team mode)
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
@@ -40,7 +58,7 @@ __device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
 }
 // a release fence followed by relaxed flag stores (several flags, one fence)
 __device__ __forceinline__ void fence_release(bool sys) {
-  if (sys)
+  if (sys && !STRAGGLAR_DIAG_FENCE_GPU)
     asm volatile("fence.acq_rel.sys;" ::: "memory");
   else
     asm volatile("fence.acq_rel.gpu;" ::: "memory");

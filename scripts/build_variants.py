@@ -38,7 +38,11 @@ VARIANTS_HINT = {
 }
 if "--hint2" in sys.argv:
     VARIANTS_HINT = {k: VARIANTS_HINT[k] for k in ("st_el", "ld_el", "st_el_ld_el")}
-VARIANTS = (VARIANTS_LL if "--ll" in sys.argv else VARIANTS_LAG if "--lag" in sys.argv
+VARIANTS_DEFER = {   # round 2 (r02v): the deferred SEND hand-off (since removed) and the scope diagnostics
+    "diag_fence_gpu": ["STRAGGLAR_DIAG_FENCE_GPU=1"],
+    "diag_acq_gpu": ["STRAGGLAR_DIAG_ACQ_GPU=1"],
+}
+VARIANTS = (VARIANTS_DEFER if "--defer" in sys.argv else VARIANTS_LL if "--ll" in sys.argv else VARIANTS_LAG if "--lag" in sys.argv
             else VARIANTS_HINT if ("--hint" in sys.argv or "--hint2" in sys.argv) else VARIANTS_ALL)
 os.makedirs(os.path.join(ROOT, "build", "variants"), exist_ok=True)
 with ThreadPoolExecutor(4) as ex:
