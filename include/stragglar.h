@@ -100,12 +100,10 @@ int stragglar_plan_layout(int world, int straggler_rank, size_t count, int dtype
 /* Host only: the pieces the host-buffer entry points (stragglar_allreduce_host,
  * stragglar_team_allreduce_host) cut a `count`-element buffer into — element
  * counts in order, written to out[0 .. max_pieces), their number to *n_pieces
- * (INVALID_ARG if more than max_pieces).  piece_bytes is the steady piece size
- * (STRAGGLAR_E2E_PIECE_BYTES); ramp != 0 (STRAGGLAR_E2E_RAMP, default on)
- * starts with pieces of 1/8, 1/4, 1/2 of it and ends with 1/2, 1/4, 1/8, so the
- * pipeline's fill and drain move little.  Every piece but the last is a
- * multiple of 16 bytes; the pieces add up to count. */
-int stragglar_plan_e2e_pieces(size_t count, int dtype, size_t piece_bytes, int ramp, size_t* out, int max_pieces,
+ * (INVALID_ARG if more than max_pieces).  piece_bytes is the piece size
+ * (STRAGGLAR_E2E_PIECE_BYTES), rounded down to 16 bytes; every piece but the
+ * last has it, the last takes the rest; the pieces add up to count. */
+int stragglar_plan_e2e_pieces(size_t count, int dtype, size_t piece_bytes, size_t* out, int max_pieces,
                               int* n_pieces);
 
 /* ---- per-process communicator (one process per GPU) ----------------------
@@ -189,8 +187,8 @@ int stragglar_broadcast_tree(int world, int* sender, int* round);
 /* End to end from host memory (collective): host_in (count elements) is
  * copied into the registered device buffer `buf`, AllReduced with
  * stragglar_allreduce, and the result copied to host_out (may equal
- * host_in), through a pipeline of pieces (STRAGGLAR_E2E_PIECE_BYTES, 8 MiB,
- * ramped at both ends: stragglar_plan_e2e_pieces): H2D of piece k+1, the
+ * host_in), through a pipeline of pieces (STRAGGLAR_E2E_PIECE_BYTES, 8 MiB;
+ * stragglar_plan_e2e_pieces): H2D of piece k+1, the
  * AllReduce of piece k and D2H of piece k-1 overlap.  Every rank cuts the
  * same pieces (the piece knobs are checked at import), so each piece is one
  * collective call.
@@ -347,8 +345,7 @@ int stragglar_team_inject_delay(uint64_t ns, void* stream);
 /* End to end from host memory: copies host_in[p] -> bufs[p] (H2D), runs the
  * StragglAR AllReduce, copies bufs[p] -> host_out[p] (D2H), and synchronizes
  * `stream`.  The elementwise SUM lets the buffer go through a pipeline of
- * pieces (default 8 MiB, STRAGGLAR_E2E_PIECE_BYTES; ramped at both ends,
- * stragglar_plan_e2e_pieces): H2D, AllReduce and D2H of consecutive pieces overlap on two copy-engine streams and `stream`.
+ * pieces (default 8 MiB, STRAGGLAR_E2E_PIECE_BYTES; stragglar_plan_e2e_pieces): H2D, AllReduce and D2H of consecutive pieces overlap on two copy-engine streams and `stream`.
  * host_in/host_out should be pinned for full PCIe bandwidth; host_out may
  * equal host_in. */
 int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_out, void* const* bufs,
@@ -415,8 +412,7 @@ int stragglar_allreduce_auto(void* buf, size_t count, int dtype, int op, void* s
  * for op lanes on small messages, 32768; 0 = off), STRAGGLAR_RS_WHOLE (Phase A
  * reduces a CTA's sub-slices as one range and flags them together, 1),
  * STRAGGLAR_TIMEOUT_MS (watchdog, 10000), STRAGGLAR_SYS_SCOPE (team mode: system-scope flags, 0), and for the host
- * entry point STRAGGLAR_E2E_PIECE_BYTES (8 MiB) / STRAGGLAR_E2E_RAMP (1) /
- * STRAGGLAR_E2E_STREAMS (1). */
+ * entry point STRAGGLAR_E2E_PIECE_BYTES (8 MiB) / STRAGGLAR_E2E_STREAMS (1). */
 
 /* Number of kernel launches the library enqueued since load (bench evidence). */
 int stragglar_launch_count(uint64_t* launches);

@@ -47,7 +47,7 @@ std::atomic<uint64_t> g_launches{0};
 // they travel in the flag-array blob and stragglar_import_handles rejects a
 // mismatch instead of running with silently different slice layouts.
 struct Layout {
-  int32_t world, sigma, G_alloc, sub_max, mover, sys_scope, lanes_max, e2e_ramp;
+  int32_t world, sigma, G_alloc, sub_max, mover, sys_scope, lanes_max, pad;
   uint64_t slice_bytes, sub_bytes, lane_slice_max, e2e_piece_bytes;   // e2e: every rank must cut the same pieces
 };
 
@@ -103,7 +103,6 @@ struct Comm {
   int sys_scope = 1;                    // STRAGGLAR_SYS_SCOPE (team mode only; default 0 there)
   uint64_t e2e_piece_bytes = 8ull << 20;// STRAGGLAR_E2E_PIECE_BYTES (8 MiB measured best)
   int e2e_streams = 1;                  // STRAGGLAR_E2E_STREAMS (1 measured best)
-  int e2e_ramp = 1;                     // STRAGGLAR_E2E_RAMP: first / last pieces 1/8, 1/4, 1/2 of a piece
   int last_slices = 0;                  // slices per chunk of the last Phase-B call (trace layout)
   double alpha_s = 3e-6;               // P:450 per-message latency used in the paper's model
   double beta_s_per_byte = 1.0 / 770e9; // measured B200 peer copy per direction (B200_PROFILING.md)
@@ -236,7 +235,6 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   if (c.lanes_max < 1) c.lanes_max = 1;
   c.e2e_piece_bytes = env_u64("STRAGGLAR_E2E_PIECE_BYTES", 8ull << 20);
   c.e2e_streams = (int)env_u64("STRAGGLAR_E2E_STREAMS", 1);
-  c.e2e_ramp = (int)env_u64("STRAGGLAR_E2E_RAMP", 1);
   c.rank_bytes = ((size_t)kSlots * G * kMaxSub * sizeof(uint32_t) + 255) / 256 * 256;
   const size_t nbytes = team ? c.rank_bytes * world : c.rank_bytes;
   auto fail_free = [&]() {
@@ -286,7 +284,6 @@ Layout layout_of(const Comm& c) {
   l.slice_bytes = c.slice_bytes;
   l.sub_bytes = c.sub_bytes;
   l.e2e_piece_bytes = c.e2e_piece_bytes;
-  l.e2e_ramp = c.e2e_ramp;
   return l;
 }
 
@@ -504,43 +501,23 @@ int read_error(Comm& c, int* code, uint32_t* where = nullptr) {
 // rank cuts the same pieces, so each piece's AllReduce is one collective call.
 // Synchronous: returns after the last D2H landed.
 //
-// The pipeline's fill (the first piece's H2D, nothing else moving) and drain
-// (the last piece's D2H) each cost one piece of PCIe time; with `ramp` the
-// first pieces grow 1/8, 1/4, 1/2 -> 1 piece and the last ones shrink the same
-// way, so fill and drain cost about 1/8 of a piece each.  Pure host logic, the
-// same on every rank for the same (count, dtype, piece, ramp).
-std::vector<uint64_t> e2e_pieces(uint64_t count, int es, uint64_t piece_bytes, bool ramp) {
+// The pieces: equal, 16-byte aligned, the last one ragged.  (Ramping the first
+// and last pieces down to 1/8 to shorten the pipeline's fill and drain was
+// measured 0.5 % slower, profiles/r02/ab/r02y_e2e_ramp_ab.json.)  Pure host
+// logic, the same on every rank for the same (count, dtype, piece).
+std::vector<uint64_t> e2e_pieces(uint64_t count, int es, uint64_t piece_bytes) {
   const uint64_t v = 16 / es;
   uint64_t piece = piece_bytes / es / v * v;
   if (piece == 0) piece = v;
   std::vector<uint64_t> lens;
-  uint64_t rem = count;
-  auto take = [&](uint64_t n) {
-    n = n < rem ? n : rem;
-    if (n) lens.push_back(n);
-    rem -= n;
-  };
-  if (!ramp || piece < 8 * v) {
-    while (rem) take(piece);
-    return lens;
-  }
-  const uint64_t q8 = piece / 8 / v * v, q4 = piece / 4 / v * v, q2 = piece / 2 / v * v;
-  take(q8);
-  take(q4);
-  take(q2);
-  const uint64_t tail = q2 + q4 + q8;        // reserved for the ramp-down
-  while (rem > piece + tail) take(piece);
-  if (rem > tail) take((rem - tail + v - 1) / v * v < piece ? (rem - tail + v - 1) / v * v : piece);
-  take(q2);
-  take(q4);
-  while (rem) take(q8);
+  for (uint64_t off = 0; off < count; off += piece) lens.push_back(count - off < piece ? count - off : piece);
   return lens;
 }
 
 template <class F>
 int e2e_pipeline(int nbufs, const void* const* host_in, void* const* host_out, void* const* bufs, size_t count, int es,
-                 cudaStream_t s, uint64_t piece_bytes, int ramp, int ncs, F&& allreduce_piece) {
-  const std::vector<uint64_t> lens = e2e_pieces(count, es, piece_bytes, ramp != 0);
+                 cudaStream_t s, uint64_t piece_bytes, int ncs, F&& allreduce_piece) {
+  const std::vector<uint64_t> lens = e2e_pieces(count, es, piece_bytes);
   const uint64_t npieces = lens.size();
   // copy streams per direction (several copy engines; buffers alternate between them)
   if (ncs < 1) ncs = 1;
@@ -749,12 +726,12 @@ int stragglar_plan_layout(int world, int straggler_rank, size_t count, int dtype
   return STRAGGLAR_OK;
 }
 
-int stragglar_plan_e2e_pieces(size_t count, int dtype, size_t piece_bytes, int ramp, size_t* out, int max_pieces,
+int stragglar_plan_e2e_pieces(size_t count, int dtype, size_t piece_bytes, size_t* out, int max_pieces,
                               int* n_pieces) {
   if (!out || !n_pieces || max_pieces < 0) return STRAGGLAR_ERR_INVALID_ARG;
   const int es = esize_of(dtype);
   if (!es) return STRAGGLAR_ERR_UNSUPPORTED;
-  const std::vector<uint64_t> lens = e2e_pieces(count, es, piece_bytes, ramp != 0);
+  const std::vector<uint64_t> lens = e2e_pieces(count, es, piece_bytes);
   if (lens.size() > (size_t)max_pieces) return STRAGGLAR_ERR_INVALID_ARG;
   for (size_t i = 0; i < lens.size(); ++i) out[i] = lens[i];
   *n_pieces = (int)lens.size();
@@ -1662,7 +1639,7 @@ int stragglar_team_allreduce_host(const void* const* host_in, void* const* host_
   const int es = esize_of(dtype);
   std::vector<void*> sub(world);
   return e2e_pipeline(world, host_in, host_out, bufs, count, es, (cudaStream_t)stream, g_team.e2e_piece_bytes,
-                      g_team.e2e_ramp, g_team.e2e_streams, [&](uint64_t off, uint64_t n) {
+                      g_team.e2e_streams, [&](uint64_t off, uint64_t n) {
                         for (int p = 0; p < world; ++p) sub[p] = (char*)bufs[p] + off * es;
                         return stragglar_team_allreduce(sub.data(), n, dtype, op, stream);
                       });
@@ -1672,7 +1649,7 @@ int stragglar_allreduce_host(const void* host_in, void* host_out, void* buf, siz
                              void* stream) {
   int st;
   uint64_t piece;
-  int ramp, ncs;
+  int ncs;
   {
     std::lock_guard<std::mutex> lk(g_mu);
     Comm& c = g_proc;
@@ -1683,14 +1660,13 @@ int stragglar_allreduce_host(const void* host_in, void* host_out, void* buf, siz
     LaunchPlan P;
     if ((st = proc_plan(buf, count, dtype, &P))) return st;   // the whole range must be registered
     piece = c.e2e_piece_bytes;
-    ramp = c.e2e_ramp;
     ncs = c.e2e_streams;
   }
   const int es = esize_of(dtype);
   const void* hin[1] = {host_in};
   void* hout[1] = {host_out};
   void* b[1] = {buf};
-  return e2e_pipeline(1, hin, hout, b, count, es, (cudaStream_t)stream, piece, ramp, ncs, [&](uint64_t off, uint64_t n) {
+  return e2e_pipeline(1, hin, hout, b, count, es, (cudaStream_t)stream, piece, ncs, [&](uint64_t off, uint64_t n) {
     return stragglar_allreduce((char*)buf + off * es, n, dtype, op, stream);
   });
 }

@@ -49,7 +49,7 @@ _SIGS = {
     "stragglar_schedule_round": ([_c_int, _c_int, ctypes.POINTER(_c_int), _c_int, ctypes.POINTER(_c_int)], _c_int),
     "stragglar_plan_layout": ([_c_int, _c_int, _c_size, _c_int, _c_int, _c_int, ctypes.POINTER(_c_int),
                                ctypes.POINTER(_c_int), ctypes.POINTER(_c_int)], _c_int),
-    "stragglar_plan_e2e_pieces": ([_c_size, _c_int, _c_size, _c_int, ctypes.POINTER(_c_size), _c_int,
+    "stragglar_plan_e2e_pieces": ([_c_size, _c_int, _c_size, ctypes.POINTER(_c_size), _c_int,
                                    ctypes.POINTER(_c_int)], _c_int),
     "stragglar_init": ([_c_int, _c_int, _c_int], _c_int),
     "stragglar_handle_size": ([ctypes.POINTER(_c_size)], _c_int),
@@ -206,13 +206,13 @@ def stragglar_plan_layout(world: int, straggler_rank: int, count: int, dtype_cod
     return g.value, sub.value, lanes.value
 
 
-def stragglar_plan_e2e_pieces(count: int, dtype_code: int, piece_bytes: int, ramp: bool = True):
+def stragglar_plan_e2e_pieces(count: int, dtype_code: int, piece_bytes: int):
     """-> element counts of the pieces the host-buffer entry points cut `count` into (host only)."""
-    cap = 64 + int(count) // max(1, int(piece_bytes) // 8) + 8
+    cap = 8 + int(count) // max(1, int(piece_bytes) // 4 // 4 * 4)
     out = (_c_size * cap)()
     k = _c_int(0)
     _ck("stragglar_plan_e2e_pieces", _lib.stragglar_plan_e2e_pieces(int(count), dtype_code, int(piece_bytes),
-                                                                    1 if ramp else 0, out, cap, ctypes.byref(k)))
+                                                                    out, cap, ctypes.byref(k)))
     return list(out[:k.value])
 
 

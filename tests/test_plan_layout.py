@@ -94,35 +94,24 @@ def test_layout_rejects_bad_arguments(S):
         S.stragglar_plan_layout(8, 0, 100, 7, 74)
 
 
+
 @pytest.mark.parametrize("dtype", [0, 1, 2])
-@pytest.mark.parametrize("piece", [16, 4096, 100_000, 8 << 20])
+@pytest.mark.parametrize("piece", [1, 16, 4096, 100_000, 8 << 20])
 @pytest.mark.parametrize("count", [0, 1, 7, 8, 1000, 65_539, 1 << 20, (1 << 26) + 3])
-@pytest.mark.parametrize("ramp", [False, True])
-def test_e2e_pieces(S, dtype, piece, count, ramp):
-    """The host-buffer pipeline's pieces: they tile [0, count) in order, every
-    piece but the last starts and ends 16-byte aligned (the kernels' vector
-    rule), none exceeds the steady piece, and with the ramp the first and last
-    pieces are 1/8 of it (fill / drain), growing and shrinking by doubling."""
+def test_e2e_pieces(S, dtype, piece, count):
+    """The host-buffer pipeline's pieces (one collective call each, so every
+    rank must cut the same ones): they tile [0, count) in order, every piece
+    but the last has the piece size rounded down to the kernels' 16-byte
+    vector (at least one vector), the last takes the rest."""
     esz = ESZ[dtype]
     v = 16 // esz
-    lens = S.stragglar_plan_e2e_pieces(count, dtype, piece, ramp)
-    assert sum(lens) == count and all(n > 0 for n in lens)
+    lens = S.stragglar_plan_e2e_pieces(count, dtype, piece)
     steady = max(v, piece // esz // v * v)
-    assert all(n % v == 0 for n in lens[:-1])
-    assert all(n <= steady for n in lens)
-    if not ramp or steady < 8 * v:
-        assert all(n == steady for n in lens[:-1])
-        return
-    q = [steady // d // v * v for d in (8, 4, 2)]
-    if count >= 2 * steady + 2 * sum(q):
-        assert lens[:3] == q and lens[3] == steady
-        assert lens[-3:-1] == [q[2], q[1]] and 0 < lens[-1] <= q[0]
-        assert len(lens) <= count // steady + 8
+    assert sum(lens) == count and all(n > 0 for n in lens)
+    assert lens[:-1] == [steady] * (len(lens) - 1)
+    assert len(lens) == -(-count // steady)
 
 
 def test_e2e_pieces_config2(S):
-    """Config 2's host pipeline (256 MiB fp32 per rank, 8 MiB pieces): 1, 2, 4 MiB up,
-    30 whole pieces and the 2 MiB remainder, 4, 2, 1 MiB down."""
-    M = (1 << 20) // 4
-    lens = S.stragglar_plan_e2e_pieces(1 << 26, 1, 8 << 20)
-    assert lens == [M, 2 * M, 4 * M] + [8 * M] * 30 + [2 * M] + [4 * M, 2 * M, M]
+    """Config 2's host pipeline: 256 MiB fp32 per rank in 32 pieces of 8 MiB."""
+    assert S.stragglar_plan_e2e_pieces(1 << 26, 1, 8 << 20) == [(8 << 20) // 4] * 32
