@@ -395,6 +395,7 @@ def bench_team(args):
             "world": world, "straggler_rank": sigma, "count": count, "buffer_bytes": S_bytes,
             "slices_per_rank": G, "delay_us": D_ns / 1e3,
             "mover": os.environ.get("STRAGGLAR_MOVER", "default"),
+            "unit_order": "op-major" if os.environ.get("STRAGGLAR_SUB_MAJOR", "1") == "0" else "sub-slice-major",
             "l2": "inputs (8 x 256 MiB) exceed the 126 MB L2; buffers reduced in place step after step",
             "parallelism": "team8-on-1gpu",
         },
@@ -435,7 +436,11 @@ def bench_team(args):
         "ring_hbm_GBps": round(bytes_ring / (T_ring * 1e-6) / 1e9, 1),
         "roofline": {"bound": "hbm", "kernel": "k_phase<..., KIND=1> (Phase B, Algorithm 1 schedule)", "achieved": round(achieved, 1),
                      "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 3), "traffic": traffic,
-                     "algorithmic_bytes": bytes_B, "peak_source": peak_src},
+                     "algorithmic_bytes": bytes_B, "peak_source": peak_src,
+                     "dram_GBps": round(traffic / (T_post * 1e-6) / 1e9, 1) if traffic else None,
+                     "dram_frac": round(traffic / (T_post * 1e-6) / 1e9 / peak, 3) if traffic else None,
+                     "note": "achieved = algorithmic bytes / time; above the copy peak when L2 serves part of "
+                             "the forwarded reads (traffic < algorithmic bytes); dram_* = ncu DRAM bytes / time"},
         "cpu_baseline": cpu,
         "e2e": {"value": round(E2E, 1), "unit": "us", "pcie_floor_us": round(pcie_floor, 1),
                 "frac_of_pcie_floor": round(pcie_floor / E2E, 3), "h2d_bytes_per_step": world * S_bytes,

@@ -406,7 +406,12 @@ int stragglar_allreduce_auto(void* buf, size_t count, int dtype, int op, void* s
  * STRAGGLAR_SUBSLICES (slices per CTA at most, 1..16; default 16) and
  * STRAGGLAR_SUBSLICE_BYTES (their target size on large messages, 131072: each
  * hop hands over ~128 KB pieces, so a forwarded slice is still in L2 when
- * the next hop reads it),
+ * the next hop reads it), STRAGGLAR_BASELINE_SUBSLICE_BYTES (the same for
+ * the Ring and RHD baselines, tuned for them: 65536 with GPU-scope flags,
+ * 131072 at system scope), STRAGGLAR_SUB_MAJOR (1: a CTA runs its units
+ * sub-slice by sub-slice — all ops / steps of sub-slice 0, then of 1, … — in
+ * Phase B, the Ring and RHD, so forwarded data is re-read while it is still in
+ * L2; 0: op by op; must agree across ranks),
  * STRAGGLAR_OP_LANES (Phase-B op lanes per slice at most, 16; 1 = off),
  * STRAGGLAR_LANE_SLICE_MAX (slices may grow to this many bytes to make room
  * for op lanes on small messages, 32768; 0 = off), STRAGGLAR_RS_WHOLE (Phase A

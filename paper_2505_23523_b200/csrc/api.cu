@@ -47,8 +47,9 @@ std::atomic<uint64_t> g_launches{0};
 // they travel in the flag-array blob and stragglar_import_handles rejects a
 // mismatch instead of running with silently different slice layouts.
 struct Layout {
-  int32_t world, sigma, G_alloc, sub_max, mover, sys_scope, lanes_max, pad;
+  int32_t world, sigma, G_alloc, sub_max, mover, sys_scope, lanes_max, sub_major;
   uint64_t slice_bytes, sub_bytes, lane_slice_max, e2e_piece_bytes;   // e2e: every rank must cut the same pieces
+  uint64_t base_sub_bytes;
 };
 
 struct IpcBlob {          // what travels between processes, per rank
@@ -76,8 +77,10 @@ struct Comm {
   int G_alloc = 0;             // CTAs per rank the flag array was sized for (fixes the flag stride)
   int sub = 1;                 // slices per CTA at most (STRAGGLAR_SUBSLICES)
   uint64_t sub_bytes = 0;      // target slice size on large messages (STRAGGLAR_SUBSLICE_BYTES)
+  uint64_t base_sub_bytes = 0; // the same for the Ring / RHD baselines (STRAGGLAR_BASELINE_SUBSLICE_BYTES)
   int lanes_max = kMaxOps;     // Phase-B op lanes per slice at most (STRAGGLAR_OP_LANES; 1 = off)
   int rs_whole = 1;                 // Phase A over a CTA's sub slices as one range (STRAGGLAR_RS_WHOLE)
+  int sub_major = 1;                // unit order of Phase B, Ring, RHD (STRAGGLAR_SUB_MAJOR; plan.h LaunchPlan::sub_major)
   uint64_t lane_slice_max = 32768;  // slices may grow to this size to make room for op lanes
                                     // (STRAGGLAR_LANE_SLICE_MAX; 0 = keep slice_bytes)
   bool rs_pending = false;     // team: a Phase A awaits its Phase B (same call epoch)
@@ -220,6 +223,10 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   c.timeout_ns = env_u64("STRAGGLAR_TIMEOUT_MS", 10000) * 1000000ull;
   c.slice_bytes = env_u64("STRAGGLAR_SLICE_BYTES", 16384);
   c.sys_scope = team ? (int)env_u64("STRAGGLAR_SYS_SCOPE", 0) : 1;
+  // the baselines' own sub-slice target, tuned for them like ours (sub-slice-major
+  // order, profiles/r02/ab/r02aa_*): Ring 1286 -> 1091 us, RHD 1386 -> 1292 us at
+  // 64 KB with GPU-scope flags (config 2); 128 KB at system scope (Ring 1369 vs 1332)
+  c.base_sub_bytes = env_u64("STRAGGLAR_BASELINE_SUBSLICE_BYTES", c.sys_scope ? 128 * 1024 : 64 * 1024);
   // Sub-slices (finer hand-offs): team Phase B -3.7 % at gpu scope; at system
   // scope (per process, MPS-shared GPU, round 2) equal or better for T_post
   // (config 2 n = 8: 667-708 vs 715-716 us) and 10 % better for the Ring, once
@@ -231,6 +238,7 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   if (c.sub > kMaxSub) c.sub = kMaxSub;
   c.lane_slice_max = env_u64("STRAGGLAR_LANE_SLICE_MAX", 32768);
   c.rs_whole = (int)env_u64("STRAGGLAR_RS_WHOLE", 1) ? 1 : 0;
+  c.sub_major = (int)env_u64("STRAGGLAR_SUB_MAJOR", 1) ? 1 : 0;
   c.lanes_max = (int)env_u64("STRAGGLAR_OP_LANES", kMaxOps);
   if (c.lanes_max < 1) c.lanes_max = 1;
   c.e2e_piece_bytes = env_u64("STRAGGLAR_E2E_PIECE_BYTES", 8ull << 20);
@@ -283,7 +291,9 @@ Layout layout_of(const Comm& c) {
   l.lane_slice_max = c.lane_slice_max;
   l.slice_bytes = c.slice_bytes;
   l.sub_bytes = c.sub_bytes;
+  l.base_sub_bytes = c.base_sub_bytes;
   l.e2e_piece_bytes = c.e2e_piece_bytes;
+  l.sub_major = c.sub_major;
   return l;
 }
 
@@ -317,7 +327,7 @@ void common_finalize(Comm& c) {
 // covering up to `sub` slices.  Any (G, sub) is safe call to call: flags hold
 // monotone epochs, so values left at other positions by earlier calls are
 // stale (< epoch); within a call every kernel uses the same layout.
-void slices_for(const Comm& c, uint64_t chunk_bytes, int* G, int* sub) {
+void slices_for(const Comm& c, uint64_t chunk_bytes, int* G, int* sub, bool baseline = false) {
   const uint64_t per = c.slice_bytes;
   uint64_t g = per ? (chunk_bytes + per - 1) / per : (uint64_t)c.G * c.sub;
   if (g < 1) g = 1;
@@ -328,7 +338,7 @@ void slices_for(const Comm& c, uint64_t chunk_bytes, int* G, int* sub) {
   }
   // large messages: each CTA covers ~chunk/(G*sub_bytes) slices of about
   // sub_bytes (rounded; 1 if sub_bytes is 0)
-  const uint64_t unit = (uint64_t)c.G * c.sub_bytes;
+  const uint64_t unit = (uint64_t)c.G * (baseline ? c.base_sub_bytes : c.sub_bytes);
   uint64_t m = unit ? (chunk_bytes + unit / 2) / unit : 1;
   if (m < 1) m = 1;
   if (m > (uint64_t)c.sub) m = c.sub;
@@ -383,6 +393,7 @@ LaunchPlan base_plan(const Comm& c, size_t count, int dtype, bool last_kernel) {
   P.host_err = c.host_err_dev;
   P.lanes = 1;
   P.rs_whole = c.rs_whole;
+  P.sub_major = c.sub_major;
   P.bc_partner = c.progs.bc_partner;
   for (int p = 0; p < c.world; ++p) {
     P.flags[p] = c.peer_flags[p];
@@ -948,7 +959,7 @@ int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* s
   if ((st = proc_plan(buf, count, dtype, &P))) return st;
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
-  slices_for(c, P.ce * P.esize, &P.G, &P.sub);
+  slices_for(c, P.ce * P.esize, &P.G, &P.sub, true);
   return launch(K_RING, dtype, P, P.G, stream);
 }
 
@@ -963,7 +974,7 @@ int stragglar_allreduce_rhd(void* buf, size_t count, int dtype, int op, void* st
   if ((st = proc_plan(buf, count, dtype, &P))) return st;
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
-  slices_for(c, P.ce * P.esize, &P.G, &P.sub);
+  slices_for(c, P.ce * P.esize, &P.G, &P.sub, true);
   return launch(K_RHD, dtype, P, P.G, stream);
 }
 
@@ -1548,7 +1559,7 @@ int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, in
   LaunchPlan P = base_plan(c, count, dtype, true);
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
-  slices_for(c, P.ce * P.esize, &P.G, &P.sub);
+  slices_for(c, P.ce * P.esize, &P.G, &P.sub, true);
   for (int p = 0; p < c.world; ++p) {
     P.buf[p] = (char*)bufs[p];
     P.local_rank[p] = p;
@@ -1567,7 +1578,7 @@ int stragglar_team_allreduce_rhd(void* const* bufs, size_t count, int dtype, int
   LaunchPlan P = base_plan(c, count, dtype, true);
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
-  slices_for(c, P.ce * P.esize, &P.G, &P.sub);
+  slices_for(c, P.ce * P.esize, &P.G, &P.sub, true);
   for (int p = 0; p < c.world; ++p) {
     P.buf[p] = (char*)bufs[p];
     P.local_rank[p] = p;

@@ -781,11 +781,17 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
     return -1;
   };
   bool ok = true;
-  for (int k = q; k < nops && ok; k += lanes) {
+  // the CTA's units (op k, sub-slice j): op by op (all sub-slices of an op,
+  // then the next op), or with P.sub_major sub-slice by sub-slice
+  const int nk = (nops - q + lanes - 1) / lanes;   // this lane's ops: k = q, q + lanes, ...
+  int ki = 0, j = 0;   // this unit's op index (k = q + ki * lanes) and sub-slice
+  for (int u = 0; u < nk * P.sub && ok;
+       ++u, P.sub_major ? (++ki == nk ? (ki = 0, ++j) : 0) : (++j == P.sub ? (j = 0, ++ki) : 0)) {
+    const int k = q + ki * lanes;
     const Op op = P.ops[me][k];
     const int c = op.chunk, peer = op.peer;
     const Range cr = chunk_range(P, c);
-    for (int j = 0; j < P.sub && ok; ++j) {
+    {
       const int v = s * P.sub + j;
       const Range sl = slice_of(cr.lo, cr.hi, v, NV, V);
       // optional trace: per op and slice, when the wait began, data movement began, it was signalled
@@ -982,10 +988,15 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_ring(const __grid_cons
   Pipe pipe = make_pipe(tma);
   char* mine = P.buf[j];
   const char* lbuf = P.buf[left];
+  // with P.sub_major the CTA runs all steps of sub-slice 0, then of 1, ... (a
+  // pipelined ring: the same per-slice dependencies, forwarded slices re-read
+  // sooner), otherwise step by step over all its sub-slices
+  const int nouter = P.sub_major ? P.sub : 1, ninner = P.sub_major ? 1 : P.sub;
+  for (int qo = 0; qo < nouter; ++qo)
   for (int t = 0; t < 2 * (W - 1); ++t) {
     const int k = (t < W - 1) ? ((j - 1 - t) % W + 2 * W) % W : ((j - t + W - 1) % W + 2 * W) % W;
     const Range cr = chunk_range(P, k);
-    for (int q = 0; q < P.sub; ++q) {
+    for (int q = qo; q < qo + ninner; ++q) {
       const int v = s * P.sub + q;
       // step 0 waits for the left neighbour's arrival (per CTA), step t for its step t-1 on slice v
       const uint32_t* wf = (t == 0) ? flag_at(P.flags[j], SLOT_RING_ARRIVE, P.fstride, s)
@@ -1043,8 +1054,11 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_rhd(const __grid_const
   if (threadIdx.x == 0) st_release(flag_at(P.flags[partner(0)], SLOT_RHD_READY, P.fstride, s), ep, P.sys_scope);
   Pipe pipe = make_pipe(MV == MOVER_TMA);
   char* mine = P.buf[j];
-  int blo = 0, m = W;   // the block of chunks j works on
   bool ok = true;
+  // with P.sub_major all steps of sub-slice 0, then of 1, ... (as in k_ring)
+  const int nouter = P.sub_major ? P.sub : 1, ninner = P.sub_major ? 1 : P.sub;
+  for (int qo = 0; qo < nouter && ok; ++qo) {
+  int blo = 0, m = W;   // the block of chunks j works on
   for (int tau = 0; tau < 2 * L && ok; ++tau) {
     const int p = partner(tau);
     const char* pbuf = P.buf[p];
@@ -1058,7 +1072,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_rhd(const __grid_const
       clo = blo ^ m;    // the partner's block (aligned siblings)
       cn = m;
     }
-    for (int q = 0; q < P.sub; ++q) {
+    for (int q = qo; q < qo + ninner; ++q) {
       const int v = s * P.sub + q;
       const uint32_t* wf = flag_at(P.flags[j], SLOT_RHD_READY + tau, P.fstride, tau == 0 ? s : v);
       if (!(ok = cta_wait(wf, ep, P, 0xE00 | tau))) break;
@@ -1081,6 +1095,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) k_rhd(const __grid_const
       blo = blo < clo ? blo : clo;
       m *= 2;
     }
+  }
   }
   // every AllGather partner finished reading my buffer (one waiting thread per flag)
   if (ok && (int)threadIdx.x < L * P.sub) {

@@ -85,7 +85,9 @@ struct LaunchPlan {
   char* buf[kMaxWorld];      // data buffer of each physical rank (local or peer mapping)
   uint32_t* flags[kMaxWorld];// flag array of each physical rank
   int last_kernel;            // 1: the call's final kernel; its last CTA to exit bumps state->epoch
-  uint32_t pad0;
+  int sub_major;             // Phase B: a CTA walks its (op, sub-slice) units sub-slice by sub-slice
+                             // (all ops of sub-slice 0, then of 1, ...) instead of op by op; must agree
+                             // across ranks (a mixed order can deadlock), so it is a layout knob
   uint64_t count;            // elements
   uint64_t ce;               // elements per chunk (chunks start at j*ce)
   int nchunks;

@@ -1,6 +1,8 @@
 """ranks whose layout knobs differ must not run with silently
-different slice layouts.  Rank 1 sets another sub-slice size; importing the
-handles must fail with INVALID_ARG on every rank.  Launched by
+different slice layouts.  Rank 1 sets another value of one knob (argv[2]=argv[3]:
+the sub-slice size, the Phase-B unit order — a mixed order can deadlock —, or
+the host pipeline's piece size); importing the handles must fail with
+INVALID_ARG on every rank.  Launched by
 tests/test_gpu_multiproc.py.  Exit 0 = behaved as specified."""
 import os
 import sys
@@ -13,9 +15,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def worker(rank, port, q):
+def worker(rank, port, q, knob, value):
     if rank == 1:
-        os.environ["STRAGGLAR_SUBSLICE_BYTES"] = "4096"
+        os.environ[knob] = value
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=2)
     torch.cuda.set_device(0)
     from paper_2505_23523_b200 import stragglar as S
@@ -33,9 +35,10 @@ def worker(rank, port, q):
 
 if __name__ == "__main__":
     port = int(sys.argv[1])
+    knob, value = (sys.argv[2], sys.argv[3]) if len(sys.argv) > 3 else ("STRAGGLAR_SUBSLICE_BYTES", "4096")
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=worker, args=(r, port, q)) for r in range(2)]
+    ps = [ctx.Process(target=worker, args=(r, port, q, knob, value)) for r in range(2)]
     for p in ps:
         p.start()
     out = dict(q.get(timeout=300) for _ in range(2))

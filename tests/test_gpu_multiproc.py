@@ -78,15 +78,18 @@ def test_ddp_comm_hook(world, sigma, mode):
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
 
 
-def test_layout_mismatch_rejected_at_import():
+@pytest.mark.parametrize("knob,value", [("STRAGGLAR_SUBSLICE_BYTES", "4096"), ("STRAGGLAR_SUB_MAJOR", "0"),
+                                         ("STRAGGLAR_E2E_PIECE_BYTES", "65536")])
+def test_layout_mismatch_rejected_at_import(knob, value):
     """Ranks with different layout knobs fail at stragglar_import_handles
-    (INVALID_ARG) instead of running with different slice layouts."""
+    (INVALID_ARG) instead of running with different slice layouts, unit
+    orders or host-pipeline pieces."""
     if not torch.cuda.is_available():
         pytest.skip("no GPU")
     import __graft_entry__
 
     __graft_entry__.build()
-    r = subprocess.run([sys.executable, os.path.join(HERE, "mp_layout_mismatch.py"), str(_port())],
+    r = subprocess.run([sys.executable, os.path.join(HERE, "mp_layout_mismatch.py"), str(_port()), knob, value],
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
 
