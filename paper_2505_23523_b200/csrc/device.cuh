@@ -246,6 +246,51 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uin
                "r"(bytes)
                : "memory");
 }
+// L2 residency by data lifetime (Phase B, STRAGGLAR_LIFETIME_HINTS=1): a copy
+// that is read again later in the call (kernels.cuh, Op::life) keeps the
+// default policy above (evict_last); dead data gets STRAGGLAR_DEAD_HINT
+// (1 = evict_first, 0 = no hint) so it does not crowd the forwarded slices out.
+#ifndef STRAGGLAR_LIFETIME_HINTS
+#define STRAGGLAR_LIFETIME_HINTS 0
+#endif
+#ifndef STRAGGLAR_DEAD_HINT
+#define STRAGGLAR_DEAD_HINT 1
+#endif
+__device__ __forceinline__ void bulk_load_life(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                               bool keep) {
+#if STRAGGLAR_LIFETIME_HINTS && STRAGGLAR_DEAD_HINT
+  if (!keep) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(l2_policy<1>())
+        : "memory");
+    return;
+  }
+#elif STRAGGLAR_LIFETIME_HINTS
+  if (!keep) {
+    bulk_load<false>(smem_dst, gsrc, bytes, bar);
+    return;
+  }
+#endif
+  bulk_load<true>(smem_dst, gsrc, bytes, bar);
+}
+__device__ __forceinline__ void bulk_store_life(void* gdst, const void* smem_src, uint32_t bytes, bool keep) {
+#if STRAGGLAR_LIFETIME_HINTS && STRAGGLAR_DEAD_HINT
+  if (!keep) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+                 "r"(smem_u32(smem_src)), "r"(bytes), "l"(l2_policy<1>())
+                 : "memory");
+    return;
+  }
+#elif STRAGGLAR_LIFETIME_HINTS
+  if (!keep) {
+    bulk_store<false>(gdst, smem_src, bytes);
+    return;
+  }
+#endif
+  bulk_store<true>(gdst, smem_src, bytes);
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }

@@ -288,8 +288,10 @@ __device__ __forceinline__ uint32_t advance_phase(uint32_t ph, uint32_t np) {
   return ph;
 }
 
-// dst <- src, nbytes a multiple of 16
-static __device__ void tma_copy(Pipe& p, char* dst, const char* src, uint64_t nbytes) {
+// dst <- src, nbytes a multiple of 16.  ld_keep / st_keep: the source / the
+// destination copy is read again later (L2 hints, STRAGGLAR_LIFETIME_HINTS).
+static __device__ void tma_copy(Pipe& p, char* dst, const char* src, uint64_t nbytes, bool ld_keep = true,
+                                bool st_keep = true) {
   const uint32_t np = (uint32_t)((nbytes + kStageBytes - 1) / kStageBytes);
   if (threadIdx.x == 0 && np) {
     fence_proxy_async_global();
@@ -298,7 +300,7 @@ static __device__ void tma_copy(Pipe& p, char* dst, const char* src, uint64_t nb
       const uint64_t off = (uint64_t)i * kStageBytes;
       const uint32_t len = (uint32_t)((nbytes - off) < kStageBytes ? (nbytes - off) : kStageBytes);
       mbar_expect_tx(&p.bar[s], len);
-      bulk_load(p.buf(s), src + off, len, &p.bar[s]);
+      bulk_load_life(p.buf(s), src + off, len, &p.bar[s], ld_keep);
     };
     for (uint32_t i = 0; i < np && i < (uint32_t)kAhead; ++i) issue(i);
     uint32_t ph = p.phase;
@@ -308,7 +310,7 @@ static __device__ void tma_copy(Pipe& p, char* dst, const char* src, uint64_t nb
       ph ^= 1u << s;
       const uint64_t off = (uint64_t)i * kStageBytes;
       const uint32_t len = (uint32_t)((nbytes - off) < kStageBytes ? (nbytes - off) : kStageBytes);
-      bulk_store(dst + off, p.buf(s), len);
+      bulk_store_life(dst + off, p.buf(s), len, st_keep);
       bulk_commit();
       if (i + kAhead < np) {
         ring_release_wait();
@@ -323,7 +325,8 @@ static __device__ void tma_copy(Pipe& p, char* dst, const char* src, uint64_t nb
 
 // d0 = d1 = a (+) b through shared memory, nbytes a multiple of 16
 template <int DT>
-__device__ void tma_add2(Pipe& p, char* d0, char* d1, const char* a, const char* b, uint64_t nbytes) {
+__device__ void tma_add2(Pipe& p, char* d0, char* d1, const char* a, const char* b, uint64_t nbytes,
+                         bool ld_keep = true, bool st0_keep = true, bool st1_keep = true) {
   constexpr uint32_t kPiece = kStageBytes / 2;
   const uint32_t np = (uint32_t)((nbytes + kPiece - 1) / kPiece);
   auto piece_len = [&](uint32_t i) -> uint32_t {
@@ -335,8 +338,8 @@ __device__ void tma_add2(Pipe& p, char* d0, char* d1, const char* a, const char*
     const uint64_t off = (uint64_t)i * kPiece;
     const uint32_t len = piece_len(i);
     mbar_expect_tx(&p.bar[s], 2 * len);
-    bulk_load(p.buf(s), a + off, len, &p.bar[s]);
-    bulk_load(p.buf(s) + kPiece, b + off, len, &p.bar[s]);
+    bulk_load_life(p.buf(s), a + off, len, &p.bar[s], ld_keep);
+    bulk_load_life(p.buf(s) + kPiece, b + off, len, &p.bar[s], ld_keep);
   };
   if (threadIdx.x == 0 && np) {
     fence_proxy_async_global();
@@ -355,8 +358,8 @@ __device__ void tma_add2(Pipe& p, char* d0, char* d1, const char* a, const char*
     __syncthreads();
     if (threadIdx.x == 0) {
       const uint64_t off = (uint64_t)i * kPiece;
-      bulk_store(d0 + off, A, len);
-      if (d1) bulk_store(d1 + off, A, len);
+      bulk_store_life(d0 + off, A, len, st0_keep);
+      if (d1) bulk_store_life(d1 + off, A, len, st1_keep);
       bulk_commit();
       if (i + kAhead < np) {
         ring_release_wait();
@@ -767,6 +770,7 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
   const int V = 16 / P.esize;
   const int lanes = P.lanes;
   constexpr bool tma = MV == MOVER_TMA;
+  constexpr bool kLife = STRAGGLAR_LIFETIME_HINTS != 0;   // L2 hints by data lifetime (Op::life)
   // the straggler reaches barrier (2): announce per CTA slot to the others
   if (q == 0 && me == P.sigma && threadIdx.x < W && (int)threadIdx.x != me)
     st_release(flag_at(P.flags[threadIdx.x], SLOT_ARRIVE + me, P.fstride, s), ep, P.sys_scope);
@@ -809,7 +813,8 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
         if (tr) tr[1] = globaltimer();
         const uint64_t a = sl.lo * P.esize, b = mid * P.esize, body = (b - a) / 16 * 16;
         if constexpr (tma)
-          tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, body);
+          tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, body, !kLife,
+                       !kLife || (op.life & LIFE_SELF_REREAD), !kLife || (op.life & LIFE_PEER_REREAD));
         else
           add2_vecs<DT>(mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, body / 16);
         add2_tail<DT>(mine + a + body, P.buf[peer] + a + body, mine + a + body, P.buf[peer] + a + body,
@@ -824,7 +829,8 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
         if (tr) tr[1] = globaltimer();
         const uint64_t a = mid * P.esize, b = sl.hi * P.esize, body = (b - a) / 16 * 16;
         if constexpr (tma)
-          tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, body);
+          tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, body, !kLife,
+                       !kLife || (op.life & LIFE_SELF_REREAD), !kLife || (op.life & LIFE_PEER_REREAD));
         else
           add2_vecs<DT>(mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, body / 16);
         add2_tail<DT>(mine + a + body, P.buf[peer] + a + body, P.buf[peer] + a + body, mine + a + body,
@@ -841,7 +847,8 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
         if (tr) tr[1] = globaltimer();
         const uint64_t a = sl.lo * P.esize, b = sl.hi * P.esize, body = (b - a) / 16 * 16;
         if constexpr (tma)
-          tma_copy(pipe, P.buf[peer] + a, mine + a, body);
+          tma_copy(pipe, P.buf[peer] + a, mine + a, body, !kLife || (op.life & LIFE_SRC_REREAD),
+                   !kLife || (op.life & LIFE_PEER_REREAD));
         else
           copy_vecs(P.buf[peer] + a, mine + a, body / 16);
         copy_tail(P.buf[peer] + a + body, mine + a + body, (int)((b - a) % 16));

@@ -289,6 +289,24 @@ RankPrograms build_programs(int n, int sigma_phys) {
       pr.ops[pa][pr.nops[pa]++] = op;
     }
   }
+  // data lifetimes for the L2 hints: a stored copy is re-read iff its holder
+  // later sends that chunk; a SEND's source iff this rank sends it once more
+  auto sends_chunk = [&](int p, int c, int after) {
+    for (int k = after + 1; k < pr.nops[p]; ++k)
+      if (pr.ops[p][k].kind == OP_SEND && pr.ops[p][k].chunk == c) return true;
+    return false;
+  };
+  for (int p = 0; p < n; ++p)
+    for (int k = 0; k < pr.nops[p]; ++k) {
+      Op& o = pr.ops[p][k];
+      o.life = 0;
+      if (sends_chunk(o.peer, o.chunk, -1)) o.life |= LIFE_PEER_REREAD;
+      if (o.kind == OP_SEND) {
+        if (sends_chunk(p, o.chunk, k)) o.life |= LIFE_SRC_REREAD;
+      } else if (sends_chunk(p, o.chunk, k)) {
+        o.life |= LIFE_SELF_REREAD;
+      }
+    }
   int snd[kMaxWorld], rnd[kMaxWorld];
   broadcast_tree(n, snd, rnd);
   pr.bc_partner = pr.phys_of_logical[0];

@@ -26,8 +26,14 @@ enum OpKind : uint8_t {
   OP_EXCH_HIGH = 2,  // straggler side of the c_r exchange: second half of every slice
   OP_SEND = 3        // push a fully reduced chunk to `peer`
 };
+// Op::life: which copies of the op's data are read again later in Phase B
+// (L2 residency hints, kernels.cuh): the source of a SEND (this rank sends the
+// chunk again), the peer's copy (the peer forwards the chunk), this rank's
+// stored copy of an exchange (this rank forwards the chunk).
+enum OpLife : uint8_t { LIFE_SRC_REREAD = 1, LIFE_PEER_REREAD = 2, LIFE_SELF_REREAD = 4 };
 struct Op {
   uint8_t kind, chunk, peer, round;  // peer is a PHYSICAL rank
+  uint8_t life;                      // OpLife bits
 };
 
 constexpr int kMaxWorld = 8;

@@ -42,7 +42,17 @@ VARIANTS_DEFER = {   # round 2 (r02v): the deferred SEND hand-off (since removed
     "diag_fence_gpu": ["STRAGGLAR_DIAG_FENCE_GPU=1"],
     "diag_acq_gpu": ["STRAGGLAR_DIAG_ACQ_GPU=1"],
 }
-VARIANTS = (VARIANTS_DEFER if "--defer" in sys.argv else VARIANTS_LL if "--ll" in sys.argv else VARIANTS_LAG if "--lag" in sys.argv
+VARIANTS_HINT3 = {   # round 2: load / store L2 hints again, with the sub-slice-major order
+    "ld_ef": ["STRAGGLAR_LOAD_HINT=1"],
+    "ld_none": ["STRAGGLAR_LOAD_HINT=0"],
+    "st_none": ["STRAGGLAR_STORE_HINT=0"],
+    "ld_ef_st_none": ["STRAGGLAR_LOAD_HINT=1", "STRAGGLAR_STORE_HINT=0"],
+}
+VARIANTS_LIFE = {   # round 2: L2 hints by data lifetime (Op::life), dead data evict_first / no hint
+    "life_ef": ["STRAGGLAR_LIFETIME_HINTS=1", "STRAGGLAR_DEAD_HINT=1"],
+    "life_none": ["STRAGGLAR_LIFETIME_HINTS=1", "STRAGGLAR_DEAD_HINT=0"],
+}
+VARIANTS = (VARIANTS_LIFE if "--life" in sys.argv else VARIANTS_HINT3 if "--hint3" in sys.argv else VARIANTS_DEFER if "--defer" in sys.argv else VARIANTS_LL if "--ll" in sys.argv else VARIANTS_LAG if "--lag" in sys.argv
             else VARIANTS_HINT if ("--hint" in sys.argv or "--hint2" in sys.argv) else VARIANTS_ALL)
 os.makedirs(os.path.join(ROOT, "build", "variants"), exist_ok=True)
 with ThreadPoolExecutor(4) as ex:
