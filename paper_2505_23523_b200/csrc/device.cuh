@@ -250,8 +250,11 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uin
 // that is read again later in the call (kernels.cuh, Op::life) keeps the
 // default policy above (evict_last); dead data gets STRAGGLAR_DEAD_HINT
 // (1 = evict_first, 0 = no hint) so it does not crowd the forwarded slices out.
+// Measured with the sub-slice-major order (profiles/r02/ab/r02ac_*): config-2
+// Phase B 570 -> 541 us, DRAM reads 1.16 -> 0.62 GB (the floor is 0.54 GB:
+// x_sigma and the partials); no hint on dead data: 566 us.
 #ifndef STRAGGLAR_LIFETIME_HINTS
-#define STRAGGLAR_LIFETIME_HINTS 0
+#define STRAGGLAR_LIFETIME_HINTS 1
 #endif
 #ifndef STRAGGLAR_DEAD_HINT
 #define STRAGGLAR_DEAD_HINT 1

@@ -52,7 +52,15 @@ VARIANTS_LIFE = {   # round 2: L2 hints by data lifetime (Op::life), dead data e
     "life_ef": ["STRAGGLAR_LIFETIME_HINTS=1", "STRAGGLAR_DEAD_HINT=1"],
     "life_none": ["STRAGGLAR_LIFETIME_HINTS=1", "STRAGGLAR_DEAD_HINT=0"],
 }
-VARIANTS = (VARIANTS_LIFE if "--life" in sys.argv else VARIANTS_HINT3 if "--hint3" in sys.argv else VARIANTS_DEFER if "--defer" in sys.argv else VARIANTS_LL if "--ll" in sys.argv else VARIANTS_LAG if "--lag" in sys.argv
+VARIANTS_TUNE3 = {   # round 2: stage ring / CTA shape again, with sub-slice-major order + lifetime hints
+    "s4_16k": ["STRAGGLAR_STAGES=4", "STRAGGLAR_STAGE_BYTES=16384"],
+    "s3_32k": ["STRAGGLAR_STAGES=3", "STRAGGLAR_STAGE_BYTES=32768"],
+    "s4_12k": ["STRAGGLAR_STAGES=4", "STRAGGLAR_STAGE_BYTES=12288"],
+    "s2_24k": ["STRAGGLAR_STAGES=2", "STRAGGLAR_STAGE_BYTES=24576"],
+    "t512": ["STRAGGLAR_THREADS=512", "STRAGGLAR_MIN_BLOCKS=2"],
+    "nolife": ["STRAGGLAR_LIFETIME_HINTS=0"],
+}
+VARIANTS = (VARIANTS_TUNE3 if "--tune3" in sys.argv else VARIANTS_LIFE if "--life" in sys.argv else VARIANTS_HINT3 if "--hint3" in sys.argv else VARIANTS_DEFER if "--defer" in sys.argv else VARIANTS_LL if "--ll" in sys.argv else VARIANTS_LAG if "--lag" in sys.argv
             else VARIANTS_HINT if ("--hint" in sys.argv or "--hint2" in sys.argv) else VARIANTS_ALL)
 os.makedirs(os.path.join(ROOT, "build", "variants"), exist_ok=True)
 with ThreadPoolExecutor(4) as ex:
