@@ -232,11 +232,14 @@ __device__ __forceinline__ void copy_tail(char* dst, const char* src, int nbytes
 // for the fused exchange every thread adds the two staged operands in shared
 // memory before the stores.  All threads track the per-stage mbarrier parity
 // identically, so the ring persists across the ops of a kernel.
+// 5 x 11 KB (round 2, with the sub-slice-major order and lifetime hints; 4 CTAs
+// per SM still fit): config-2 Phase B 540 -> 513 us, 1 GiB bf16 2158 -> 2037 us
+// vs 3 x 16 KB (profiles/r02/ab/r02ae_*).  Phase A keeps larger stages (kRsStages).
 #ifndef STRAGGLAR_STAGES
-#define STRAGGLAR_STAGES 3
+#define STRAGGLAR_STAGES 5
 #endif
 #ifndef STRAGGLAR_STAGE_BYTES
-#define STRAGGLAR_STAGE_BYTES 16384
+#define STRAGGLAR_STAGE_BYTES 11264
 #endif
 constexpr int kStages = STRAGGLAR_STAGES;
 // Refill lag: 1 = a stage is refilled one iteration after its stores were
@@ -377,33 +380,46 @@ __device__ void tma_add2(Pipe& p, char* d0, char* d1, const char* a, const char*
 // Phase A through shared memory: per stage, the W-1 non-straggler operands of
 // one piece (ascending physical order) are bulk-loaded, summed by the CTA in
 // canonical order into operand slot 0, and bulk-stored to the owner.
+// Phase A cuts the same shared memory into its own, fewer and larger stages
+// (STRAGGLAR_RS_STAGES, barriers 0.. of the ring): a stage holds W-1 operand
+// pieces, and the many small stages that suit the copies (5 x 11 KB) leave it
+// ~1.6 KB per operand (measured: 342 -> 370 us at config 2).  The ring is
+// empty between ops, and each barrier's phase bit is tracked per use, so the
+// two geometries share it.
+#ifndef STRAGGLAR_RS_STAGES
+#define STRAGGLAR_RS_STAGES 3
+#endif
+constexpr int kRsStages = STRAGGLAR_RS_STAGES < kStages ? STRAGGLAR_RS_STAGES : kStages;
+constexpr uint32_t kRsStageBytes = (kStages * kStageBytes / kRsStages) / 16 * 16;
+constexpr int kRsAhead = kRsStages - STRAGGLAR_TMA_LAG;
 template <int DT, int W>
 __device__ void tma_reduce(Pipe& p, char* dst, const char* const (&src)[W - 1], uint64_t lo_b, uint64_t nbytes) {
-  constexpr uint32_t kPiece = (kStageBytes / (W - 1)) / 16 * 16;
+  constexpr uint32_t kPiece = (kRsStageBytes / (W - 1)) / 16 * 16;
+  auto sbuf = [&](int s) { return p.stage + (size_t)s * kRsStageBytes; };
   const uint32_t np = (uint32_t)((nbytes + kPiece - 1) / kPiece);
   auto piece_len = [&](uint32_t i) -> uint32_t {
     const uint64_t off = (uint64_t)i * kPiece;
     return (uint32_t)((nbytes - off) < kPiece ? (nbytes - off) : kPiece);
   };
   auto issue = [&](uint32_t i) {
-    const int s = i % kStages;
+    const int s = i % kRsStages;
     const uint64_t off = lo_b + (uint64_t)i * kPiece;
     const uint32_t len = piece_len(i);
     mbar_expect_tx(&p.bar[s], (W - 1) * len);
 #pragma unroll
-    for (int j = 0; j < W - 1; ++j) bulk_load<false>(p.buf(s) + j * kPiece, src[j] + off, len, &p.bar[s]);
+    for (int j = 0; j < W - 1; ++j) bulk_load<false>(sbuf(s) + j * kPiece, src[j] + off, len, &p.bar[s]);
   };
   if (threadIdx.x == 0 && np) {
     fence_proxy_async_global();
-    for (uint32_t i = 0; i < np && i < (uint32_t)kAhead; ++i) issue(i);
+    for (uint32_t i = 0; i < np && i < (uint32_t)kRsAhead; ++i) issue(i);
   }
   uint32_t ph = p.phase;
   for (uint32_t i = 0; i < np; ++i) {
-    const int s = i % kStages;
+    const int s = i % kRsStages;
     const uint32_t len = piece_len(i);
     mbar_wait(&p.bar[s], (ph >> s) & 1u);
     ph ^= 1u << s;
-    char* base = p.buf(s);
+    char* base = sbuf(s);
     for (uint32_t v = threadIdx.x; v < len / 16; v += blockDim.x) {
       Acc<DT> acc;
       acc.init(reinterpret_cast<const uint4*>(base)[v]);
@@ -416,9 +432,9 @@ __device__ void tma_reduce(Pipe& p, char* dst, const char* const (&src)[W - 1], 
     if (threadIdx.x == 0) {
       bulk_store(dst + lo_b + (uint64_t)i * kPiece, base, len);
       bulk_commit();
-      if (i + kAhead < np) {
+      if (i + kRsAhead < np) {
         ring_release_wait();
-        issue(i + kAhead);
+        issue(i + kRsAhead);
       }
     }
   }

@@ -60,7 +60,21 @@ VARIANTS_TUNE3 = {   # round 2: stage ring / CTA shape again, with sub-slice-maj
     "t512": ["STRAGGLAR_THREADS=512", "STRAGGLAR_MIN_BLOCKS=2"],
     "nolife": ["STRAGGLAR_LIFETIME_HINTS=0"],
 }
-VARIANTS = (VARIANTS_TUNE3 if "--tune3" in sys.argv else VARIANTS_LIFE if "--life" in sys.argv else VARIANTS_HINT3 if "--hint3" in sys.argv else VARIANTS_DEFER if "--defer" in sys.argv else VARIANTS_LL if "--ll" in sys.argv else VARIANTS_LAG if "--lag" in sys.argv
+VARIANTS_TUNE4 = {   # round 2: stage rings around 4 x 12 KB (4 CTAs per SM must still fit)
+    "s4_12k": ["STRAGGLAR_STAGES=4", "STRAGGLAR_STAGE_BYTES=12288"],
+    "s4_13k": ["STRAGGLAR_STAGES=4", "STRAGGLAR_STAGE_BYTES=13312"],
+    "s5_11k": ["STRAGGLAR_STAGES=5", "STRAGGLAR_STAGE_BYTES=11264"],
+    "s5_9k": ["STRAGGLAR_STAGES=5", "STRAGGLAR_STAGE_BYTES=9216"],
+    "s6_8k": ["STRAGGLAR_STAGES=6", "STRAGGLAR_STAGE_BYTES=8192"],
+    "s3_18k": ["STRAGGLAR_STAGES=3", "STRAGGLAR_STAGE_BYTES=18432"],
+}
+VARIANTS_RS = {   # round 2: Phase A's own stage geometry over the 5 x 11 KB ring
+    "s3_16k": ["STRAGGLAR_STAGES=3", "STRAGGLAR_STAGE_BYTES=16384"],
+    "rs5": ["STRAGGLAR_RS_STAGES=5"],
+    "rs2": ["STRAGGLAR_RS_STAGES=2"],
+    "rs4": ["STRAGGLAR_RS_STAGES=4"],
+}
+VARIANTS = (VARIANTS_RS if "--rs" in sys.argv else VARIANTS_TUNE4 if "--tune4" in sys.argv else VARIANTS_TUNE3 if "--tune3" in sys.argv else VARIANTS_LIFE if "--life" in sys.argv else VARIANTS_HINT3 if "--hint3" in sys.argv else VARIANTS_DEFER if "--defer" in sys.argv else VARIANTS_LL if "--ll" in sys.argv else VARIANTS_LAG if "--lag" in sys.argv
             else VARIANTS_HINT if ("--hint" in sys.argv or "--hint2" in sys.argv) else VARIANTS_ALL)
 os.makedirs(os.path.join(ROOT, "build", "variants"), exist_ok=True)
 with ThreadPoolExecutor(4) as ex:
