@@ -370,7 +370,10 @@ def bench_team(args):
     if os.path.exists(prof):
         try:
             tr = json.load(open(prof))
-            if tr.get("workload") == args.workload:
+            from paper_2505_23523_b200.build import device_digest
+
+            # only for the kernels it was captured on (a stale figure would misstate dram_frac)
+            if tr.get("workload") == args.workload and tr.get("device_digest") == device_digest():
                 traffic = tr.get("phase_b_dram_bytes")
         except Exception:
             pass

@@ -411,7 +411,8 @@ int stragglar_allreduce_auto(void* buf, size_t count, int dtype, int op, void* s
  * 131072 at system scope), STRAGGLAR_SUB_MAJOR (1: a CTA runs its units
  * sub-slice by sub-slice — all ops / steps of sub-slice 0, then of 1, … — in
  * Phase B, the Ring and RHD, so forwarded data is re-read while it is still in
- * L2; 0: op by op; must agree across ranks),
+ * L2; 0: op by op; must agree across ranks), STRAGGLAR_BASELINE_SUB_MAJOR (the
+ * same for the Ring and RHD: 1 with GPU-scope flags, 0 at system scope),
  * STRAGGLAR_OP_LANES (Phase-B op lanes per slice at most, 16; 1 = off),
  * STRAGGLAR_LANE_SLICE_MAX (slices may grow to this many bytes to make room
  * for op lanes on small messages, 32768; 0 = off), STRAGGLAR_RS_WHOLE (Phase A

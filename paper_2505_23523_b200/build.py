@@ -35,6 +35,20 @@ def source_digest(defines=()) -> str:
     return h.hexdigest()
 
 
+def device_digest() -> str:
+    """Content hash of the device code (kernels, device primitives, launch plan
+    layout): an ncu DRAM-traffic figure is only valid for the kernels it was
+    captured on (profiles/latest_traffic.json, bench.py)."""
+    import hashlib
+
+    h = hashlib.sha256()
+    for f in sorted(os.listdir(CSRC)):
+        if f.startswith("kernels") or f in ("device.cuh", "plan.h", "schedule.h"):
+            h.update(f.encode())
+            h.update(open(os.path.join(CSRC, f), "rb").read())
+    return h.hexdigest()[:16]
+
+
 def needs_build() -> bool:
     stamp = LIB + ".sha256"
     if not os.path.exists(LIB) or not os.path.exists(stamp):

@@ -50,6 +50,7 @@ struct Layout {
   int32_t world, sigma, G_alloc, sub_max, mover, sys_scope, lanes_max, sub_major;
   uint64_t slice_bytes, sub_bytes, lane_slice_max, e2e_piece_bytes;   // e2e: every rank must cut the same pieces
   uint64_t base_sub_bytes;
+  int32_t base_sub_major, pad2;
 };
 
 struct IpcBlob {          // what travels between processes, per rank
@@ -78,6 +79,7 @@ struct Comm {
   int sub = 1;                 // slices per CTA at most (STRAGGLAR_SUBSLICES)
   uint64_t sub_bytes = 0;      // target slice size on large messages (STRAGGLAR_SUBSLICE_BYTES)
   uint64_t base_sub_bytes = 0; // the same for the Ring / RHD baselines (STRAGGLAR_BASELINE_SUBSLICE_BYTES)
+  int base_sub_major = 1;      // their unit order (STRAGGLAR_BASELINE_SUB_MAJOR)
   int lanes_max = kMaxOps;     // Phase-B op lanes per slice at most (STRAGGLAR_OP_LANES; 1 = off)
   int rs_whole = 1;                 // Phase A over a CTA's sub slices as one range (STRAGGLAR_RS_WHOLE)
   int sub_major = 1;                // unit order of Phase B, Ring, RHD (STRAGGLAR_SUB_MAJOR; plan.h LaunchPlan::sub_major)
@@ -227,6 +229,10 @@ int common_init(Comm& c, int world, int rank, int sigma, bool team) {
   // order, profiles/r02/ab/r02aa_*): Ring 1286 -> 1091 us, RHD 1386 -> 1292 us at
   // 64 KB with GPU-scope flags (config 2); 128 KB at system scope (Ring 1369 vs 1332)
   c.base_sub_bytes = env_u64("STRAGGLAR_BASELINE_SUBSLICE_BYTES", c.sys_scope ? 128 * 1024 : 64 * 1024);
+  // and their own unit order: sub-slice-major helps them with GPU-scope flags
+  // (Ring 1377 -> 1286 us, team config 2) but not per process under MPS (n = 8:
+  // Ring 1082 -> 1278 us, RHD 1013 -> 1317 us, profiles/r02/final/r02f2_*)
+  c.base_sub_major = (int)env_u64("STRAGGLAR_BASELINE_SUB_MAJOR", c.sys_scope ? 0 : 1) ? 1 : 0;
   // Sub-slices (finer hand-offs): team Phase B -3.7 % at gpu scope; at system
   // scope (per process, MPS-shared GPU, round 2) equal or better for T_post
   // (config 2 n = 8: 667-708 vs 715-716 us) and 10 % better for the Ring, once
@@ -292,6 +298,7 @@ Layout layout_of(const Comm& c) {
   l.slice_bytes = c.slice_bytes;
   l.sub_bytes = c.sub_bytes;
   l.base_sub_bytes = c.base_sub_bytes;
+  l.base_sub_major = c.base_sub_major;
   l.e2e_piece_bytes = c.e2e_piece_bytes;
   l.sub_major = c.sub_major;
   return l;
@@ -960,6 +967,7 @@ int stragglar_allreduce_ring(void* buf, size_t count, int dtype, int op, void* s
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
   slices_for(c, P.ce * P.esize, &P.G, &P.sub, true);
+  P.sub_major = c.base_sub_major;
   return launch(K_RING, dtype, P, P.G, stream);
 }
 
@@ -975,6 +983,7 @@ int stragglar_allreduce_rhd(void* buf, size_t count, int dtype, int op, void* st
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
   slices_for(c, P.ce * P.esize, &P.G, &P.sub, true);
+  P.sub_major = c.base_sub_major;
   return launch(K_RHD, dtype, P, P.G, stream);
 }
 
@@ -1560,6 +1569,7 @@ int stragglar_team_allreduce_ring(void* const* bufs, size_t count, int dtype, in
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
   slices_for(c, P.ce * P.esize, &P.G, &P.sub, true);
+  P.sub_major = c.base_sub_major;
   for (int p = 0; p < c.world; ++p) {
     P.buf[p] = (char*)bufs[p];
     P.local_rank[p] = p;
@@ -1579,6 +1589,7 @@ int stragglar_team_allreduce_rhd(void* const* bufs, size_t count, int dtype, int
   P.ce = chunk_elems(count, c.world, P.esize);
   P.nchunks = c.world;
   slices_for(c, P.ce * P.esize, &P.G, &P.sub, true);
+  P.sub_major = c.base_sub_major;
   for (int p = 0; p < c.world; ++p) {
     P.buf[p] = (char*)bufs[p];
     P.local_rank[p] = p;

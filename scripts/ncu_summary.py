@@ -77,8 +77,12 @@ def main():
             name = r["kernel"].replace("(int)", "")
             if ("k_phase<" in name and name.split(">")[0].endswith(", 1")):
                 tr = r["dram__bytes_read.sum"]["value"] + r["dram__bytes_write.sum"]["value"]
+                sys.path.insert(0, ROOT)
+                from paper_2505_23523_b200.build import device_digest
+
                 json.dump({"workload": "config2", "phase_b_dram_bytes": tr, "source": f"profiles/{tag}/ncu_summary.json",
-                           "kernel": r["kernel"]}, open(os.path.join(outdir, "latest_traffic.json"), "w"), indent=1)
+                           "kernel": r["kernel"], "device_digest": device_digest()},
+                          open(os.path.join(outdir, "latest_traffic.json"), "w"), indent=1)
     print(open(os.path.join(d, "ncu_summary.md")).read())
 
 
