@@ -80,6 +80,74 @@ __device__ __forceinline__ void cta_signal(uint32_t* f, uint32_t epoch, bool sys
   if (threadIdx.x == kSignalThread) st_release(f, epoch, sys);
 }
 
+// Signalling warp (Phase B, STRAGGLAR_SIGNALLER): at system scope a unit's
+// release fence costs thread 0 ~2 us (profiles/r02/ab/r02aj_trace_*: a CTA's
+// units move 343 us at system scope vs 270 us at GPU scope, waits unchanged).
+// With the signaller, warp 1 leaves the CTA's barriers for the whole of
+// complete_body and only publishes flags: thread 0 completes a unit's stores,
+// posts the flag to a shared-memory queue (st.release.cta) and goes on; warp 1's
+// lane 0 takes it (ld.acquire.cta), issues the system-scope fence and stores
+// the flag.  Cumulativity carries thread 0's completed stores to the waiter.
+// The other 7 warps synchronise on named barrier 1.
+#ifndef STRAGGLAR_SIGNALLER
+#define STRAGGLAR_SIGNALLER 0
+#endif
+constexpr int kGrp = kThreads - 32;     // threads of the CTA without warp 1
+constexpr int kSigQ = 64;               // queue entries (thread 0 waits if it is full)
+constexpr uint32_t kSigDone = 0xffffffffu;
+__device__ __forceinline__ int grp_tid() { return threadIdx.x < 32 ? (int)threadIdx.x : (int)threadIdx.x - 32; }
+__device__ __forceinline__ void grp_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kGrp) : "memory"); }
+__device__ __forceinline__ int grp_sync_and(int pred) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred a, b;\n\tsetp.ne.s32 a, %1, 0;\n\tbar.red.and.pred b, 1, %2, a;\n\tselp.s32 %0, 1, 0, b;\n}"
+      : "=r"(r)
+      : "r"(pred), "n"(kGrp)
+      : "memory");
+  return r;
+}
+struct SigQ {
+  uint32_t head, tail;   // entries posted by thread 0 / published by the signaller
+  uint32_t e[kSigQ];     // (peer << 24) | flag index in the peer's array
+};
+__device__ __forceinline__ uint32_t ld_acquire_cta_smem(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta_smem(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+// thread 0: queue the flag (its unit's stores have completed: wait_group 0)
+__device__ __forceinline__ void sig_post(SigQ& q, uint32_t entry) {
+  const uint32_t h = q.head;
+  while (h - ld_acquire_cta_smem(&q.tail) >= (uint32_t)kSigQ) {
+  }
+  q.e[h % kSigQ] = entry;
+  st_release_cta_smem(&q.head, h + 1);
+}
+// warp 1, lane 0: publish every queued flag until kSigDone
+__device__ __forceinline__ void sig_loop(SigQ& q, const LaunchPlan& P, uint32_t ep) {
+  uint32_t t = 0;
+  for (;;) {
+    const uint32_t h = ld_acquire_cta_smem(&q.head);
+    for (; t < h; ++t) {
+      const uint32_t e = q.e[t % kSigQ];
+      if (e == kSigDone) return;
+      fence_release(P.sys_scope != 0);
+      st_flag(P.flags[e >> 24] + (e & 0xffffffu), ep, P.sys_scope != 0);
+      st_release_cta_smem(&q.tail, t + 1);
+    }
+  }
+}
+// group versions of cta_wait / cta_wait_range (warp 1 excluded)
+__device__ __forceinline__ bool grp_wait(const uint32_t* f, uint32_t epoch, const LaunchPlan& P, uint32_t where,
+                                         bool local = false) {
+  int ok = 1;
+  if (threadIdx.x == 0) ok = spin_wait(f, epoch, P, where, local ? false : P.sys_scope != 0);
+  return grp_sync_and(ok);
+}
+
 // The call's epoch lives in device memory (state->epoch + 1), so a captured
 // CUDA graph replays correctly.  It is incremented once every CTA of the
 // call's final kernel has read it: thread 0 of each CTA takes a ticket from a
@@ -327,7 +395,7 @@ static __device__ void tma_copy(Pipe& p, char* dst, const char* src, uint64_t nb
 }
 
 // d0 = d1 = a (+) b through shared memory, nbytes a multiple of 16
-template <int DT>
+template <int DT, bool GRP = false>   // GRP: run by the CTA without warp 1 (signalling warp)
 __device__ void tma_add2(Pipe& p, char* d0, char* d1, const char* a, const char* b, uint64_t nbytes,
                          bool ld_keep = true, bool st0_keep = true, bool st1_keep = true) {
   constexpr uint32_t kPiece = kStageBytes / 2;
@@ -356,9 +424,15 @@ __device__ void tma_add2(Pipe& p, char* d0, char* d1, const char* a, const char*
     ph ^= 1u << s;
     uint4* A = reinterpret_cast<uint4*>(p.buf(s));
     const uint4* B = reinterpret_cast<const uint4*>(p.buf(s) + kPiece);
-    for (uint32_t v = threadIdx.x; v < len / 16; v += blockDim.x) A[v] = add_vec<DT>(A[v], B[v]);
-    fence_proxy_async_smem();
-    __syncthreads();
+    if constexpr (GRP) {
+      for (uint32_t v = grp_tid(); v < len / 16; v += kGrp) A[v] = add_vec<DT>(A[v], B[v]);
+      fence_proxy_async_smem();
+      grp_sync();
+    } else {
+      for (uint32_t v = threadIdx.x; v < len / 16; v += blockDim.x) A[v] = add_vec<DT>(A[v], B[v]);
+      fence_proxy_async_smem();
+      __syncthreads();
+    }
     if (threadIdx.x == 0) {
       const uint64_t off = (uint64_t)i * kPiece;
       bulk_store_life(d0 + off, A, len, st0_keep);
@@ -801,6 +875,16 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
     return -1;
   };
   bool ok = true;
+  // signalling warp (STRAGGLAR_SIGNALLER, TMA, one op lane): warp 1 only publishes flags
+  const bool sig = STRAGGLAR_SIGNALLER && tma && lanes == 1;
+  __shared__ SigQ sq;
+  if (sig) {
+    if (threadIdx.x == 0) sq.head = sq.tail = 0;
+    __syncthreads();
+  }
+  if (sig && (threadIdx.x >> 5) == 1) {
+    if (threadIdx.x == 32) sig_loop(sq, P, ep);
+  } else {
   // the CTA's units (op k, sub-slice j): op by op (all sub-slices of an op,
   // then the next op), or with P.sub_major sub-slice by sub-slice
   const int nk = (nops - q + lanes - 1) / lanes;   // this lane's ops: k = q, q + lanes, ...
@@ -825,12 +909,19 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
         if (FUSED && lanes > 1 &&
             !(ok = cta_wait_range(P.flags[me], SLOT_RS_LOCAL, s * lanes, lanes, ep, P, 0x210 | k, true)))
           break;
-        if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, P.fstride, s), ep, P, 0x200 | k))) break;
+        if (!(ok = sig ? grp_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, P.fstride, s), ep, P, 0x200 | k)
+                       : cta_wait(flag_at(P.flags[me], SLOT_ARRIVE + peer, P.fstride, s), ep, P, 0x200 | k)))
+          break;
         if (tr) tr[1] = globaltimer();
         const uint64_t a = sl.lo * P.esize, b = mid * P.esize, body = (b - a) / 16 * 16;
-        if constexpr (tma)
-          tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, body, !kLife,
-                       !kLife || (op.life & LIFE_SELF_REREAD), !kLife || (op.life & LIFE_PEER_REREAD));
+        if constexpr (tma) {
+          if (sig)
+            tma_add2<DT, true>(pipe, mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, body, !kLife,
+                               !kLife || (op.life & LIFE_SELF_REREAD), !kLife || (op.life & LIFE_PEER_REREAD));
+          else
+            tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, body, !kLife,
+                         !kLife || (op.life & LIFE_SELF_REREAD), !kLife || (op.life & LIFE_PEER_REREAD));
+        }
         else
           add2_vecs<DT>(mine + a, P.buf[peer] + a, mine + a, P.buf[peer] + a, body / 16);
         add2_tail<DT>(mine + a + body, P.buf[peer] + a + body, mine + a + body, P.buf[peer] + a + body,
@@ -839,14 +930,20 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
         // straggler: [mid, hi) of c_r; waits for rank r's Phase-A partial
         if (lanes > 1) {   // Phase A of the slice was split over the lanes (rs_body)
           if (!(ok = cta_wait_range(P.flags[me], SLOT_RSDONE + c, s * lanes, lanes, ep, P, 0x300 | k))) break;
-        } else if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, P.fstride, v), ep, P, 0x300 | k))) {
+        } else if (!(ok = sig ? grp_wait(flag_at(P.flags[me], SLOT_RSDONE + c, P.fstride, v), ep, P, 0x300 | k)
+                              : cta_wait(flag_at(P.flags[me], SLOT_RSDONE + c, P.fstride, v), ep, P, 0x300 | k))) {
           break;
         }
         if (tr) tr[1] = globaltimer();
         const uint64_t a = mid * P.esize, b = sl.hi * P.esize, body = (b - a) / 16 * 16;
-        if constexpr (tma)
-          tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, body, !kLife,
-                       !kLife || (op.life & LIFE_SELF_REREAD), !kLife || (op.life & LIFE_PEER_REREAD));
+        if constexpr (tma) {
+          if (sig)
+            tma_add2<DT, true>(pipe, mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, body, !kLife,
+                               !kLife || (op.life & LIFE_SELF_REREAD), !kLife || (op.life & LIFE_PEER_REREAD));
+          else
+            tma_add2<DT>(pipe, mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, body, !kLife,
+                         !kLife || (op.life & LIFE_SELF_REREAD), !kLife || (op.life & LIFE_PEER_REREAD));
+        }
         else
           add2_vecs<DT>(mine + a, P.buf[peer] + a, P.buf[peer] + a, mine + a, body / 16);
         add2_tail<DT>(mine + a + body, P.buf[peer] + a + body, P.buf[peer] + a + body, mine + a + body,
@@ -854,7 +951,9 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
       } else {
         // copy of a fully reduced chunk (push); if this rank computed half of it
         // in an exchange on another lane, that half must have been stored too
-        if (!(ok = cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, P.fstride, v), ep, P, 0x400 | k))) break;
+        if (!(ok = sig ? grp_wait(flag_at(P.flags[me], SLOT_HAVE + c, P.fstride, v), ep, P, 0x400 | k)
+                       : cta_wait(flag_at(P.flags[me], SLOT_HAVE + c, P.fstride, v), ep, P, 0x400 | k)))
+          break;
         if (lanes > 1) {
           const int el = exch_lane(c);
           if (el >= 0 && el != q && !(ok = cta_wait(flag_at(P.flags[me], SLOT_SELF + c, P.fstride, v), ep, P, 0x410 | k, true)))
@@ -869,21 +968,29 @@ __device__ void complete_body(const LaunchPlan& P, Pipe& pipe, int s, int q, int
           copy_vecs(P.buf[peer] + a, mine + a, body / 16);
         copy_tail(P.buf[peer] + a + body, mine + a + body, (int)((b - a) % 16));
       }
-      cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, P.fstride, v), ep, P.sys_scope);
+      if (sig) {
+        grp_sync();   // the tail threads' stores (warp 0) before thread 0's post
+        if (threadIdx.x == 0) sig_post(sq, ((uint32_t)peer << 24) | (uint32_t)((SLOT_HAVE + c) * P.fstride + v));
+      } else {
+        cta_signal(flag_at(P.flags[peer], SLOT_HAVE + c, P.fstride, v), ep, P.sys_scope);
+      }
       if (lanes > 1 && op.kind != OP_SEND && threadIdx.x == kSignalThread)
         st_release(flag_at(P.flags[me], SLOT_SELF + c, P.fstride, v), ep, false);
       if (tr) tr[2] = globaltimer();
     }
   }
+  if (sig && threadIdx.x == 0) sig_post(sq, kSigDone);
   // postcondition: every chunk has landed here (one waiting thread per
   // (chunk, slice) flag, so the acquire loads overlap; lanes split the chunks)
   if (ok) {
     const int nc = (P.nchunks - q + lanes - 1) / lanes;   // chunks c = q, q + lanes, ...
-    if ((int)threadIdx.x < nc * P.sub) {
-      const int c = q + (threadIdx.x / P.sub) * lanes, j = threadIdx.x % P.sub;
+    const int t = sig ? grp_tid() : (int)threadIdx.x;
+    if (t < nc * P.sub) {
+      const int c = q + (t / P.sub) * lanes, j = t % P.sub;
       spin_wait(flag_at(P.flags[me], SLOT_HAVE + c, P.fstride, s * P.sub + j), ep, P, 0x500 | c);
     }
   }
+  }   // not the signalling warp
   __syncthreads();
 }
 

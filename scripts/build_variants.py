@@ -74,7 +74,8 @@ VARIANTS_RS = {   # round 2: Phase A's own stage geometry over the 5 x 11 KB rin
     "rs2": ["STRAGGLAR_RS_STAGES=2"],
     "rs4": ["STRAGGLAR_RS_STAGES=4"],
 }
-VARIANTS = (VARIANTS_RS if "--rs" in sys.argv else VARIANTS_TUNE4 if "--tune4" in sys.argv else VARIANTS_TUNE3 if "--tune3" in sys.argv else VARIANTS_LIFE if "--life" in sys.argv else VARIANTS_HINT3 if "--hint3" in sys.argv else VARIANTS_DEFER if "--defer" in sys.argv else VARIANTS_LL if "--ll" in sys.argv else VARIANTS_LAG if "--lag" in sys.argv
+VARIANTS_SIG = {"sig": ["STRAGGLAR_SIGNALLER=1"]}   # round 2: signalling warp in Phase B
+VARIANTS = (VARIANTS_SIG if "--sig" in sys.argv else VARIANTS_RS if "--rs" in sys.argv else VARIANTS_TUNE4 if "--tune4" in sys.argv else VARIANTS_TUNE3 if "--tune3" in sys.argv else VARIANTS_LIFE if "--life" in sys.argv else VARIANTS_HINT3 if "--hint3" in sys.argv else VARIANTS_DEFER if "--defer" in sys.argv else VARIANTS_LL if "--ll" in sys.argv else VARIANTS_LAG if "--lag" in sys.argv
             else VARIANTS_HINT if ("--hint" in sys.argv or "--hint2" in sys.argv) else VARIANTS_ALL)
 os.makedirs(os.path.join(ROOT, "build", "variants"), exist_ok=True)
 with ThreadPoolExecutor(4) as ex:
