@@ -89,8 +89,11 @@ __device__ __forceinline__ void cta_signal(uint32_t* f, uint32_t epoch, bool sys
 // lane 0 takes it (ld.acquire.cta), issues the system-scope fence and stores
 // the flag.  Cumulativity carries thread 0's completed stores to the waiter.
 // The other 7 warps synchronise on named barrier 1.
+// Measured (profiles/r02/ab/r02ak_*, two repetitions): config-2 Phase B 512 -> 493 us
+// (GPU scope), 526-528 -> 502-508 us (system scope), 1 GiB bf16 at system scope
+// 2125-2133 -> 1918-1930 us; MPS n = 8 654 -> 648 us.
 #ifndef STRAGGLAR_SIGNALLER
-#define STRAGGLAR_SIGNALLER 0
+#define STRAGGLAR_SIGNALLER 1
 #endif
 constexpr int kGrp = kThreads - 32;     // threads of the CTA without warp 1
 constexpr int kSigQ = 64;               // queue entries (thread 0 waits if it is full)
